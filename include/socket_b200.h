@@ -1,0 +1,229 @@
+/*
+ * socket_b200.h -- C ABI of the B200-native SOCKET decode hot path.
+ *
+ * SOCKET (arxiv 2602.06283) scores every cached key by a soft collision of
+ * L SimHash buckets, keeps the top-k keys and runs exact attention over them.
+ * Citations "P:L" are lines of the paper's text.
+ *
+ *   stage                      paper                                  entry point
+ *   key hashing (prefill)      Alg. 1, P:194-209, P:263               socket_hash_keys
+ *   query soft hashing         Alg. 2, P:211-225                      socket_query_tables
+ *   soft-collision scoring     Eq. 4, Alg. 4 P:1485-1506    socket_score
+ *   top-k selection            Alg. 3 l.244, P:686            socket_topk
+ *   sparse flash-decode        Eq. 2 P:169-174, P:271, P:309, P:701   socket_sparse_decode
+ *   LSE combine of partials    (Flash-Decode split merge)      socket_lse_combine
+ *   dense decode (k = n)       Eq. 1 P:16-22                          socket_dense_decode
+ *   sequence-shard resolve     exact global top-k over shards         socket_topk_resolve
+ *
+ * Conventions (all entry points)
+ *  - Every pointer argument is DEVICE memory owned by the caller, except the
+ *    `socket_cfg*` (host).  The library never allocates, frees or copies
+ *    host<->device; temporary storage is the caller's `ws` buffer of at least
+ *    socket_workspace_bytes(cfg, op, k) bytes (16-byte aligned).
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream).  No call synchronizes or reads device data
+ *    on the host.
+ *  - bf16 arrays are passed as `const void*` holding IEEE bfloat16 values.
+ *  - Errors: host-side validation returns SOCKET_EINVAL (null required pointer,
+ *    P not in [1,8], L < 1, d != 128, tau <= 0, k <= 0, sink+window > k,
+ *    H_q % H_kv != 0, N_max not a multiple of 32, bad ranges);
+ *    SOCKET_EUNSUPPORTED for valid but not implemented shapes;
+ *    SOCKET_EWORKSPACE if ws_bytes is too small; SOCKET_ECUDA if a launch
+ *    fails.  The message of the last non-OK status of the calling thread is
+ *    returned by socket_last_error().  Nothing aborts, throws or prints.
+ *  - Data-dependent conditions are not errors: k > #valid keys gives
+ *    cnt = #valid; a row with no valid key gives cnt = 0, a zero output and
+ *    lse = -inf.
+ *  - Determinism: identical inputs give bit-identical outputs (no
+ *    order-dependent atomics; top-k compaction is stable).
+ */
+#ifndef SOCKET_B200_H
+#define SOCKET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SOCKET_ABI_VERSION 1
+
+typedef enum {
+  SOCKET_OK = 0,
+  SOCKET_EINVAL = 1,
+  SOCKET_EUNSUPPORTED = 2,
+  SOCKET_ECUDA = 3,
+  SOCKET_EWORKSPACE = 4
+} socket_status;
+
+/* How query heads of one GQA group share a selection (reading R-14;
+ * the paper is single-query).
+ *  KV_SHARED: one top-k per (b, KV head) from s_g(j) = ||v_j|| * sum_{h in g} w_hat_h(j);
+ *             H_sel = H_kv selection rows; all G = H_q/H_kv query heads attend
+ *             over the same selected rows.
+ *  PER_QHEAD: one top-k per (b, query head) from s_h(j) = ||v_j|| * w_hat_h(j);
+ *             H_sel = H_q selection rows (the paper's literal single-query form). */
+typedef enum { SOCKET_GROUP_KV_SHARED = 0, SOCKET_GROUP_PER_QHEAD = 1 } socket_group_mode;
+
+typedef struct {
+  int32_t B;          /* batch                                                     */
+  int32_t H_q;        /* query heads                                               */
+  int32_t H_kv;       /* key/value heads; H_q % H_kv == 0                          */
+  int32_t d;          /* head dim; must be 128                                     */
+  int32_t N_max;      /* token capacity = row stride of K/V/vnorm/scores; %32 == 0 */
+  int32_t L;          /* hash tables, >= 1 (Alg. 1 "#tables L")                    */
+  int32_t P;          /* hyperplanes per table, 1..8 (Alg. 1 "#hyperplanes P")     */
+  float tau;          /* temperature > 0 (Alg. 2)                                  */
+  float sm_scale;     /* softmax scale on q.k (reading R-2; usually 1/sqrt(d))     */
+  int32_t group_mode; /* socket_group_mode                                         */
+} socket_cfg;
+
+/* ------------------------------------------------------------------------ *
+ * Data layouts (all row-major, innermost last)
+ *   q       [B][H_q][d]            bf16
+ *   K, V    [B][H_kv][N_max][d]    bf16   (256-byte rows for d = 128)
+ *   W       [L][P][d]              bf16   projections W^(l) (Alg. 1 l.201);
+ *                                         one W shared by every b and head
+ *   vnorm   [B][H_kv][N_max]       fp32   ||v_j||_2
+ *   seq_lens[B]                    int32  valid keys are j < seq_lens[b]
+ *   mask    [B][N_max]             uint8  optional; 0 = invalid key (Alg. 4 m_j)
+ *   scores  [B][H_sel][N_max]      fp32   -inf for invalid keys (Alg. 4)
+ *   idx     [B][H_sel][k]          int32  selected keys, ascending; -1 past cnt
+ *   cnt     [B][H_sel]             int32
+ *   out     [B][H_q][d]            bf16
+ *   lse     [B][H_q]               fp32   natural-log sum of exp(sm_scale q.k) over S
+ *   partial [B][H_q][d+2]          fp32   (m, l, o[d]): m = max logit, l = sum e^{z-m},
+ *                                         o = sum e^{z-m} v  (unnormalised)
+ *
+ * Codes (the "index", Alg. 1 output b_j^(l)):  one byte per (key, table), in a
+ * key-tiled, bank-rotated layout chosen for the score kernel:
+ *   Lp  = socket_code_slots(L) = 8, 16, 32, or L rounded up to a multiple of 32
+ *   M   = min(Lp, 32) - 1
+ *   slot s of key j holds the bucket id of table  t(s, j) = (s & ~M) | ((s + j) & M)
+ *   (slots with t >= L are padding and hold 0)
+ *   CB  = min(Lp, 16)  bytes per chunk
+ *   byte offset of (b, h, j, s) =
+ *        ((b*H_kv + h) * N_max) * Lp
+ *      + ((j >> 5) * (Lp / CB) + s / CB) * (32 * CB) + (j & 31) * CB + (s % CB)
+ * Rotating each key's slots by j mod 32 makes the 32 lanes of a warp (lane =
+ * key j mod 32) look up 32 different tables at every step, i.e. 32 different
+ * shared-memory banks.  socket_pack_codes /
+ * socket_unpack_codes convert from / to the plain [B][H_kv][L][N_max] uint8
+ * layout.
+ * ------------------------------------------------------------------------ */
+
+/* Slots per key of the code layout (see above); 0 if L < 1. */
+int32_t socket_code_slots(int32_t L);
+/* Bytes of the codes buffer for cfg: B*H_kv*N_max*socket_code_slots(L). */
+size_t socket_codes_bytes(const socket_cfg* cfg);
+
+/* Workspace requirement of an entry point (op = SOCKET_OP_*), for budget k. */
+enum {
+  SOCKET_OP_HASH = 0,
+  SOCKET_OP_TABLES = 1,
+  SOCKET_OP_SCORE = 2,
+  SOCKET_OP_TOPK = 3,
+  SOCKET_OP_SPARSE_DECODE = 4,
+  SOCKET_OP_DENSE_DECODE = 5,
+  SOCKET_OP_RESOLVE = 6
+};
+size_t socket_workspace_bytes(const socket_cfg* cfg, int32_t op, int32_t k);
+
+/* Alg. 1 PrecomputeKeyHashes, applied to token rows
+ * [n_begin, n_begin + n_count) of every (b, kv head):
+ *   x_{l,i}(j) = sum_t W[l][i][t] * K[b][h][j][t]   (fp32 accumulation)
+ *   bit_i = (x_{l,i} >= 0)        -- sign(0) = +1, reading R-3
+ *   b_j^(l) = sum_i bit_i << i    -- row i = bit i, LSB first, reading R-4
+ * Writes those keys' codes (layout above) and, if V != NULL, vnorm[j] =
+ * sqrt(sum_t V[j][t]^2) (fp32).  The per-step append of a decode step is the
+ * call with n_count = 1.  V == NULL requires vnorm == NULL.
+ * Requires 0 <= n_begin, n_begin + n_count <= N_max. */
+socket_status socket_hash_keys(const socket_cfg* cfg, const void* K, const void* V,
+                               int32_t n_begin, int32_t n_count, const void* W,
+                               uint8_t* codes, float* vnorm, void* stream);
+
+/* Layout converters for codes: plain [B][H_kv][L][N_max] uint8 <-> tiled layout. */
+socket_status socket_pack_codes(const socket_cfg* cfg, const uint8_t* plain, uint8_t* codes,
+                                void* stream);
+socket_status socket_unpack_codes(const socket_cfg* cfg, const uint8_t* codes, uint8_t* plain,
+                                  void* stream);
+
+/* Alg. 2 SoftBucketProbs for every (b, selection row):
+ *   u_{l,i} = tanh(W[l][i] . q) / sqrt(d)
+ *   p_h^(l)(r) = softmax_r(u^(l) . c_r / tau),  c_{r,i} = +1 iff bit i of r (R-5),
+ * evaluated in the exact product form prod_i sigma(2 u_i c_{r,i} / tau).
+ * tables[b][row][l][r] (fp32, R = 2^P) = p_h (PER_QHEAD) or sum_{h in group} p_h
+ * (KV_SHARED). */
+socket_status socket_query_tables(const socket_cfg* cfg, const void* q, const void* W,
+                                  float* tables, void* stream);
+
+/* Eq. 4 + Alg. 4: for every (b, row) and key j < N_max
+ *   w_hat(j) = sum_{l=0}^{L-1} T_row^(l)(b_j^(l))      (T from Alg. 2 as above)
+ *   scores[b][row][j] = vnorm[b][g][j] * w_hat(j)        if j < seq_lens[b] and mask != 0
+ *                     = -inf                             otherwise
+ * (g = kv head of the row).  Computes the tables itself (into ws). */
+socket_status socket_score(const socket_cfg* cfg, const void* q, const void* W,
+                           const uint8_t* codes, const float* vnorm, const int32_t* seq_lens,
+                           const uint8_t* mask, float* scores, void* ws, size_t ws_bytes,
+                           void* stream);
+
+/* Alg. 3 l.244 TopK with forced sink / local window: per (b, row),
+ * with n = seq_lens[b] and valid = (scores != -inf) & (j < n):
+ *   k_eff = min(k, #valid); forced F = valid & (j < sink | n - window <= j < n);
+ *   S = F plus the (k_eff - |F|) best remaining keys under the total order
+ *   (score descending, index ascending) -- ties to the smaller index (R-15).
+ * Writes idx[b][row][0..cnt) ascending, -1 after, cnt[b][row] = k_eff, and if
+ * sel_scores != NULL, sel_scores[b][row][i] = scores[idx[i]] (-inf past cnt).
+ * Requires k <= N_max, sink + window <= k. */
+socket_status socket_topk(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,
+                          int32_t k, int32_t sink, int32_t window, int32_t* idx, int32_t* cnt,
+                          float* sel_scores, void* ws, size_t ws_bytes, void* stream);
+
+/* Eq. 2 with exact logits (reading R-1): for every
+ * (b, query head h) with selection row r(h) (= h // G for KV_SHARED, h for PER_QHEAD)
+ *   z_j = sm_scale * q_h . k_j,  j in S = idx[b][r][0..cnt)
+ *   y = sum_j softmax(z)_j v_j,  lse = log sum_j exp(z_j)
+ * idx rows have stride k.  Writes out (bf16, round-to-nearest) and lse if
+ * non-NULL, and/or the unnormalised partial state (m, l, o) if partial != NULL
+ * (used by sequence sharding; combine with socket_lse_combine). */
+socket_status socket_sparse_decode(const socket_cfg* cfg, const void* q, const void* K,
+                                   const void* V, const int32_t* idx, const int32_t* cnt,
+                                   int32_t k, void* out, float* lse, float* partial, void* ws,
+                                   size_t ws_bytes, void* stream);
+
+/* Merge G partial states (m, l, o) over disjoint key sets (flash-decode split
+ * merge): M = max_s m_s, w_s = e^{m_s - M}, y = sum w_s o_s / sum w_s l_s,
+ * lse = M + log sum w_s l_s.  partials [G][B][H_q][d+2]; all-empty gives y = 0,
+ * lse = -inf. */
+socket_status socket_lse_combine(const socket_cfg* cfg, const float* partials, int32_t G,
+                                 void* out, float* lse, void* stream);
+
+/* Eq. 1 (with sm_scale): dense flash-decode over every key
+ * j < seq_lens[b] of the kv head of each query head; the k = n baseline. */
+socket_status socket_dense_decode(const socket_cfg* cfg, const void* q, const void* K,
+                                  const void* V, const int32_t* seq_lens, void* out, float* lse,
+                                  void* ws, size_t ws_bytes, void* stream);
+
+/* Sequence sharding, exact global top-k.  Shard s of G
+ * owns keys [s*N_shard, (s+1)*N_shard).  Each shard runs socket_topk locally
+ * (k, sel_scores) and the G candidate lists are all-gathered (rank order):
+ *   cand_scores [G][B][H_sel][k] fp32, cand_idx [G][B][H_sel][k] int32 (local ids).
+ * This call selects, per (b, row), the k best candidates over all shards under
+ * (score desc, global index asc) and writes this rank's share:
+ *   idx[b][row][0..cnt) = local indices owned by `rank`, ascending; cnt.
+ * Equal to the single-device top-k of the concatenated rows (sink = window = 0). */
+socket_status socket_topk_resolve(const socket_cfg* cfg, const float* cand_scores,
+                                  const int32_t* cand_idx, int32_t G, int32_t rank, int32_t k,
+                                  int32_t* idx, int32_t* cnt, void* ws, size_t ws_bytes,
+                                  void* stream);
+
+/* Message of the calling thread's last non-OK status ("" if none). */
+const char* socket_last_error(void);
+/* SOCKET_ABI_VERSION of the loaded library. */
+int32_t socket_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOCKET_B200_H */

@@ -185,8 +185,8 @@ def topk_select(s: np.ndarray, k: int, n: int, sink: int = 0, window: int = 0) -
     Returns the selected indices in ascending order (int64).
     """
     N = s.shape[0]
-    valid = ~np.isneginf(s)                                 # -inf = invalid (m_j = 0)
     j = np.arange(N)
+    valid = ~np.isneginf(s) & (j < n)                       # m_j = 0: -inf or past n (Alg. 4)
     forced = valid & ((j < sink) | ((j >= n - window) & (j < n)))
     n_valid = int(valid.sum())
     k_eff = min(k, n_valid)
@@ -306,7 +306,7 @@ def topk_bruteforce(s, k, n, sink=0, window=0):
     the forced set and in which every non-forced member beats every valid
     non-member under (score desc, index asc).  Tiny inputs only."""
     N = len(s)
-    valid = [not (np.isneginf(s[j])) for j in range(N)]
+    valid = [not (np.isneginf(s[j])) and j < n for j in range(N)]
     forced = {j for j in range(N) if valid[j] and (j < sink or n - window <= j < n)}
     k_eff = min(k, sum(valid))
 

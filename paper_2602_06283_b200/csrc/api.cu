@@ -1,0 +1,224 @@
+// extern "C" boundary of libsocket_b200: argument validation, workspace
+// carving, launches.  See include/socket_b200.h for the contract.
+#include <cmath>
+#include <string>
+
+#include "internal.cuh"
+
+namespace sk {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+socket_status fail(socket_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+socket_status check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SOCKET_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return SOCKET_OK;
+}
+
+static socket_status validate(const socket_cfg* c) {
+  if (!c) return fail(SOCKET_EINVAL, "cfg is NULL");
+  if (c->B < 0 || c->H_q < 1 || c->H_kv < 1 || c->N_max < 0)
+    return fail(SOCKET_EINVAL, "B, H_q, H_kv, N_max must be non-negative (heads >= 1)");
+  if (c->H_q % c->H_kv != 0) return fail(SOCKET_EINVAL, "H_q % H_kv != 0");
+  if (c->d != kD) {
+    if (c->d <= 0) return fail(SOCKET_EINVAL, "d must be positive");
+    return fail(SOCKET_EUNSUPPORTED, "only d = 128 is implemented");
+  }
+  if (c->N_max % 32 != 0) return fail(SOCKET_EINVAL, "N_max must be a multiple of 32");
+  if (c->L < 1) return fail(SOCKET_EINVAL, "L must be >= 1");
+  if (c->L > 128) return fail(SOCKET_EUNSUPPORTED, "L > 128 not implemented");
+  if (c->P < 1 || c->P > 16) return fail(SOCKET_EINVAL, "P must be in [1, 16]");
+  if (c->P > 8) return fail(SOCKET_EUNSUPPORTED, "P > 8 (u16 codes) not implemented");
+  if (!(c->tau > 0.f) || !std::isfinite(c->tau)) return fail(SOCKET_EINVAL, "tau must be > 0");
+  if (!std::isfinite(c->sm_scale)) return fail(SOCKET_EINVAL, "sm_scale must be finite");
+  if (c->group_mode != SOCKET_GROUP_KV_SHARED && c->group_mode != SOCKET_GROUP_PER_QHEAD)
+    return fail(SOCKET_EINVAL, "unknown group_mode");
+  return SOCKET_OK;
+}
+
+#define SK_CHECK(x)                   \
+  do {                                \
+    socket_status _s = (x);           \
+    if (_s != SOCKET_OK) return _s;   \
+  } while (0)
+#define SK_NONNULL(p) \
+  if (!(p)) return fail(SOCKET_EINVAL, #p " is NULL")
+
+static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+int32_t socket_version(void) { return SOCKET_ABI_VERSION; }
+
+const char* socket_last_error(void) { return g_last_error.c_str(); }
+
+int32_t socket_code_slots(int32_t L) { return code_slots(L); }
+
+size_t socket_codes_bytes(const socket_cfg* c) {
+  if (!c) return 0;
+  return (size_t)c->B * c->H_kv * c->N_max * code_slots(c->L);
+}
+
+size_t socket_workspace_bytes(const socket_cfg* c, int32_t op, int32_t k) {
+  if (validate(c) != SOCKET_OK) return 0;
+  switch (op) {
+    case SOCKET_OP_SCORE:
+      return align16((size_t)c->B * num_sel_rows(*c) * lut_bytes_per_row(c->L));
+    case SOCKET_OP_SPARSE_DECODE:
+      return align16(decode_workspace_bytes(*c, k > 0 ? k : 1, false));
+    case SOCKET_OP_DENSE_DECODE:
+      return align16(decode_workspace_bytes(*c, 1, true));
+    default:
+      return 0;
+  }
+}
+
+socket_status socket_hash_keys(const socket_cfg* cfg, const void* K, const void* V,
+                               int32_t n_begin, int32_t n_count, const void* W, uint8_t* codes,
+                               float* vnorm, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(K);
+  SK_NONNULL(W);
+  SK_NONNULL(codes);
+  if ((V == nullptr) != (vnorm == nullptr)) return fail(SOCKET_EINVAL, "V and vnorm must both be set or both NULL");
+  if (n_begin < 0 || n_count < 0 || (long long)n_begin + n_count > cfg->N_max)
+    return fail(SOCKET_EINVAL, "bad [n_begin, n_begin + n_count) range");
+  if (cfg->B == 0) return SOCKET_OK;
+  return launch_hash_keys(*cfg, K, V, n_begin, n_count, W, codes, vnorm, S(stream));
+}
+
+socket_status socket_pack_codes(const socket_cfg* cfg, const uint8_t* plain, uint8_t* codes,
+                                void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(plain);
+  SK_NONNULL(codes);
+  return launch_pack_codes(*cfg, plain, codes, false, S(stream));
+}
+
+socket_status socket_unpack_codes(const socket_cfg* cfg, const uint8_t* codes, uint8_t* plain,
+                                  void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(plain);
+  SK_NONNULL(codes);
+  return launch_pack_codes(*cfg, plain, const_cast<uint8_t*>(codes), true, S(stream));
+}
+
+socket_status socket_query_tables(const socket_cfg* cfg, const void* q, const void* W,
+                                  float* tables, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(q);
+  SK_NONNULL(W);
+  SK_NONNULL(tables);
+  if (cfg->B == 0) return SOCKET_OK;
+  return launch_query_tables(*cfg, q, W, tables, nullptr, S(stream));
+}
+
+socket_status socket_score(const socket_cfg* cfg, const void* q, const void* W,
+                           const uint8_t* codes, const float* vnorm, const int32_t* seq_lens,
+                           const uint8_t* mask, float* scores, void* ws, size_t ws_bytes,
+                           void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(q);
+  SK_NONNULL(W);
+  SK_NONNULL(codes);
+  SK_NONNULL(vnorm);
+  SK_NONNULL(seq_lens);
+  SK_NONNULL(scores);
+  const size_t need = socket_workspace_bytes(cfg, SOCKET_OP_SCORE, 0);
+  if (need && (!ws || ws_bytes < need)) return fail(SOCKET_EWORKSPACE, "score: workspace too small");
+  if (cfg->B == 0 || cfg->N_max == 0) return SOCKET_OK;
+  float* lut = static_cast<float*>(ws);
+  SK_CHECK(launch_query_tables(*cfg, q, W, nullptr, lut, S(stream)));
+  return launch_score(*cfg, lut, codes, vnorm, seq_lens, mask, scores, S(stream));
+}
+
+socket_status socket_topk(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,
+                          int32_t k, int32_t sink, int32_t window, int32_t* idx, int32_t* cnt,
+                          float* sel_scores, void* ws, size_t ws_bytes, void* stream) {
+  (void)ws;
+  (void)ws_bytes;
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(scores);
+  SK_NONNULL(seq_lens);
+  SK_NONNULL(idx);
+  SK_NONNULL(cnt);
+  if (k <= 0) return fail(SOCKET_EINVAL, "k must be >= 1");
+  if (k > cfg->N_max) return fail(SOCKET_EINVAL, "k > N_max");
+  if (sink < 0 || window < 0 || (long long)sink + window > k)
+    return fail(SOCKET_EINVAL, "need 0 <= sink, window and sink + window <= k");
+  if (cfg->B == 0) return SOCKET_OK;
+  return launch_topk(*cfg, scores, seq_lens, k, sink, window, idx, cnt, sel_scores, S(stream));
+}
+
+socket_status socket_topk_resolve(const socket_cfg* cfg, const float* cand_scores,
+                                  const int32_t* cand_idx, int32_t G, int32_t rank, int32_t k,
+                                  int32_t* idx, int32_t* cnt, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  (void)ws;
+  (void)ws_bytes;
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(cand_scores);
+  SK_NONNULL(cand_idx);
+  SK_NONNULL(idx);
+  SK_NONNULL(cnt);
+  if (G < 1 || rank < 0 || rank >= G) return fail(SOCKET_EINVAL, "need 0 <= rank < G");
+  if (k <= 0) return fail(SOCKET_EINVAL, "k must be >= 1");
+  if (cfg->B == 0) return SOCKET_OK;
+  return launch_topk_resolve(*cfg, cand_scores, cand_idx, G, rank, k, idx, cnt, S(stream));
+}
+
+socket_status socket_sparse_decode(const socket_cfg* cfg, const void* q, const void* K,
+                                   const void* V, const int32_t* idx, const int32_t* cnt,
+                                   int32_t k, void* out, float* lse, float* partial, void* ws,
+                                   size_t ws_bytes, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(q);
+  SK_NONNULL(K);
+  SK_NONNULL(V);
+  SK_NONNULL(idx);
+  SK_NONNULL(cnt);
+  SK_NONNULL(ws);
+  if (!out && !partial) return fail(SOCKET_EINVAL, "out and partial are both NULL");
+  if (lse && !out) return fail(SOCKET_EINVAL, "lse requires out");
+  if (k <= 0) return fail(SOCKET_EINVAL, "k must be >= 1");
+  if (cfg->B == 0) return SOCKET_OK;
+  return launch_decode(*cfg, q, K, V, idx, cnt, k, nullptr, false, out, lse, partial, ws,
+                       ws_bytes, S(stream));
+}
+
+socket_status socket_dense_decode(const socket_cfg* cfg, const void* q, const void* K,
+                                  const void* V, const int32_t* seq_lens, void* out, float* lse,
+                                  void* ws, size_t ws_bytes, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(q);
+  SK_NONNULL(K);
+  SK_NONNULL(V);
+  SK_NONNULL(seq_lens);
+  SK_NONNULL(out);
+  SK_NONNULL(ws);
+  if (cfg->B == 0) return SOCKET_OK;
+  return launch_decode(*cfg, q, K, V, nullptr, nullptr, 1, seq_lens, true, out, lse, nullptr, ws,
+                       ws_bytes, S(stream));
+}
+
+socket_status socket_lse_combine(const socket_cfg* cfg, const float* partials, int32_t G,
+                                 void* out, float* lse, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(partials);
+  SK_NONNULL(out);
+  if (G < 1) return fail(SOCKET_EINVAL, "G must be >= 1");
+  return launch_lse_combine(*cfg, partials, G, out, lse, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,165 @@
+// Alg. 1 PrecomputeKeyHashes and value norms.
+//
+// Codes are written in the key-tiled, bank-rotated layout documented in
+// include/socket_b200.h.  The tensor-core (tcgen05) projection GEMM for large
+// prefills lives in hash_tc.cu; this file holds the CUDA-core path used for
+// small ranges (the per-step append of a decode step, n_count = 1) and for
+// configurations the tcgen05 kernel does not tile, plus the layout converters.
+#include "internal.cuh"
+
+namespace sk {
+
+// Byte offset of (row-local key j, slot s) inside one (b, kv-head) code region.
+__device__ __forceinline__ size_t code_off(int j, int s, int Lp) {
+  const int CB = Lp < 16 ? Lp : 16;
+  return ((size_t)(j >> 5) * (Lp / CB) + s / CB) * (32 * CB) + (j & 31) * CB + (s % CB);
+}
+// table held by slot s of key j
+__device__ __forceinline__ int slot_table(int s, int j, int Lp) {
+  const int M = (Lp < 32 ? Lp : 32) - 1;
+  return (s & ~M) | ((s + j) & M);
+}
+
+// ----------------------------------------------------------------------------
+// CUDA-core hash: one CTA = one 32-key tile of one (b, kv-head); warp w
+// computes tables l = w, w+8, ... for the 32 keys (lane = key), each table
+// being P dot products of length 128 accumulated in fp32, t ascending.
+// ----------------------------------------------------------------------------
+constexpr int kHashThreads = 256;
+
+__global__ void __launch_bounds__(kHashThreads)
+hash_keys_simt_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict__ W,
+                      uint8_t* __restrict__ codes, int H_kv, int N_max, int L, int P, int Lp,
+                      int n_begin, int n_end) {
+  __shared__ float kt[kD][33];            // K tile transposed: kt[t][key]
+  __shared__ uint8_t cs[32][128 + 4];     // codes of the tile: cs[key][table]  (L <= 128)
+  const int bh = blockIdx.y;
+  const int tile = (n_begin >> 5) + blockIdx.x;
+  const int j0 = tile * 32;
+  const uint16_t* Kb = K + ((size_t)bh * N_max + j0) * kD;
+  for (int i = threadIdx.x; i < 32 * kD; i += kHashThreads) {
+    const int key = i / kD, t = i % kD;
+    kt[t][key] = __uint_as_float((uint32_t)Kb[(size_t)key * kD + t] << 16);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int l = warp; l < L; l += kHashThreads / 32) {
+    uint32_t code = 0;
+    for (int i = 0; i < P; ++i) {
+      const uint16_t* w = W + ((size_t)l * P + i) * kD;
+      float x = 0.f;
+#pragma unroll 8
+      for (int t = 0; t < kD; ++t) x = fmaf(__uint_as_float((uint32_t)w[t] << 16), kt[t][lane], x);
+      code |= (x >= 0.f ? 1u : 0u) << i;   // sign(0) = +1 (R-3); row i -> bit i (R-4)
+    }
+    cs[lane][l] = (uint8_t)code;
+  }
+  __syncthreads();
+  // write: thread = (key, chunk); CB contiguous bytes per (key, chunk)
+  const int CB = Lp < 16 ? Lp : 16;
+  const int nch = Lp / CB;
+  uint8_t* cb = codes + (size_t)bh * N_max * Lp;
+  for (int i = threadIdx.x; i < 32 * nch; i += kHashThreads) {
+    const int key = i & 31, ch = i >> 5;
+    const int j = j0 + key;
+    if (j < n_begin || j >= n_end) continue;
+    uint8_t buf[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      if (e < CB) {
+        const int s = ch * CB + e;
+        const int t = slot_table(s, j, Lp);
+        buf[e] = t < L ? cs[key][t] : 0;
+      }
+    }
+    uint8_t* dst = cb + code_off(j, ch * CB, Lp);
+    if (CB == 16) {
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(buf);
+    } else {
+      *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(buf);
+    }
+  }
+}
+
+// ||v_j||_2: one warp per row, lane sums 4 elements, fixed butterfly order.
+__global__ void vnorm_kernel(const uint16_t* __restrict__ V, float* __restrict__ vnorm,
+                             int N_max, int n_begin, int n_count, int rows_total) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows_total) return;
+  const int bh = warp / n_count, j = n_begin + warp % n_count;
+  const uint2 u = *reinterpret_cast<const uint2*>(V + ((size_t)bh * N_max + j) * kD + lane * 4);
+  float a = bf16lo(u.x), b = bf16hi(u.x), c = bf16lo(u.y), e = bf16hi(u.y);
+  float s = fmaf(a, a, fmaf(b, b, fmaf(c, c, e * e)));
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) vnorm[(size_t)bh * N_max + j] = sqrtf(s);
+}
+
+// plain [bh][L][N_max] <-> tiled layout; one thread per (bh, j, slot)
+__global__ void pack_codes_kernel(const uint8_t* __restrict__ plain, uint8_t* __restrict__ codes,
+                                  int N_max, int L, int Lp, long long total, bool unpack) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int s = (int)(i % Lp);
+  const long long r = i / Lp;
+  const int j = (int)(r % N_max);
+  const long long bh = r / N_max;
+  const int t = slot_table(s, j, Lp);
+  uint8_t* cdst = codes + bh * (long long)N_max * Lp + code_off(j, s, Lp);
+  if (!unpack) {
+    *cdst = t < L ? plain[(bh * L + t) * N_max + j] : 0;
+  } else if (t < L) {
+    const_cast<uint8_t*>(plain)[(bh * L + t) * N_max + j] = *cdst;
+  }
+}
+
+socket_status launch_hash_keys_simt(const socket_cfg& c, const void* K, const void* W,
+                                    uint8_t* codes, int n_begin, int n_count, cudaStream_t st) {
+  const int Lp = code_slots(c.L);
+  const int t0 = n_begin >> 5, t1 = (n_begin + n_count - 1) >> 5;
+  dim3 grid(t1 - t0 + 1, c.B * c.H_kv);
+  hash_keys_simt_kernel<<<grid, kHashThreads, 0, st>>>(
+      (const uint16_t*)K, (const uint16_t*)W, codes, c.H_kv, c.N_max, c.L, c.P, Lp, n_begin,
+      n_begin + n_count);
+  return check_launch("hash_keys_simt_kernel");
+}
+
+socket_status launch_hash_keys_tc(const socket_cfg& c, const void* K, const void* W,
+                                  uint8_t* codes, int n_begin, int n_count, cudaStream_t st,
+                                  bool* used);
+
+socket_status launch_hash_keys(const socket_cfg& c, const void* K, const void* V, int n_begin,
+                               int n_count, const void* W, uint8_t* codes, float* vnorm,
+                               cudaStream_t st) {
+  if (n_count == 0) return SOCKET_OK;
+  bool used = false;
+  socket_status s = launch_hash_keys_tc(c, K, W, codes, n_begin, n_count, st, &used);
+  if (s != SOCKET_OK) return s;
+  if (!used) {
+    s = launch_hash_keys_simt(c, K, W, codes, n_begin, n_count, st);
+    if (s != SOCKET_OK) return s;
+  }
+  if (V) {
+    const int rows = c.B * c.H_kv * n_count;
+    const int threads = 256;
+    const int blocks = (int)(((long long)rows * 32 + threads - 1) / threads);
+    vnorm_kernel<<<blocks, threads, 0, st>>>((const uint16_t*)V, vnorm, c.N_max, n_begin, n_count,
+                                             rows);
+    s = check_launch("vnorm_kernel");
+  }
+  return s;
+}
+
+socket_status launch_pack_codes(const socket_cfg& c, const uint8_t* plain, uint8_t* codes,
+                                bool unpack, cudaStream_t st) {
+  const int Lp = code_slots(c.L);
+  const long long total = (long long)c.B * c.H_kv * c.N_max * Lp;
+  if (total == 0) return SOCKET_OK;
+  const int threads = 256;
+  pack_codes_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0, st>>>(
+      plain, codes, c.N_max, c.L, Lp, total, unpack);
+  return check_launch("pack_codes_kernel");
+}
+
+}  // namespace sk

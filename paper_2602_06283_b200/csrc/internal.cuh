@@ -1,0 +1,115 @@
+// Internal helpers of libsocket_b200 (sm_100a).  Not part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/socket_b200.h"
+
+namespace sk {
+
+// ----------------------------------------------------------------------------
+// error reporting (thread-local last error; the C ABI never throws)
+// ----------------------------------------------------------------------------
+void set_error(const std::string& msg);
+socket_status fail(socket_status st, const std::string& msg);
+socket_status check_launch(const char* what);
+
+constexpr int kD = 128;           // head dim supported by every kernel
+constexpr int kNumSMs = 148;      // B200
+constexpr int kLutPanelCols = 64; // LUT row = 64 fp32 columns = 256 B
+constexpr int kLutRows = 256;     // 2^P rows for P <= 8
+
+inline int code_slots(int L) {
+  if (L < 1) return 0;
+  if (L <= 8) return 8;
+  if (L <= 16) return 16;
+  if (L <= 32) return 32;
+  return (L + 31) / 32 * 32;
+}
+inline int lut_panels(int Lp) { return Lp <= 64 ? 1 : (Lp + 63) / 64; }
+inline int num_sel_rows(const socket_cfg& c) {
+  return c.group_mode == SOCKET_GROUP_PER_QHEAD ? c.H_q : c.H_kv;
+}
+inline size_t lut_bytes_per_row(int L) {
+  return (size_t)lut_panels(code_slots(L)) * kLutRows * kLutPanelCols * sizeof(float);
+}
+
+// ----------------------------------------------------------------------------
+// launchers (defined in the kernel .cu files)
+// ----------------------------------------------------------------------------
+socket_status launch_hash_keys(const socket_cfg& c, const void* K, const void* V, int n_begin,
+                               int n_count, const void* W, uint8_t* codes, float* vnorm,
+                               cudaStream_t st);
+socket_status launch_pack_codes(const socket_cfg& c, const uint8_t* plain, uint8_t* codes,
+                                bool unpack, cudaStream_t st);
+socket_status launch_query_tables(const socket_cfg& c, const void* q, const void* W,
+                                  float* tables_plain, float* lut, cudaStream_t st);
+socket_status launch_score(const socket_cfg& c, const float* lut, const uint8_t* codes,
+                           const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
+                           float* scores, cudaStream_t st);
+socket_status launch_topk(const socket_cfg& c, const float* scores, const int32_t* seq_lens,
+                          int k, int sink, int window, int32_t* idx, int32_t* cnt,
+                          float* sel_scores, cudaStream_t st);
+socket_status launch_topk_resolve(const socket_cfg& c, const float* cand_scores,
+                                  const int32_t* cand_idx, int G, int rank, int k, int32_t* idx,
+                                  int32_t* cnt, cudaStream_t st);
+size_t decode_workspace_bytes(const socket_cfg& c, int k, bool dense);
+socket_status launch_decode(const socket_cfg& c, const void* q, const void* K, const void* V,
+                            const int32_t* idx, const int32_t* cnt, int k,
+                            const int32_t* seq_lens, bool dense, void* out, float* lse,
+                            float* partial, void* ws, size_t ws_bytes, cudaStream_t st);
+socket_status launch_lse_combine(const socket_cfg& c, const float* partials, int G,
+                                 void* out, float* lse, cudaStream_t st);
+
+}  // namespace sk
+
+// ----------------------------------------------------------------------------
+// device helpers
+// ----------------------------------------------------------------------------
+#ifdef __CUDACC__
+namespace sk {
+
+__device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
+
+// round-to-nearest-even fp32 -> bf16 bits (finite inputs)
+__device__ __forceinline__ uint32_t f2bf_bits(float f) {
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7F800000u) == 0x7F800000u) return (u >> 16) | ((u & 0xFFFFu) ? 0x40u : 0u);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return u >> 16;
+}
+
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg_nc_v2(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p));
+  return r;
+}
+
+// monotone map fp32 -> u32 (larger float <=> larger key)
+__device__ __forceinline__ uint32_t f2key(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+}  // namespace sk
+#endif

@@ -1,0 +1,224 @@
+"""Thin torch-facing wrappers over the C ABI (include/socket_b200.h).
+
+Marshalling only: each function validates tensor dtypes/shapes/devices,
+allocates outputs and workspaces with torch (PyTorch = device memory and
+streams), and calls the library on the current CUDA stream.  Every step of
+the SOCKET path runs in the library's sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import SocketCfg, check, lib
+
+KV_SHARED = _lib.GROUP_KV_SHARED
+PER_QHEAD = _lib.GROUP_PER_QHEAD
+
+
+@dataclass(frozen=True)
+class Config:
+    """Mirror of socket_cfg (see include/socket_b200.h)."""
+    B: int
+    H_q: int
+    H_kv: int
+    N_max: int
+    L: int = 60            # Table 6 default
+    P: int = 8
+    tau: float = 0.5
+    sm_scale: float | None = None   # default 1/sqrt(d) (reading R-2)
+    group_mode: int = KV_SHARED
+    d: int = 128
+
+    def c(self) -> SocketCfg:
+        s = self.sm_scale if self.sm_scale is not None else 1.0 / math.sqrt(self.d)
+        return SocketCfg(self.B, self.H_q, self.H_kv, self.d, self.N_max, self.L, self.P,
+                         float(self.tau), float(s), int(self.group_mode))
+
+    @property
+    def H_sel(self) -> int:
+        return self.H_q if self.group_mode == PER_QHEAD else self.H_kv
+
+    @property
+    def code_slots(self) -> int:
+        return int(lib().socket_code_slots(self.L))
+
+    @property
+    def scale(self) -> float:
+        return self.sm_scale if self.sm_scale is not None else 1.0 / math.sqrt(self.d)
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(t):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _need(t, dtype, shape, name):
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name}: must be a contiguous CUDA tensor")
+
+
+def workspace_bytes(cfg: Config, op: int, k: int = 1) -> int:
+    c = cfg.c()
+    return int(lib().socket_workspace_bytes(ctypes.byref(c), op, k))
+
+
+def workspace(cfg: Config, op: int, k: int, device) -> torch.Tensor:
+    n = max(16, workspace_bytes(cfg, op, k))
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def codes_bytes(cfg: Config) -> int:
+    c = cfg.c()
+    return int(lib().socket_codes_bytes(ctypes.byref(c)))
+
+
+def alloc_codes(cfg: Config, device) -> torch.Tensor:
+    return torch.zeros(codes_bytes(cfg), dtype=torch.uint8, device=device)
+
+
+# ---------------------------------------------------------------------------
+def hash_keys(cfg: Config, K, W, codes, V=None, vnorm=None, n_begin: int = 0, n_count=None):
+    """Alg. 1 on rows [n_begin, n_begin+n_count) of every (b, kv head)."""
+    n_count = cfg.N_max - n_begin if n_count is None else n_count
+    _need(K, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.N_max, cfg.d), "K")
+    _need(W, torch.bfloat16, (cfg.L, cfg.P, cfg.d), "W")
+    _need(codes, torch.uint8, (codes_bytes(cfg),), "codes")
+    if V is not None:
+        _need(V, torch.bfloat16, K.shape, "V")
+        _need(vnorm, torch.float32, (cfg.B, cfg.H_kv, cfg.N_max), "vnorm")
+    c = cfg.c()
+    check(lib().socket_hash_keys(ctypes.byref(c), _p(K), _p(V), n_begin, n_count, _p(W),
+                                 _p(codes), _p(vnorm), _stream(K)))
+    return codes
+
+
+def pack_codes(cfg: Config, plain):
+    _need(plain, torch.uint8, (cfg.B, cfg.H_kv, cfg.L, cfg.N_max), "plain codes")
+    codes = alloc_codes(cfg, plain.device)
+    c = cfg.c()
+    check(lib().socket_pack_codes(ctypes.byref(c), _p(plain), _p(codes), _stream(plain)))
+    return codes
+
+
+def unpack_codes(cfg: Config, codes):
+    _need(codes, torch.uint8, (codes_bytes(cfg),), "codes")
+    plain = torch.zeros((cfg.B, cfg.H_kv, cfg.L, cfg.N_max), dtype=torch.uint8, device=codes.device)
+    c = cfg.c()
+    check(lib().socket_unpack_codes(ctypes.byref(c), _p(codes), _p(plain), _stream(codes)))
+    return plain
+
+
+def query_tables(cfg: Config, q, W):
+    """Alg. 2 tables [B][H_sel][L][2^P] (group-summed in KV_SHARED mode)."""
+    _need(q, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "q")
+    _need(W, torch.bfloat16, (cfg.L, cfg.P, cfg.d), "W")
+    t = torch.empty((cfg.B, cfg.H_sel, cfg.L, 1 << cfg.P), dtype=torch.float32, device=q.device)
+    c = cfg.c()
+    check(lib().socket_query_tables(ctypes.byref(c), _p(q), _p(W), _p(t), _stream(q)))
+    return t
+
+
+def score(cfg: Config, q, W, codes, vnorm, seq_lens, mask=None, out=None, ws=None):
+    """Eq. 4 + Alg. 4 scores [B][H_sel][N_max] (fp32, -inf for invalid keys)."""
+    _need(q, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "q")
+    _need(seq_lens, torch.int32, (cfg.B,), "seq_lens")
+    if mask is not None:
+        _need(mask, torch.uint8, (cfg.B, cfg.N_max), "mask")
+    if out is None:
+        out = torch.empty((cfg.B, cfg.H_sel, cfg.N_max), dtype=torch.float32, device=q.device)
+    if ws is None:
+        ws = workspace(cfg, _lib.OP_SCORE, 1, q.device)
+    c = cfg.c()
+    check(lib().socket_score(ctypes.byref(c), _p(q), _p(W), _p(codes), _p(vnorm), _p(seq_lens),
+                             _p(mask), _p(out), _p(ws), ws.numel(), _stream(q)))
+    return out
+
+
+def topk(cfg: Config, scores, seq_lens, k: int, sink: int = 0, window: int = 0,
+         idx=None, cnt=None, sel_scores=None, want_scores: bool = False):
+    """Alg. 3 l.244 TopK: idx [B][H_sel][k] ascending (-1 past cnt), cnt [B][H_sel]."""
+    _need(scores, torch.float32, (cfg.B, cfg.H_sel, cfg.N_max), "scores")
+    dev = scores.device
+    if idx is None:
+        idx = torch.empty((cfg.B, cfg.H_sel, k), dtype=torch.int32, device=dev)
+    if cnt is None:
+        cnt = torch.empty((cfg.B, cfg.H_sel), dtype=torch.int32, device=dev)
+    if want_scores and sel_scores is None:
+        sel_scores = torch.empty((cfg.B, cfg.H_sel, k), dtype=torch.float32, device=dev)
+    c = cfg.c()
+    check(lib().socket_topk(ctypes.byref(c), _p(scores), _p(seq_lens), k, sink, window, _p(idx),
+                            _p(cnt), _p(sel_scores), None, 0, _stream(scores)))
+    return (idx, cnt, sel_scores) if want_scores else (idx, cnt)
+
+
+def sparse_decode(cfg: Config, q, K, V, idx, cnt, k: int, out=None, lse=None, partial=None,
+                  ws=None, want_out: bool = True):
+    """Eq. 2 exact attention over the selected rows; out bf16 [B][H_q][d], lse fp32."""
+    dev = q.device
+    if want_out and out is None:
+        out = torch.empty((cfg.B, cfg.H_q, cfg.d), dtype=torch.bfloat16, device=dev)
+        lse = torch.empty((cfg.B, cfg.H_q), dtype=torch.float32, device=dev) if lse is None else lse
+    if ws is None:
+        ws = workspace(cfg, _lib.OP_SPARSE_DECODE, k, dev)
+    c = cfg.c()
+    check(lib().socket_sparse_decode(ctypes.byref(c), _p(q), _p(K), _p(V), _p(idx), _p(cnt), k,
+                                     _p(out), _p(lse), _p(partial), _p(ws), ws.numel(), _stream(q)))
+    return out, lse
+
+
+def dense_decode(cfg: Config, q, K, V, seq_lens, out=None, lse=None, ws=None):
+    """Eq. 1 dense flash-decode over j < seq_lens[b] (the k = n baseline)."""
+    dev = q.device
+    if out is None:
+        out = torch.empty((cfg.B, cfg.H_q, cfg.d), dtype=torch.bfloat16, device=dev)
+    if lse is None:
+        lse = torch.empty((cfg.B, cfg.H_q), dtype=torch.float32, device=dev)
+    if ws is None:
+        ws = workspace(cfg, _lib.OP_DENSE_DECODE, 1, dev)
+    c = cfg.c()
+    check(lib().socket_dense_decode(ctypes.byref(c), _p(q), _p(K), _p(V), _p(seq_lens), _p(out),
+                                    _p(lse), _p(ws), ws.numel(), _stream(q)))
+    return out, lse
+
+
+def lse_combine(cfg: Config, partials, out=None, lse=None):
+    """Merge G partial states [G][B][H_q][d+2] -> out bf16, lse."""
+    G = partials.shape[0]
+    _need(partials, torch.float32, (G, cfg.B, cfg.H_q, cfg.d + 2), "partials")
+    dev = partials.device
+    if out is None:
+        out = torch.empty((cfg.B, cfg.H_q, cfg.d), dtype=torch.bfloat16, device=dev)
+    if lse is None:
+        lse = torch.empty((cfg.B, cfg.H_q), dtype=torch.float32, device=dev)
+    c = cfg.c()
+    check(lib().socket_lse_combine(ctypes.byref(c), _p(partials), G, _p(out), _p(lse),
+                                   _stream(partials)))
+    return out, lse
+
+
+def topk_resolve(cfg: Config, cand_scores, cand_idx, rank: int, k: int, idx=None, cnt=None):
+    """Exact global top-k share of `rank` from all-gathered shard candidates."""
+    G = cand_scores.shape[0]
+    _need(cand_scores, torch.float32, (G, cfg.B, cfg.H_sel, k), "cand_scores")
+    _need(cand_idx, torch.int32, (G, cfg.B, cfg.H_sel, k), "cand_idx")
+    dev = cand_scores.device
+    if idx is None:
+        idx = torch.empty((cfg.B, cfg.H_sel, k), dtype=torch.int32, device=dev)
+    if cnt is None:
+        cnt = torch.empty((cfg.B, cfg.H_sel), dtype=torch.int32, device=dev)
+    c = cfg.c()
+    check(lib().socket_topk_resolve(ctypes.byref(c), _p(cand_scores), _p(cand_idx), G, rank, k,
+                                    _p(idx), _p(cnt), None, 0, _stream(cand_scores)))
+    return idx, cnt

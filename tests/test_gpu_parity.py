@@ -1,0 +1,362 @@
+"""GPU parity: every stage of the CUDA path (through the C ABI) against the
+float64 oracle on identical seeded inputs.  Tolerances are the north star's
+(BASELINE.json) and DESIGN.md "Numerics":
+  codes   bit-exact except bits whose oracle margin < 1e-5 (logged)
+  tables  <= 2e-6 relative
+  scores  <= 1e-5 relative (fp32 vs float64)
+  top-k   identical when both sides select from the same fp32 scores;
+          vs float64 scores: symmetric difference only at documented near-ties
+  output  <= 2e-3 absolute (bf16), lse <= 1e-3 absolute
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle as O
+from helpers import bits_to_dev, rel_err
+
+pytestmark = pytest.mark.gpu
+
+ops = pytest.importorskip("paper_2602_06283_b200.ops")
+from paper_2602_06283_b200 import Config, KV_SHARED, PER_QHEAD, SocketDecoder  # noqa: E402
+
+DEV = "cuda"
+
+
+def make(B, H_q, H_kv, N, L, P, seed=0, seq_lens=None, variant="gauss", tau=0.5, mode=KV_SHARED,
+         n_needle=0):
+    c = datagen.make_case(B, H_q, H_kv, N, 128, seed, variant=variant, seq_lens=seq_lens,
+                          n_needle=n_needle)
+    W = datagen.make_projections(1000 + seed, L, P, 128)
+    cfg = Config(B=B, H_q=H_q, H_kv=H_kv, N_max=N, L=L, P=P, tau=tau, group_mode=mode)
+    dev = dict(q=bits_to_dev(c["q"]), K=bits_to_dev(c["K"]), V=bits_to_dev(c["V"]),
+               W=bits_to_dev(W), seq_lens=torch.from_numpy(c["seq_lens"]).to(DEV))
+    return cfg, c, W, dev
+
+
+# ---------------------------------------------------------------------------
+# Alg. 1 codes and norms
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("B,H,N,L,P", [(1, 1, 4096, 16, 8), (2, 2, 1024, 60, 8), (1, 2, 512, 8, 4),
+                                       (1, 1, 256, 64, 8), (1, 1, 256, 3, 2), (1, 1, 128, 100, 8),
+                                       (2, 1, 96, 33, 7), (1, 3, 64, 128, 8)])
+def test_codes_bit_exact(B, H, N, L, P):
+    cfg, c, W, d = make(B, H, H, N, L, P, seed=L + P)
+    codes = ops.alloc_codes(cfg, DEV)
+    vnorm = torch.zeros((B, H, N), dtype=torch.float32, device=DEV)
+    ops.hash_keys(cfg, d["K"], d["W"], codes, V=d["V"], vnorm=vnorm)
+    got = ops.unpack_codes(cfg, codes).cpu().numpy().astype(np.int64)
+    ref, margin = O.hash_keys(O.widen(c["K"]), O.widen(W))
+    diff = got != ref
+    if diff.any():
+        # a flipped code must be explained by a near-zero projection of that key/table
+        bi, hi, li, ji = np.nonzero(diff)
+        for b, h, l, j in zip(bi, hi, li, ji):
+            flipped = (got[b, h, l, j] ^ ref[b, h, l, j])
+            for i in range(P):
+                if flipped >> i & 1:
+                    assert margin[b, h, l, i, j] < 1e-5, (b, h, l, j, i, margin[b, h, l, i, j])
+        print(f"logged {int(diff.sum())} near-zero-margin code flips")
+    assert diff.sum() <= max(2, diff.size // 100000)
+    vn_ref = O.value_norms(O.widen(c["V"]))
+    assert np.max(rel_err(vnorm.cpu().numpy(), vn_ref)) < 1e-6
+
+
+def test_hash_partial_ranges_touch_only_their_rows():
+    cfg, c, W, d = make(1, 2, 2, 256, 16, 8, seed=5)
+    codes = ops.alloc_codes(cfg, DEV)
+    ref, _ = O.hash_keys(O.widen(c["K"]), O.widen(W))
+    ops.hash_keys(cfg, d["K"], d["W"], codes, n_begin=37, n_count=1)    # append-style
+    ops.hash_keys(cfg, d["K"], d["W"], codes, n_begin=100, n_count=61)  # ragged range
+    got = ops.unpack_codes(cfg, codes).cpu().numpy().astype(np.int64)
+    inside = np.zeros(256, bool)
+    inside[37] = True
+    inside[100:161] = True
+    assert np.array_equal(got[..., inside], ref[..., inside])
+    assert np.all(got[..., ~inside] == 0)
+
+
+def test_pack_unpack_roundtrip():
+    for L in (3, 16, 60, 100):
+        cfg = Config(B=2, H_q=2, H_kv=2, N_max=96, L=L, P=8)
+        plain = torch.randint(0, 256, (2, 2, L, 96), dtype=torch.uint8, device=DEV)
+        assert torch.equal(ops.unpack_codes(cfg, ops.pack_codes(cfg, plain)), plain)
+
+
+# ---------------------------------------------------------------------------
+# Alg. 2 tables
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("P,mode,tau", [(8, KV_SHARED, 0.5), (8, PER_QHEAD, 0.3), (4, KV_SHARED, 0.7),
+                                        (1, PER_QHEAD, 0.5), (8, KV_SHARED, 0.05)])
+def test_tables(P, mode, tau):
+    cfg, c, W, d = make(2, 8, 2, 64, 60, P, seed=P, tau=tau, mode=mode)
+    got = ops.query_tables(cfg, d["q"], d["W"]).cpu().numpy()
+    ref = O.selection_tables(O.widen(c["q"]), O.widen(W), tau, 2, mode)
+    assert got.shape == ref.shape
+    assert np.max(rel_err(got, ref)) < 2e-6
+
+
+# ---------------------------------------------------------------------------
+# Eq. 4 / Alg. 4 scores
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("L,mode,lens", [(16, KV_SHARED, [4096]), (60, KV_SHARED, [3000, 4096]),
+                                         (60, PER_QHEAD, [2500, 17]), (8, KV_SHARED, [4096, 0]),
+                                         (64, KV_SHARED, [4090]), (128, PER_QHEAD, [1000])])
+def test_scores(L, mode, lens):
+    B = len(lens)
+    cfg, c, W, d = make(B, 8, 2, 4096, L, 8, seed=L, seq_lens=lens, mode=mode)
+    codes_ref, _ = O.hash_keys(O.widen(c["K"]), O.widen(W))
+    codes = ops.pack_codes(cfg, torch.from_numpy(codes_ref.astype(np.uint8)).to(DEV))
+    vn_ref = O.value_norms(O.widen(c["V"]))
+    vnorm = torch.from_numpy(vn_ref.astype(np.float32)).to(DEV)
+    mask = torch.ones((B, 4096), dtype=torch.uint8, device=DEV)
+    mask[:, 7::97] = 0
+    got = ops.score(cfg, d["q"], d["W"], codes, vnorm, d["seq_lens"], mask=mask).cpu().numpy()
+    T = O.selection_tables(O.widen(c["q"]), O.widen(W), 0.5, 2, mode)
+    G = 4
+    for b in range(B):
+        for r in range(cfg.H_sel):
+            g = r if mode == KV_SHARED else r // G
+            w = O.soft_scores(T[b, r], codes_ref[b, g])
+            s = O.masked_value_scores(w, vn_ref[b, g].astype(np.float32).astype(np.float64),
+                                      lens[b], mask[b].cpu().numpy())
+            fin = np.isfinite(s)
+            assert np.array_equal(np.isfinite(got[b, r]), fin)
+            assert np.all(np.isneginf(got[b, r][~fin]))
+            if fin.any():
+                assert np.max(rel_err(got[b, r][fin], s[fin])) <= 1e-5
+
+
+# ---------------------------------------------------------------------------
+# Top-k
+# ---------------------------------------------------------------------------
+def _check_topk_same_scores(cfg, scores, lens, k, sink=0, window=0):
+    idx, cnt = ops.topk(cfg, scores, torch.tensor(lens, dtype=torch.int32, device=DEV), k, sink, window)
+    s = scores.cpu().numpy().astype(np.float64)
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    for b in range(cfg.B):
+        for r in range(cfg.H_sel):
+            ref = O.topk_select(s[b, r], k, lens[b], sink, window)
+            assert cnt[b, r] == len(ref)
+            assert np.array_equal(idx[b, r, :cnt[b, r]], ref)
+            assert np.all(idx[b, r, cnt[b, r]:] == -1)
+
+
+@pytest.mark.parametrize("N,k,lens,sink,window", [
+    (4096, 512, [4096], 0, 0), (4096, 512, [4096, 3001], 16, 32), (32768, 3277, [32768], 0, 0),
+    (1024, 1024, [1024, 700], 0, 0), (256, 100, [0, 50, 256], 0, 0), (131072, 13107, [131072], 0, 0),
+    (2048, 7, [2048], 3, 4),
+])
+def test_topk_identical_on_same_scores(N, k, lens, sink, window):
+    B = len(lens)
+    cfg = Config(B=B, H_q=8, H_kv=2, N_max=N, L=16, P=8)
+    g = torch.Generator(device=DEV).manual_seed(N + k)
+    scores = torch.rand((B, 2, N), generator=g, device=DEV)
+    for b, n in enumerate(lens):
+        scores[b, :, n:] = -math.inf
+    scores[:, :, 5::13] = -math.inf                        # masked keys
+    _check_topk_same_scores(cfg, scores, lens, k, sink, window)
+
+
+def test_topk_heavy_ties():
+    """Massive exact ties (scores in {0, .25, .5, .75}): ties go to smaller index."""
+    cfg = Config(B=2, H_q=4, H_kv=4, N_max=8192, L=16, P=8)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    scores = (torch.randint(0, 4, (2, 4, 8192), generator=g, device=DEV).float() / 4)
+    _check_topk_same_scores(cfg, scores, [8192, 5000], 1500)
+    scores = torch.full((2, 4, 8192), 0.5, device=DEV)      # all equal
+    _check_topk_same_scores(cfg, scores, [8192, 8192], 777)
+
+
+def test_topk_negative_and_large_scores():
+    cfg = Config(B=1, H_q=1, H_kv=1, N_max=4096, L=16, P=8)
+    g = torch.Generator(device=DEV).manual_seed(4)
+    scores = torch.randn((1, 1, 4096), generator=g, device=DEV) * 1e3
+    _check_topk_same_scores(cfg, scores, [4096], 333)
+
+
+# ---------------------------------------------------------------------------
+# sparse attention
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", [KV_SHARED, PER_QHEAD])
+def test_sparse_decode_on_gpu_selection(mode):
+    lens = [4096, 1999]
+    cfg, c, W, d = make(2, 8, 2, 4096, 16, 8, seed=11, seq_lens=lens, mode=mode)
+    k = 512
+    g = torch.Generator(device=DEV).manual_seed(9)
+    scores = torch.rand((2, cfg.H_sel, 4096), generator=g, device=DEV)
+    for b, n in enumerate(lens):
+        scores[b, :, n:] = -math.inf
+    idx, cnt = ops.topk(cfg, scores, d["seq_lens"], k)
+    out, lse = ops.sparse_decode(cfg, d["q"], d["K"], d["V"], idx, cnt, k)
+    out = out.float().cpu().numpy()
+    lse = lse.cpu().numpy()
+    q, K, V = O.widen(c["q"]), O.widen(c["K"]), O.widen(c["V"])
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    for b in range(2):
+        for h in range(8):
+            r = h // 4 if mode == KV_SHARED else h
+            S = idx[b, r, :cnt[b, r]]
+            y, l = O.sparse_attention(q[b, h], K[b, h // 4], V[b, h // 4], S, cfg.scale)
+            assert np.max(np.abs(out[b, h] - y)) <= 2e-3
+            assert abs(lse[b, h] - l) <= 1e-3
+
+
+def test_sparse_full_budget_equals_dense_and_sdpa():
+    N = 1024
+    cfg, c, W, d = make(1, 8, 2, N, 16, 8, seed=12)
+    idx = torch.arange(N, dtype=torch.int32, device=DEV).repeat(1, 2, 1).contiguous()
+    cnt = torch.full((1, 2), N, dtype=torch.int32, device=DEV)
+    out_s, lse_s = ops.sparse_decode(cfg, d["q"], d["K"], d["V"], idx, cnt, N)
+    out_d, lse_d = ops.dense_decode(cfg, d["q"], d["K"], d["V"], d["seq_lens"])
+    assert torch.equal(out_s, out_d)
+    qq = d["q"].float().view(1, 8, 1, 128)
+    KK = d["K"].float().repeat_interleave(4, dim=1)
+    VV = d["V"].float().repeat_interleave(4, dim=1)
+    ref = torch.nn.functional.scaled_dot_product_attention(qq, KK, VV, scale=cfg.scale).view(1, 8, 128)
+    assert (out_d.float() - ref).abs().max().item() <= 2e-3
+
+
+def test_empty_selection_gives_zero_and_neg_inf():
+    cfg, c, W, d = make(2, 4, 1, 256, 16, 8, seed=13, seq_lens=[0, 256])
+    dec = SocketDecoder(cfg, d["W"], d["K"], d["V"], k=64)
+    dec.prefill()
+    out, lse = dec.step(d["q"], d["seq_lens"])
+    assert torch.all(out[0] == 0) and torch.all(torch.isneginf(lse[0]))
+    assert torch.all(torch.isfinite(lse[1]))
+
+
+def test_lse_combine_matches_union():
+    """Partials from disjoint index sets merged == attention over the union."""
+    cfg, c, W, d = make(1, 4, 1, 2048, 16, 8, seed=14)
+    k = 300
+    sel = torch.randperm(2048, generator=torch.Generator().manual_seed(1))[:2 * k].sort().values
+    parts = []
+    for a in (sel[:k], sel[k:]):
+        idx = a.to(torch.int32).view(1, 1, k).to(DEV)
+        cnt = torch.full((1, 1), k, dtype=torch.int32, device=DEV)
+        p = torch.empty((1, 4, 130), dtype=torch.float32, device=DEV)
+        ops.sparse_decode(cfg, d["q"], d["K"], d["V"], idx, cnt, k, partial=p, want_out=False)
+        parts.append(p)
+    out, lse = ops.lse_combine(cfg, torch.stack(parts))
+    q, K, V = O.widen(c["q"]), O.widen(c["K"]), O.widen(c["V"])
+    for h in range(4):
+        y, l = O.sparse_attention(q[0, h], K[0, 0], V[0, 0], sel.numpy(), cfg.scale)
+        assert np.max(np.abs(out[0, h].float().cpu().numpy() - y)) <= 2e-3
+        assert abs(lse[0, h].item() - l) <= 1e-3
+
+
+# ---------------------------------------------------------------------------
+# end to end
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", [KV_SHARED, PER_QHEAD])
+def test_decode_step_c1_end_to_end(mode):
+    """BASELINE config 1: single head, n=4096, L=16, P=8, k=512 (+ a GQA case)."""
+    for (H_q, H_kv) in ((1, 1), (8, 2)):
+        cfg, c, W, d = make(1, H_q, H_kv, 4096, 16, 8, seed=21 + H_q, mode=mode,
+                            variant="needle", n_needle=64)
+        dec = SocketDecoder(cfg, d["W"], d["K"], d["V"], k=512)
+        dec.prefill()
+        out, lse = dec.step(d["q"], d["seq_lens"])
+        ref = O.decode_step(c["q"], c["K"], c["V"], W, c["seq_lens"], tau=0.5, k=512,
+                            sm_scale=cfg.scale, group_mode=mode)
+        idx, cnt = dec.idx.cpu().numpy(), dec.cnt.cpu().numpy()
+        sc = dec.scores.cpu().numpy()
+        q, K, V = O.widen(c["q"]), O.widen(c["K"]), O.widen(c["V"])
+        for r in range(cfg.H_sel):
+            s_ref = ref["scores"][(0, r)]
+            fin = np.isfinite(s_ref)
+            assert np.max(rel_err(sc[0, r][fin], s_ref[fin])) <= 1e-5
+            S_gpu = idx[0, r, :cnt[0, r]]
+            S_ref = ref["sel"][(0, r)]
+            assert len(S_gpu) == len(S_ref)
+            kth = np.sort(s_ref[S_ref])[0]
+            for j in np.setxor1d(S_gpu, S_ref):          # documented near-ties only
+                assert abs(s_ref[j] - kth) <= 1e-5 * kth, (j, s_ref[j], kth)
+        G = H_q // H_kv
+        for h in range(H_q):
+            r = h // G if mode == KV_SHARED else h
+            S = idx[0, r, :cnt[0, r]]
+            y, l = O.sparse_attention(q[0, h], K[0, h // G], V[0, h // G], S, cfg.scale)
+            assert np.max(np.abs(out[0, h].float().cpu().numpy() - y)) <= 2e-3
+            if np.array_equal(S, ref["sel"][(0, r)]):
+                assert np.max(np.abs(out[0, h].float().cpu().numpy() - ref["y"][(0, h)])) <= 2e-3
+
+
+def test_cuda_graph_replay_matches_eager():
+    cfg, c, W, d = make(2, 8, 2, 2048, 60, 8, seed=31)
+    dec = SocketDecoder(cfg, d["W"], d["K"], d["V"], k=205)
+    dec.prefill()
+    out_e, lse_e = [t.clone() for t in dec.step(d["q"], d["seq_lens"], append_pos=2047)]
+    dec.capture(d["q"], d["seq_lens"], append_pos=2047)
+    out_g, lse_g = dec.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out_e, out_g) and torch.equal(lse_e, lse_g)     # deterministic
+
+
+def test_topk_resolve_virtual_shards():
+    """Sequence sharding on one device: G virtual shards -> local top-k ->
+    (gathered) candidates -> resolve == single-device top-k of the whole row."""
+    G, Ns, k = 4, 4096, 1500
+    cfg_full = Config(B=2, H_q=8, H_kv=2, N_max=G * Ns, L=16, P=8)
+    cfg_sh = Config(B=2, H_q=8, H_kv=2, N_max=Ns, L=16, P=8)
+    g = torch.Generator(device=DEV).manual_seed(7)
+    full = (torch.randint(0, 50, (2, 2, G * Ns), generator=g, device=DEV).float() / 50)  # ties
+    full[1, :, 10000:] = -math.inf
+    lens_full = torch.tensor([G * Ns, 10000], dtype=torch.int32, device=DEV)
+    idx_full, cnt_full = ops.topk(cfg_full, full, lens_full, k)
+    cs, ci = [], []
+    for s in range(G):
+        part = full[:, :, s * Ns:(s + 1) * Ns].contiguous()
+        lens = torch.clamp(lens_full - s * Ns, 0, Ns).to(torch.int32)
+        i, n, sc = ops.topk(cfg_sh, part, lens, k, want_scores=True)
+        cs.append(sc)
+        ci.append(i)
+    cs, ci = torch.stack(cs), torch.stack(ci)
+    got = [[] for _ in range(2 * 2)]
+    for s in range(G):
+        i, n = ops.topk_resolve(cfg_sh, cs, ci, s, k)
+        for row in range(4):
+            b, r = divmod(row, 2)
+            got[row] += [int(x) + s * Ns for x in i[b, r, :n[b, r]].tolist()]
+    for row in range(4):
+        b, r = divmod(row, 2)
+        ref = idx_full[b, r, :cnt_full[b, r]].tolist()
+        assert got[row] == ref
+
+
+@pytest.mark.parametrize("B,k", [(16, 3277)])
+def test_full_size_c2_sampled(B, k):
+    """BASELINE config 2 at full size (32 q / 8 kv heads, 32K, L=60, P=8,
+    10x sparsity), launch configuration of bench.py; sampled rows vs oracle."""
+    N, L, P = 32768, 60, 8
+    cfg = Config(B=B, H_q=32, H_kv=8, N_max=N, L=L, P=P, tau=0.5)
+    q, K, V = datagen.torch_make_cache(B, 32, 8, N, 128, seed=77)
+    Wb = datagen.make_projections(4242, L, P, 128)
+    W = bits_to_dev(Wb)
+    lens = torch.full((B,), N, dtype=torch.int32, device=DEV)
+    dec = SocketDecoder(cfg, W, K, V, k=k)
+    dec.prefill()
+    out, lse = dec.step(q, lens, append_pos=N - 1)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    for (b, g) in [(0, 0), (B - 1, 7), (int(rng.integers(B)), int(rng.integers(8)))]:
+        Kb = K[b, g].view(torch.int16).cpu().numpy().view(np.uint16)
+        Vb = V[b, g].view(torch.int16).cpu().numpy().view(np.uint16)
+        qb = q[b, g * 4:(g + 1) * 4].view(torch.int16).cpu().numpy().view(np.uint16)
+        ref = O.decode_step(qb[None], Kb[None, None], Vb[None, None], Wb, np.array([N]), tau=0.5,
+                            k=k, sm_scale=cfg.scale)
+        s_ref = ref["scores"][(0, 0)]
+        assert np.max(rel_err(dec.scores[b, g].cpu().numpy(), s_ref)) <= 1e-5
+        S_gpu = dec.idx[b, g, :dec.cnt[b, g]].cpu().numpy()
+        S_ref = ref["sel"][(0, 0)]
+        kth = np.sort(s_ref[S_ref])[0]
+        for j in np.setxor1d(S_gpu, S_ref):
+            assert abs(s_ref[j] - kth) <= 1e-5 * kth
+        qf, Kf, Vf = O.widen(qb), O.widen(Kb), O.widen(Vb)
+        for h in range(4):
+            y, _ = O.sparse_attention(qf[h], Kf, Vf, S_gpu, cfg.scale)
+            assert np.max(np.abs(out[b, g * 4 + h].float().cpu().numpy() - y)) <= 2e-3

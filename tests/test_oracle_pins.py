@@ -292,6 +292,8 @@ def test_topk_special_cases():
     s2 = s.copy()
     s2[20:] = -np.inf
     assert np.array_equal(O.topk_select(s2, 30, 20), np.arange(20))          # k > n_valid
+    assert np.array_equal(O.topk_select(s, 30, 20), np.arange(20))           # j >= n invalid
+    assert np.array_equal(O.topk_bruteforce(s[:8], 3, 5), O.topk_select(s[:8], 3, 5))
 
 
 # ---------------------------------------------------------------------------
