@@ -114,6 +114,58 @@ __global__ void pack_codes_kernel(const uint8_t* __restrict__ plain, uint8_t* __
   }
 }
 
+// ----------------------------------------------------------------------------
+// Append path (decode step: n_count new keys per (b, kv-head), typically 1).
+// grid.x = table pairs, grid.y = key blocks of 64; thread = (key, table):
+// P dot products of length 128 in fp32 (t ascending), one code byte written to
+// slot s = (l & ~M) | ((l - j) & M) of key j (inverse of slot_table).
+// ----------------------------------------------------------------------------
+constexpr int kAppendTables = 2;
+constexpr int kAppendKeys = 64;
+
+__global__ void __launch_bounds__(kAppendTables * kAppendKeys)
+hash_append_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict__ W,
+                   uint8_t* __restrict__ codes, int N_max, int L, int P, int Lp, int n_begin,
+                   int n_count, int total_keys) {
+  __shared__ float ws[kAppendTables][8][kD];
+  const int l0 = blockIdx.x * kAppendTables;
+  for (int i = threadIdx.x; i < kAppendTables * 8 * kD; i += blockDim.x) {
+    const int tl = i / (8 * kD), p = (i / kD) % 8, t = i % kD;
+    const int l = l0 + tl;
+    ws[tl][p][t] = (l < L && p < P) ? __uint_as_float((uint32_t)W[((size_t)l * P + p) * kD + t] << 16) : 0.f;
+  }
+  __syncthreads();
+  const int key = blockIdx.y * kAppendKeys + (threadIdx.x % kAppendKeys);
+  const int tl = threadIdx.x / kAppendKeys;
+  const int l = l0 + tl;
+  if (key >= total_keys || l >= Lp) return;
+  const int bh = key / n_count, j = n_begin + key % n_count;
+  uint32_t code = 0;
+  if (l < L) {
+    const uint4* kr = reinterpret_cast<const uint4*>(K + ((size_t)bh * N_max + j) * kD);
+    float x[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) x[p] = 0.f;
+#pragma unroll 4
+    for (int c = 0; c < kD / 8; ++c) {
+      const uint4 u = kr[c];
+      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float kv = (e & 1) ? bf16hi(w4[e >> 1]) : bf16lo(w4[e >> 1]);
+#pragma unroll
+        for (int p = 0; p < 8; ++p) x[p] = fmaf(ws[tl][p][c * 8 + e], kv, x[p]);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+      if (p < P) code |= (x[p] >= 0.f ? 1u : 0u) << p;   // sign(0) = +1 (R-3), LSB = row 0 (R-4)
+  }
+  const int M = (Lp < 32 ? Lp : 32) - 1;
+  const int s = (l & ~M) | ((l - j) & M);
+  codes[(size_t)bh * N_max * Lp + code_off(j, s, Lp)] = (uint8_t)code;
+}
+
 socket_status launch_hash_keys_simt(const socket_cfg& c, const void* K, const void* W,
                                     uint8_t* codes, int n_begin, int n_count, cudaStream_t st) {
   const int Lp = code_slots(c.L);
@@ -133,13 +185,20 @@ socket_status launch_hash_keys(const socket_cfg& c, const void* K, const void* V
                                int n_count, const void* W, uint8_t* codes, float* vnorm,
                                cudaStream_t st) {
   if (n_count == 0) return SOCKET_OK;
-  bool used = false;
-  socket_status s = launch_hash_keys_tc(c, K, W, codes, n_begin, n_count, st, &used);
-  if (s != SOCKET_OK) return s;
-  if (!used) {
-    s = launch_hash_keys_simt(c, K, W, codes, n_begin, n_count, st);
-    if (s != SOCKET_OK) return s;
+  socket_status s = SOCKET_OK;
+  if (n_count <= 16) {
+    const int Lp = code_slots(c.L);
+    const int total = c.B * c.H_kv * n_count;
+    dim3 grid((Lp + kAppendTables - 1) / kAppendTables, (total + kAppendKeys - 1) / kAppendKeys);
+    hash_append_kernel<<<grid, kAppendTables * kAppendKeys, 0, st>>>(
+        (const uint16_t*)K, (const uint16_t*)W, codes, c.N_max, c.L, c.P, Lp, n_begin, n_count, total);
+    s = check_launch("hash_append_kernel");
+  } else {
+    bool used = false;
+    s = launch_hash_keys_tc(c, K, W, codes, n_begin, n_count, st, &used);
+    if (s == SOCKET_OK && !used) s = launch_hash_keys_simt(c, K, W, codes, n_begin, n_count, st);
   }
+  if (s != SOCKET_OK) return s;
   if (V) {
     const int rows = c.B * c.H_kv * n_count;
     const int threads = 256;

@@ -16,70 +16,112 @@
 namespace sk {
 
 constexpr int kTabThreads = 256;
-constexpr int kTabPerCta = 8;     // tables per CTA
-constexpr int kMaxHeads = 16;     // heads per selection row
+constexpr int kTabPerCta = 4;     // tables per CTA
+constexpr int kMaxHeads = 8;      // heads per selection row
 
+// One CTA = (b, selection row) x 8 tables.  Steps (all latency-oriented):
+//  1. stage q (NH heads) and W^(l) of the 8 tables in shared memory (16-B loads);
+//  2. one thread per (head, table, bit): x = W_i . q in fp64 (bf16 products are
+//     exact), u = tanh(x)/sqrt(d), factors sigma(+-2u/tau) in fp64;
+//  3. half tables lo(r & 15) = prod_{i<4} f_i, hi(r >> 4) = prod_{i>=4} f_i in
+//     fp64, rounded once to fp32;
+//  4. T(r) = sum_h lo_h * hi_h; consecutive threads write consecutive table
+//     columns of one LUT row (coalesced 32-byte segments).
 __global__ void __launch_bounds__(kTabThreads)
 query_tables_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ W,
                     float* __restrict__ plain, float* __restrict__ lut, int H_q, int H_sel,
                     int NH, int L, int P, int Lp, float tau) {
   __shared__ float qs[kMaxHeads][kD];
-  __shared__ float f[kMaxHeads][kTabPerCta][8][2];   // sigma factors per (h, table, bit, value)
+  __shared__ float wsm[kTabPerCta * 8][kD + 1];
+  __shared__ double fx[kMaxHeads][kTabPerCta][8][2];        // sigma factors
+  __shared__ float half_lo[kMaxHeads][16][kTabPerCta];
+  __shared__ float half_hi[kMaxHeads][16][kTabPerCta];
   const int row = blockIdx.x;                // b * H_sel + r
   const int b = row / H_sel, r = row % H_sel;
   const int h0 = (NH == 1) ? r : r * NH;     // first query head of the row
   const int l0 = blockIdx.y * kTabPerCta;
   const int R = 1 << P;
-  for (int i = threadIdx.x; i < NH * kD; i += kTabThreads) {
-    const int h = i / kD, t = i % kD;
-    qs[h][t] = __uint_as_float((uint32_t)q[((size_t)b * H_q + h0 + h) * kD + t] << 16);
-  }
-  __syncthreads();
-  // dot products x = W[l][i] . q_h : one warp per (h, table, bit); lane holds 4
-  // elements.  The few L*P*NH projections and their logistic factors are
-  // evaluated in fp64 (bf16 x bf16 products are exact there), so the factors
-  // carry only their final fp32 rounding; the fp32 dot product error would be
-  // amplified by 2/(sqrt(d) tau) in sigma.
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double inv_sqrt_d = 1.0 / sqrt((double)kD);
-  const int ndots = NH * kTabPerCta * P;
-  for (int di = warp; di < ndots; di += kTabThreads / 32) {
-    const int i = di % P, tl = (di / P) % kTabPerCta, h = di / (P * kTabPerCta);
-    const int l = l0 + tl;
-    if (l >= L) {  // padding table: never contributes (its LUT column is zeroed below)
-      if (lane == 0) { f[h][tl][i][0] = 0.f; f[h][tl][i][1] = 0.f; }
-      continue;
-    }
-    const uint2 u = *reinterpret_cast<const uint2*>(W + ((size_t)l * P + i) * kD + lane * 4);
-    const float* qq = &qs[h][lane * 4];
-    double x = (double)bf16lo(u.x) * qq[0];
-    x = fma((double)bf16hi(u.x), (double)qq[1], x);
-    x = fma((double)bf16lo(u.y), (double)qq[2], x);
-    x = fma((double)bf16hi(u.y), (double)qq[3], x);
+  const int tid = threadIdx.x;
+  // 1. staging
+  for (int i = tid; i < NH * (kD / 8); i += kTabThreads) {
+    const int h = i / (kD / 8), c = i % (kD / 8);
+    const uint4 u = *reinterpret_cast<const uint4*>(q + ((size_t)b * H_q + h0 + h) * kD + c * 8);
+    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) {
-      const double uu = tanh(x) * inv_sqrt_d;            // Alg. 2 l.217
-      const double a = 2.0 * uu / (double)tau;           // logit gap of bit i
-      f[h][tl][i][1] = (float)(1.0 / (1.0 + exp(-a)));   // c_{r,i} = +1  (bit set)
-      f[h][tl][i][0] = (float)(1.0 / (1.0 + exp(a)));    // c_{r,i} = -1
+    for (int e = 0; e < 4; ++e) {
+      qs[h][c * 8 + 2 * e] = bf16lo(w4[e]);
+      qs[h][c * 8 + 2 * e + 1] = bf16hi(w4[e]);
+    }
+  }
+  const int nrows_w = kTabPerCta * P;        // W rows of this CTA
+  for (int i = tid; i < nrows_w * (kD / 8); i += kTabThreads) {
+    const int wr = i / (kD / 8), c = i % (kD / 8);
+    const int l = l0 + wr / P;
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (l < L) u = *reinterpret_cast<const uint4*>(W + ((size_t)l * P + wr % P) * kD + c * 8);
+    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      wsm[wr][c * 8 + 2 * e] = bf16lo(w4[e]);
+      wsm[wr][c * 8 + 2 * e + 1] = bf16hi(w4[e]);
     }
   }
   __syncthreads();
-  const int nent = kTabPerCta * 256;
+  // 2. projections and logistic factors: every product of
+  //    two bf16 values is exact in fp32; each half of the 128-term sum is
+  //    accumulated with TwoSum compensation by one of two threads, and the
+  //    halves are merged in fp64, so x is exact to ~2^-48.  u = tanh(x)/sqrt(d)
+  //    and sigma(+-2u/tau) use the accurate fp32 functions (<= 2 ulp each), so a
+  //    factor carries <= 3 ulp + 3 ulp * |a|; no fp64 transcendentals.
+  const float inv_sqrt_d = 0.08838834764831845f;   // 1/sqrt(128), correctly rounded
+  const int ndots = NH * nrows_w;
+  for (int base = 0; base < 2 * ndots; base += kTabThreads) {   // uniform trip count
+    const int di2 = base + tid;
+    const bool act = di2 < 2 * ndots;
+    const int di = act ? di2 >> 1 : 0, part = di2 & 1;            // two threads per dot
+    const int wr = di % nrows_w, h = di / nrows_w;
+    float s0 = 0.f, c0 = 0.f;
+    const int t0 = part * (kD / 2);
+#pragma unroll 8
+    for (int t = t0; t < t0 + kD / 2; ++t) {
+      const float p0 = wsm[wr][t] * qs[h][t];       // exact
+      const float u0 = s0 + p0, b0 = u0 - s0;
+      c0 += (s0 - (u0 - b0)) + (p0 - b0);
+      s0 = u0;
+    }
+    const double mine = (double)s0 + (double)c0;
+    const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
+    if (act && part == 0) {
+      const float x = (float)(mine + other);
+      const float uu = tanhf(x) * inv_sqrt_d;       // Alg. 2 l.217
+      const float a = 2.0f * uu / tau;              // logit gap of bit i
+      fx[h][wr / P][wr % P][1] = (double)(1.0f / (1.0f + expf(-a)));   // c_{r,i} = +1 (bit set)
+      fx[h][wr / P][wr % P][0] = (double)(1.0f / (1.0f + expf(a)));    // c_{r,i} = -1
+    }
+  }
+  __syncthreads();
+  // 3. half tables (bits 0..3 and 4..P-1; an empty product is 1)
+  for (int i = tid; i < NH * kTabPerCta * 32; i += kTabThreads) {
+    const int e = i & 15, hi = (i >> 4) & 1, tl = (i >> 5) % kTabPerCta, h = i / (32 * kTabPerCta);
+    double p = 1.0;
+#pragma unroll
+    for (int bit = 0; bit < 4; ++bit) {
+      const int ib = hi * 4 + bit;
+      if (ib < P) p *= fx[h][tl][ib][(e >> bit) & 1];
+    }
+    if (hi) half_hi[h][e][tl] = (float)p; else half_lo[h][e][tl] = (float)p;
+  }
+  __syncthreads();
+  // 4. entries: thread -> (row rr, table tl) with tl fastest
   const int panels = Lp <= 64 ? 1 : (Lp + 63) / 64;
   float* lrow = lut ? lut + (size_t)row * panels * (256 * 64) : nullptr;
-  for (int e = threadIdx.x; e < nent; e += kTabThreads) {
-    const int tl = e / 256, rr = e % 256;
+  for (int e = tid; e < 256 * kTabPerCta; e += kTabThreads) {
+    const int tl = e % kTabPerCta, rr = e / kTabPerCta;
     const int l = l0 + tl;
     if (l >= Lp) continue;
     float T = 0.f;
     if (l < L && rr < R) {
-      for (int h = 0; h < NH; ++h) {
-        float p = 1.0f;
-        for (int i = 0; i < P; ++i) p *= f[h][tl][i][(rr >> i) & 1];
-        T += p;
-      }
+      for (int h = 0; h < NH; ++h) T = fmaf(half_lo[h][rr & 15][tl], half_hi[h][rr >> 4][tl], T);
       if (plain) plain[((size_t)row * L + l) * R + rr] = T;
     }
     if (lrow) {
@@ -96,7 +138,7 @@ socket_status launch_query_tables(const socket_cfg& c, const void* q, const void
                                   float* plain, float* lut, cudaStream_t st) {
   const int H_sel = num_sel_rows(c);
   const int NH = c.group_mode == SOCKET_GROUP_PER_QHEAD ? 1 : c.H_q / c.H_kv;
-  if (NH > kMaxHeads) return fail(SOCKET_EUNSUPPORTED, "more than 16 query heads per KV head");
+  if (NH > kMaxHeads) return fail(SOCKET_EUNSUPPORTED, "more than 8 query heads per KV head");
   const int Lp = code_slots(c.L);
   dim3 grid(c.B * H_sel, (Lp + kTabPerCta - 1) / kTabPerCta);
   query_tables_kernel<<<grid, kTabThreads, 0, st>>>((const uint16_t*)q, (const uint16_t*)W, plain,
@@ -224,29 +266,52 @@ score_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
     const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
     float* srow = scores + (size_t)row * N_max;
     bool lut_ready = !need_lut;
-    // each warp takes tiles tile0 + warp + 8*i; two tiles (keys) per lane per step
-    for (int tt = tile0 + warp; tt < tile1; tt += 2 * kScoreWarps) {
-      const int tb = tt + kScoreWarps;
-      const bool has_b = tb < tile1;
-      const int j_a = tt * 32 + lane, j_b = tb * 32 + lane;
-      const bool va = tt < valid_tiles, vb = has_b && tb < valid_tiles;
-      CodeRegs<LP> c[2];
-      float vn[2] = {0.f, 0.f};
-      if (va) { load_codes<LP>(c[0], crow + (size_t)tt * 32 * LP, lane); vn[0] = vrow[j_a]; }
-      if (vb) { load_codes<LP>(c[1], crow + (size_t)tb * 32 * LP, lane); vn[1] = vrow[j_b]; }
-      else { for (int w = 0; w < CodeRegs<LP>::NW; ++w) c[1].w[w] = 0; }
-      if (va && !lut_ready) { mbar_wait(&bar, phase); lut_ready = true; }
-      float acc[2];
-      if (va) lookup_sum<LP, 2>(c, acc, smem, lane);
-      const float ninf = -INFINITY;
-      {
-        bool ok = va && j_a < n && (!mrow || mrow[j_a]);
-        srow[j_a] = ok ? vn[0] * acc[0] : ninf;
+    // each warp takes tile pairs (tt, tt + 8) with tt = tile0 + warp + 16 i; the
+    // codes of the next pair are loaded while the current pair is looked up.
+    auto load_pair = [&](CodeRegs<LP> (&c)[2], float (&vn)[2], int tt) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int ti = tt + u * kScoreWarps;
+        if (ti < tile1 && ti < valid_tiles) {
+          load_codes<LP>(c[u], crow + (size_t)ti * 32 * LP, lane);
+          vn[u] = vrow[ti * 32 + lane];
+        } else {
+#pragma unroll
+          for (int w = 0; w < CodeRegs<LP>::NW; ++w) c[u].w[w] = 0;
+          vn[u] = 0.f;
+        }
       }
-      if (has_b) {
-        bool ok = vb && j_b < n && (!mrow || mrow[j_b]);
-        srow[j_b] = ok ? vn[1] * acc[1] : ninf;
+    };
+    auto finish_pair = [&](const CodeRegs<LP> (&c)[2], const float (&vn)[2], int tt) {
+      const bool any_valid = tt < valid_tiles;
+      float acc[2] = {0.f, 0.f};
+      if (any_valid) {
+        if (!lut_ready) { mbar_wait(&bar, phase); lut_ready = true; }
+        lookup_sum<LP, 2>(c, acc, smem, lane);
       }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int ti = tt + u * kScoreWarps;
+        if (ti < tile1) {
+          const int j = ti * 32 + lane;
+          const bool ok = ti < valid_tiles && j < n && (!mrow || mrow[j]);
+          srow[j] = ok ? vn[u] * acc[u] : -INFINITY;
+        }
+      }
+    };
+    CodeRegs<LP> ca[2], cb[2];
+    float va[2], vb[2];
+    int tt = tile0 + warp;
+    if (tt < tile1) load_pair(ca, va, tt);
+    while (tt < tile1) {
+      const int t2 = tt + 2 * kScoreWarps;
+      if (t2 < tile1) load_pair(cb, vb, t2);
+      finish_pair(ca, va, tt);
+      if (t2 >= tile1) break;
+      const int t3 = t2 + 2 * kScoreWarps;
+      if (t3 < tile1) load_pair(ca, va, t3);
+      finish_pair(cb, vb, t2);
+      tt = t3;
     }
     if (need_lut) {
       if (!lut_ready) mbar_wait(&bar, phase);

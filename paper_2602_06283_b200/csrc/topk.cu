@@ -1,16 +1,24 @@
 // Alg. 3 l.244 TopK with forced sink / local window (l.686), and
 // the exact resolve step of sequence sharding.
 //
-// One thread-block CLUSTER per selection row.  Each CTA of the cluster owns a
-// contiguous slice of the row and keeps it in shared memory as monotone u32
-// keys (larger score <=> larger key; invalid = 0; forced = 0xFFFFFFFF).  An
-// MSB-first radix select with 8-bit digits finds the k_eff-th largest key T:
-// every pass builds a local 256-bin histogram (match_any-aggregated shared
-// atomics), the cluster sums the CTAs' histograms through distributed shared
-// memory (DSMEM) and every CTA takes the same digit decision.  No sort.
-// Selection = keys > T plus the first (quota) keys == T in index order, which
+// One thread-block CLUSTER per selection row.  Each CTA owns a contiguous
+// slice of the row and keeps it in shared memory as monotone u32 keys (larger
+// score <=> larger key; invalid = 0; forced sink/window keys = 0xFFFFFFFF).
+// Selection = keys > T plus the first `quota` keys == T in index order, which
 // is exactly "score descending, ties to the smaller index" (reading R-15).
-// A stable ballot compaction writes the selected indices in ascending order.
+//
+// Finding T (the k_eff-th largest key), no sort:
+//   1. cluster-reduce (#valid, #forced, min and max regular key) through
+//      distributed shared memory (DSMEM);
+//   2. one 2048-bin histogram over the row's actual key range [min, max]
+//      (bin = (key - min) >> shift, the smallest shift that fits: monotone,
+//      exact integer arithmetic), summed across the cluster through DSMEM; the bin holding
+//      the target rank is found by a suffix scan;
+//   3. the keys of that bin (typically tens) are gathered from every CTA and
+//      T is resolved exactly by a local radix select over them.
+//   If the bin is too full to gather (massive exact ties, degenerate ranges),
+//   a 4-pass MSB radix select over the whole cluster (8-bit digits) is used.
+// A stable ballot compaction then writes the selected indices in ascending order.
 #include <cooperative_groups.h>
 
 #include "internal.cuh"
@@ -21,6 +29,8 @@ namespace sk {
 
 constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
+constexpr int kBins = 2048;
+constexpr int kCandCap = 2048;
 
 struct TopkArgs {
   // mode 0: scores [rows][N_max], n = seq_lens[b]
@@ -43,7 +53,13 @@ __device__ __forceinline__ float load_elem(const TopkArgs& a, int row, int e) {
   return a.cand_scores[((size_t)s * a.rows + row) * a.k + i];
 }
 
-// exclusive scan over the 16 warps of one value per warp; returns prefix, total via ref
+__device__ __forceinline__ uint32_t make_key(float s, int e, int n, int sink, int window, int mode) {
+  if (s == -INFINITY) return 0u;
+  if (mode == 0 && (e < sink || e >= n - window)) return 0xFFFFFFFFu;
+  return f2key(s);
+}
+
+// exclusive scan over the warps of one value per warp
 __device__ __forceinline__ int block_excl_scan_warps(int v, int* sh, int warp, int lane, int& total) {
   __syncthreads();
   if (lane == 0) sh[warp] = v;
@@ -59,12 +75,65 @@ __device__ __forceinline__ int block_excl_scan_warps(int v, int* sh, int warp, i
   return pre;
 }
 
+struct TopkShared {
+  uint32_t hist[kBins];          // local histogram (also radix fallback buffers)
+  uint32_t ghist[kBins];         // cluster-summed histogram
+  uint32_t cand[kCandCap];       // local candidates
+  uint32_t gcand[kCandCap];      // gathered candidates
+  uint32_t rhist[256];           // local radix histogram for candidate resolve
+  int scan[kTopkWarps];
+  uint32_t stat[8];              // nvalid, nforced, kmin, kmax, ncand, gt, eq, emit
+  uint32_t dec[4];
+};
+
+// Local exact select over a small candidate array: the `need`-th largest key
+// (1-based) and how many candidates are strictly greater.
+__device__ void local_select(const uint32_t* c, int C, uint32_t need, TopkShared& S, int tid,
+                             int warp, int lane, uint32_t& T, uint32_t& above) {
+  uint32_t prefix = 0, k_rem = need;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    const uint32_t hmask = pass == 0 ? 0u : (0xFFFFFFFFu << (shift + 8));
+    for (int i = tid; i < 256; i += kTopkThreads) S.rhist[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < ((C + 31) & ~31); i += kTopkThreads) {
+      const bool m = i < C && (c[i] & hmask) == (prefix & hmask);
+      const uint32_t bin = m ? ((c[i] >> shift) & 255u) : 256u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+      if (m && lane == __ffs(peers) - 1) atomicAdd(&S.rhist[bin], (uint32_t)__popc(peers));
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t c8[8], tot = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { c8[q] = S.rhist[255 - (lane * 8 + q)]; tot += c8[q]; }
+      uint32_t inc = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const uint32_t excl = inc - tot;
+      const unsigned hb = __ballot_sync(0xffffffffu, excl < k_rem && inc >= k_rem);
+      if (lane == __ffs(hb) - 1) {
+        uint32_t run = excl;
+        for (int q = 0; q < 8; ++q) {
+          if (run + c8[q] >= k_rem) { S.dec[0] = 255 - (lane * 8 + q); S.dec[1] = k_rem - run; break; }
+          run += c8[q];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= S.dec[0] << shift;
+    k_rem = S.dec[1];
+  }
+  T = prefix;
+  above = need - k_rem;
+}
+
 __global__ void __launch_bounds__(kTopkThreads, 1) topk_cluster_kernel(TopkArgs a) {
   extern __shared__ __align__(16) uint32_t keys[];          // [per]
-  __shared__ uint32_t hist[2][256];
-  __shared__ int sh_scan[kTopkWarps];
-  __shared__ int sh_cnt[4];                                  // valid, gt, eq, emit
-  __shared__ uint32_t sh_dec[2];                             // digit, k_rem
+  __shared__ TopkShared S;
 
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
@@ -78,64 +147,190 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_cluster_kernel(TopkArgs 
   len = len < 0 ? 0 : (len > a.per ? a.per : len);
   const int len32 = (len + 31) & ~31;
 
-  // ---- load slice as keys -------------------------------------------------
-  int nvalid = 0;
-  for (int i = tid; i < len32; i += kTopkThreads) {
-    uint32_t key = 0;
-    if (i < len) {
-      const int e = base + i;
-      const float s = load_elem(a, row, e);
-      if (s != -INFINITY) {
-        key = f2key(s);
-        if (a.mode == 0 && (e < a.sink || e >= n - a.window)) key = 0xFFFFFFFFu;
+  // ---- 0. load slice as keys (4 elements per thread per step) ---------------
+  uint32_t nvalid = 0, nforced = 0, kmin = 0xFFFFFFFFu, kmax = 0u;
+  if (a.mode == 0) {
+    const float* src = a.scores + (size_t)row * a.N_max + base;   // 128-B aligned
+    constexpr int U = 4;                                          // float4 loads in flight
+    for (int i0 = tid * 4; i0 < len32; i0 += kTopkThreads * 4 * U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i4 = i0 + u * kTopkThreads * 4;
+        v[u] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        if (i4 + 3 < len) v[u] = *reinterpret_cast<const float4*>(src + i4);
+        else if (i4 < len) {
+          v[u].x = src[i4];
+          if (i4 + 1 < len) v[u].y = src[i4 + 1];
+          if (i4 + 2 < len) v[u].z = src[i4 + 2];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i4 = i0 + u * kTopkThreads * 4;
+        if (i4 >= len32) break;
+        const float vs[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+        uint4 kk;
+        uint32_t* kp = &kk.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t key = make_key(vs[e], base + i4 + e, n, a.sink, a.window, 0);
+          kp[e] = key;
+          nvalid += key != 0u;
+          nforced += key == 0xFFFFFFFFu;
+          if (key != 0u && key != 0xFFFFFFFFu) { kmin = min(kmin, key); kmax = max(kmax, key); }
+        }
+        *reinterpret_cast<uint4*>(keys + i4) = kk;
       }
     }
-    keys[i] = key;
-    nvalid += key != 0;
+  } else {
+    for (int i = tid; i < len32; i += kTopkThreads) {
+      uint32_t key = 0;
+      if (i < len) key = make_key(load_elem(a, row, base + i), base + i, n, 0, 0, 1);
+      keys[i] = key;
+      nvalid += key != 0u;
+      if (key != 0u) { kmin = min(kmin, key); kmax = max(kmax, key); }
+    }
   }
-  for (int i = tid; i < 512; i += kTopkThreads) (&hist[0][0])[i] = 0;
-  if (tid < 4) sh_cnt[tid] = 0;
+  if (tid < 8) S.stat[tid] = (tid == 2) ? 0xFFFFFFFFu : 0u;   // kmin starts at +max
+  for (int i = tid; i < kBins; i += kTopkThreads) S.hist[i] = 0;
   __syncthreads();
-  {
-    int v = nvalid;
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0 && v) atomicAdd(&sh_cnt[0], v);
+  for (int o = 16; o >= 1; o >>= 1) {
+    nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
+    nforced += __shfl_xor_sync(0xffffffffu, nforced, o);
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if (lane == 0) {
+    atomicAdd(&S.stat[0], nvalid);
+    atomicAdd(&S.stat[1], nforced);
+    atomicMin(&S.stat[2], kmin);
+    atomicMax(&S.stat[3], kmax);
   }
   cluster.sync();
-  int total_valid = 0;
-  for (int c = 0; c < csize; ++c) total_valid += *cluster.map_shared_rank(&sh_cnt[0], c);
-  const int k_eff = a.k < total_valid ? a.k : total_valid;
+  uint32_t tvalid = 0, tforced = 0, gmin = 0xFFFFFFFFu, gmax = 0;
+  for (int c = 0; c < csize; ++c) {
+    const uint32_t* rs = cluster.map_shared_rank(S.stat, c);
+    tvalid += rs[0];
+    tforced += rs[1];
+    gmin = min(gmin, rs[2]);
+    gmax = max(gmax, rs[3]);
+  }
+  const uint32_t k_eff = min((uint32_t)a.k, tvalid);
 
-  // ---- radix select --------------------------------------------------------
-  uint32_t T = 0, quota = 0;       // select keys > T, plus `quota` keys == T
-  if (k_eff < total_valid) {
-    uint32_t prefix = 0, k_rem = (uint32_t)k_eff;
+  // ---- find T and quota --------------------------------------------------------
+  uint32_t T = 0, quota = 0;            // select keys > T, plus `quota` keys == T
+  bool done = false;
+  if (k_eff == tvalid) {
+    done = true;                         // everything valid is selected
+  } else if (k_eff <= tforced) {
+    T = 0xFFFFFFFFu;                     // only forced keys (they all tie at the max key)
+    quota = k_eff;
+    done = true;
+  }
+  const uint32_t need = k_eff - tforced;  // rank among regular keys (>= 1 when !done)
+  bool fallback = false;
+  if (!done) {
+    // 2. adaptive histogram over [gmin, gmax]
+    // bin = (key - gmin) >> sh with the smallest sh that maps [gmin, gmax] into
+    // kBins bins: monotone and exact (no division)
+    const uint32_t span = gmax - gmin;
+    const int sh = span < (uint32_t)kBins ? 0 : (32 - __clz(span)) - 11;
+    for (int i = tid; i < len32; i += kTopkThreads) {
+      const uint32_t key = keys[i];
+      if (key != 0u && key != 0xFFFFFFFFu) {
+        atomicAdd(&S.hist[(key - gmin) >> sh], 1u);
+      }
+    }
+    cluster.sync();
+    for (int i = tid; i < kBins; i += kTopkThreads) {
+      uint32_t s = 0;
+      for (int c = 0; c < csize; ++c) s += *cluster.map_shared_rank(&S.hist[i], c);
+      S.ghist[i] = s;
+    }
+    __syncthreads();
+    // suffix scan over bins (descending): each warp owns 128 bins, lane 4 of them
+    {
+      const int b0 = kBins - 1 - (warp * 128 + lane * 4);
+      uint32_t c4[4], tot = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { c4[q] = S.ghist[b0 - q]; tot += c4[q]; }
+      uint32_t inc = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) S.scan[warp] = (int)inc;
+      __syncthreads();
+      uint32_t wpre = 0;
+      for (int w = 0; w < warp; ++w) wpre += (uint32_t)S.scan[w];
+      const uint32_t excl = wpre + inc - tot;
+      if (excl < need && excl + tot >= need) {
+        uint32_t run = excl;
+        for (int q = 0; q < 4; ++q) {
+          if (run + c4[q] >= need) { S.dec[0] = (uint32_t)(b0 - q); S.dec[1] = need - run; S.dec[2] = c4[q]; break; }
+          run += c4[q];
+        }
+      }
+      __syncthreads();
+    }
+    const uint32_t bstar = S.dec[0], need2 = S.dec[1], C = S.dec[2];
+    if (C <= (uint32_t)kCandCap) {
+      // 3. gather the bin's keys from every CTA, resolve T exactly
+      for (int i = tid; i < len32; i += kTopkThreads) {
+        const uint32_t key = keys[i];
+        if (key != 0u && key != 0xFFFFFFFFu && ((key - gmin) >> sh) == bstar) {
+          const uint32_t pos = atomicAdd(&S.stat[4], 1u);
+          S.cand[pos] = key;
+        }
+      }
+      cluster.sync();
+      uint32_t off = 0;
+      for (int c = 0; c < csize; ++c) {
+        const uint32_t nc = *cluster.map_shared_rank(&S.stat[4], c);
+        const uint32_t* rc = cluster.map_shared_rank(S.cand, c);
+        for (uint32_t i = tid; i < nc; i += kTopkThreads) S.gcand[off + i] = rc[i];
+        off += nc;
+      }
+      __syncthreads();
+      uint32_t above;
+      local_select(S.gcand, (int)C, need2, S, tid, warp, lane, T, above);
+      quota = need2 - above;
+    } else {
+      fallback = true;
+    }
+  }
+  if (fallback) {
+    // 4-pass MSB radix select over the cluster (8-bit digits), regular keys only
+    uint32_t prefix = 0, k_rem = need;
+    uint32_t* h2 = S.hist;                  // two 256-bin buffers: hist[0..255], hist[256..511]
+    cluster.sync();                          // everyone finished reading the 2048-bin histograms
+    for (int i = tid; i < 512; i += kTopkThreads) h2[i] = 0;
+    __syncthreads();
     for (int pass = 0; pass < 4; ++pass) {
       const int shift = 24 - 8 * pass;
-      const int buf = pass & 1;
+      uint32_t* hb = h2 + (pass & 1) * 256;
       const uint32_t hmask = pass == 0 ? 0u : (0xFFFFFFFFu << (shift + 8));
       for (int i = tid; i < len32; i += kTopkThreads) {
         const uint32_t key = keys[i];
-        const bool m = (key & hmask) == (prefix & hmask) && i < len;
+        const bool m = key != 0u && key != 0xFFFFFFFFu && (key & hmask) == (prefix & hmask);
         const uint32_t bin = m ? ((key >> shift) & 255u) : 256u;
         const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-        if (m && lane == __ffs(peers) - 1) atomicAdd(&hist[buf][bin], (uint32_t)__popc(peers));
+        if (m && lane == __ffs(peers) - 1) atomicAdd(&hb[bin], (uint32_t)__popc(peers));
       }
       cluster.sync();
-      // warp 0: sum the cluster's histograms and pick the digit
       if (warp == 0) {
-        uint32_t c8[8];
-        uint32_t tot = 0;
+        uint32_t c8[8], tot = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const int bin = 255 - (lane * 8 + q);             // lane 0 holds the top bins
+          const int bin = 255 - (lane * 8 + q);
           uint32_t s = 0;
-          for (int c = 0; c < csize; ++c) s += *cluster.map_shared_rank(&hist[buf][bin], c);
+          for (int c = 0; c < csize; ++c) s += *cluster.map_shared_rank(&hb[bin], c);
           c8[q] = s;
           tot += s;
         }
-        // inclusive scan of lane totals (descending-bin order)
         uint32_t inc = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -143,88 +338,69 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_cluster_kernel(TopkArgs 
           if (lane >= o) inc += y;
         }
         const uint32_t excl = inc - tot;
-        const bool hit = excl < k_rem && inc >= k_rem;
-        const uint32_t hb = __ballot_sync(0xffffffffu, hit);
-        const int src = __ffs(hb) - 1;
-        if (lane == src) {
+        const unsigned hbits = __ballot_sync(0xffffffffu, excl < k_rem && inc >= k_rem);
+        if (lane == __ffs(hbits) - 1) {
           uint32_t run = excl;
           for (int q = 0; q < 8; ++q) {
-            if (run + c8[q] >= k_rem) {
-              sh_dec[0] = (uint32_t)(255 - (lane * 8 + q));
-              sh_dec[1] = k_rem - run;
-              break;
-            }
+            if (run + c8[q] >= k_rem) { S.dec[0] = 255 - (lane * 8 + q); S.dec[1] = k_rem - run; break; }
             run += c8[q];
           }
         }
       }
-      // clear the other buffer (its last readers finished before this pass's sync)
-      for (int i = tid; i < 256; i += kTopkThreads) hist[buf ^ 1][i] = 0;
+      // clear the other buffer (its last remote readers finished before this sync)
+      for (int i = tid; i < 256; i += kTopkThreads) h2[((pass + 1) & 1) * 256 + i] = 0;
       __syncthreads();
-      prefix |= sh_dec[0] << shift;
-      k_rem = sh_dec[1];
+      prefix |= S.dec[0] << shift;
+      k_rem = S.dec[1];
     }
     T = prefix;
     quota = k_rem;
   }
-  // ---- stable compaction -----------------------------------------------------
-  // warp w scans a contiguous block of the slice in 32-key groups
+
+  // ---- stable compaction ------------------------------------------------------
   const int groups = len32 >> 5;
   const int gpw = (groups + kTopkWarps - 1) / kTopkWarps;
   const int g0 = warp * gpw;
   const int g1 = min(groups, g0 + gpw);
-  int gt_w = 0, eq_w = 0;
+  int eq_w = 0;
   for (int gi = g0; gi < g1; ++gi) {
-    const int i = gi * 32 + lane;
-    const uint32_t key = keys[i];
-    const bool valid = i < len && key != 0;
-    gt_w += __popc(__ballot_sync(0xffffffffu, valid && key > T));
-    eq_w += __popc(__ballot_sync(0xffffffffu, valid && key == T));
+    const uint32_t key = keys[gi * 32 + lane];
+    eq_w += __popc(__ballot_sync(0xffffffffu, key != 0u && key == T));
   }
-  int gt_tot, eq_tot;
-  const int gt_pre = block_excl_scan_warps(gt_w, sh_scan, warp, lane, gt_tot);
-  const int eq_pre = block_excl_scan_warps(eq_w, sh_scan, warp, lane, eq_tot);
-  if (tid == 0) { sh_cnt[1] = gt_tot; sh_cnt[2] = eq_tot; }
+  int eq_tot;
+  const int eq_pre = block_excl_scan_warps(eq_w, S.scan, warp, lane, eq_tot);
+  if (tid == 0) S.stat[6] = (uint32_t)eq_tot;
   cluster.sync();
-  int eq_before = 0, gt_before = 0;
-  for (int c = 0; c < crank; ++c) {
-    gt_before += *cluster.map_shared_rank(&sh_cnt[1], c);
-    eq_before += *cluster.map_shared_rank(&sh_cnt[2], c);
-  }
-  // emission: mode 0 emits every selected key; mode 1 only keys of shard `rank`
+  int eq_before = 0;
+  for (int c = 0; c < crank; ++c) eq_before += (int)*cluster.map_shared_rank(&S.stat[6], c);
   const int emit_lo = a.mode == 0 ? 0 : a.rank * a.k;
   const int emit_hi = a.mode == 0 ? n : (a.rank + 1) * a.k;
-  auto take = [&](uint32_t key, int eq_rank_global) -> bool {
-    return key > T || (key == T && (uint32_t)eq_rank_global < quota);
-  };
-  // pass 1: emitted count per warp
   int em_w = 0;
   {
     int eq_run = eq_before + eq_pre;
     for (int gi = g0; gi < g1; ++gi) {
       const int i = gi * 32 + lane;
       const uint32_t key = keys[i];
-      const bool valid = i < len && key != 0;
-      const bool isEq = valid && key == T;
-      const unsigned eb = __ballot_sync(0xffffffffu, isEq);
+      const bool valid = key != 0u;
+      const unsigned eb = __ballot_sync(0xffffffffu, valid && key == T);
       const int my_eq = eq_run + __popc(eb & ((1u << lane) - 1u));
       const int e = base + i;
-      const bool sel = valid && take(key, my_eq) && e >= emit_lo && e < emit_hi;
+      const bool sel = valid && (key > T || (key == T && (uint32_t)my_eq < quota)) &&
+                       e >= emit_lo && e < emit_hi;
       em_w += __popc(__ballot_sync(0xffffffffu, sel));
       eq_run += __popc(eb);
     }
   }
   int em_tot;
-  const int em_pre = block_excl_scan_warps(em_w, sh_scan, warp, lane, em_tot);
-  if (tid == 0) sh_cnt[3] = em_tot;
+  const int em_pre = block_excl_scan_warps(em_w, S.scan, warp, lane, em_tot);
+  if (tid == 0) S.stat[7] = (uint32_t)em_tot;
   cluster.sync();
   int em_before = 0, em_all = 0;
   for (int c = 0; c < csize; ++c) {
-    const int x = *cluster.map_shared_rank(&sh_cnt[3], c);
+    const int x = (int)*cluster.map_shared_rank(&S.stat[7], c);
     em_all += x;
     em_before += c < crank ? x : 0;
   }
-  // pass 2: write
   {
     int eq_run = eq_before + eq_pre;
     int pos = em_before + em_pre;
@@ -233,12 +409,12 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_cluster_kernel(TopkArgs 
     for (int gi = g0; gi < g1; ++gi) {
       const int i = gi * 32 + lane;
       const uint32_t key = keys[i];
-      const bool valid = i < len && key != 0;
-      const bool isEq = valid && key == T;
-      const unsigned eb = __ballot_sync(0xffffffffu, isEq);
+      const bool valid = key != 0u;
+      const unsigned eb = __ballot_sync(0xffffffffu, valid && key == T);
       const int my_eq = eq_run + __popc(eb & ((1u << lane) - 1u));
       const int e = base + i;
-      const bool sel = valid && take(key, my_eq) && e >= emit_lo && e < emit_hi;
+      const bool sel = valid && (key > T || (key == T && (uint32_t)my_eq < quota)) &&
+                       e >= emit_lo && e < emit_hi;
       const unsigned sb = __ballot_sync(0xffffffffu, sel);
       if (sel) {
         const int p = pos + __popc(sb & ((1u << lane) - 1u));
@@ -253,7 +429,6 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_cluster_kernel(TopkArgs 
       eq_run += __popc(eb);
     }
   }
-  // tail fill and count (CTA 0)
   if (crank == 0) {
     int32_t* orow = a.idx + (size_t)row * a.k;
     for (int p = em_all + tid; p < a.k; p += kTopkThreads) {
@@ -267,7 +442,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_cluster_kernel(TopkArgs 
 
 static socket_status launch_topk_common(TopkArgs a, int n_max_row, cudaStream_t st) {
   // cluster size: enough CTAs to keep the machine busy, slices fit in smem
-  const size_t kMaxSlice = 48 * 1024;   // keys per CTA (192 KB)
+  const size_t kMaxSlice = 40 * 1024;   // keys per CTA (160 KB)
   int cs = 1;
   while (cs < 16 && ((size_t)(n_max_row + cs - 1) / cs > kMaxSlice || a.rows * cs < kNumSMs))
     cs *= 2;
