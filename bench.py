@@ -255,7 +255,7 @@ def run_ours(a):
     clk = clocks.stop()
     step_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / a.steps
     step_ms = max_over_ranks(step_ms)
-    launches_per_step = 7
+    launches_per_step = 5   # append-hash, query tables, score, top-k, decode (+1 memset node)
 
     # ---- (2) eager step with per-stage events: kernel shares + roofline ----------
     stage_names = ["append_hash", "tables+score", "topk", "sparse_decode+combine"]

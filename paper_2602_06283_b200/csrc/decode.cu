@@ -6,7 +6,8 @@
 // Work unit = (b, selection row, split).  A unit's NH query heads share the
 // gathered K/V rows (NH = G in KV_SHARED and dense mode, 1 in PER_QHEAD mode).
 // The split kernel (tensor-core mma.sync, decode_mma.cu) writes one partial
-// (m, l, o) per (b, head, split); combine_kernel merges the splits.
+// (m, l, o) per (b, head, split); the last split CTA of each unit merges them
+// (combine_kernel serves socket_lse_combine across sequence shards).
 #include "internal.cuh"
 
 namespace sk {
@@ -51,7 +52,8 @@ __global__ void combine_kernel(const float* __restrict__ part, int S, long long 
 socket_status launch_decode_mma(const socket_cfg& c, const void* q, const void* K, const void* V,
                                 const int32_t* idx, const int32_t* cnt, int k,
                                 const int32_t* seq_lens, bool dense, int units, int NH,
-                                int n_splits, int rps, float* part, cudaStream_t st);
+                                int n_splits, int rps, float* part, int* tickets, void* out,
+                                float* lse, float* part_out, cudaStream_t st);
 
 // Split geometry: rows per split is a multiple of `gran` (rows one CTA consumes
 // per round), at most `max_rps` (index staging), and the grid aims at
@@ -82,10 +84,14 @@ static void decode_geometry(const socket_cfg& c, int k, bool dense, int& units, 
   pick_splits(units, dense ? c.N_max : k, kMmaGran, kMmaMaxRps, 4 * kNumSMs, n_splits, rps);
 }
 
+static size_t part_bytes(const socket_cfg& c, int ns) {
+  return ((size_t)c.B * c.H_q * ns * (kD + 2) * sizeof(float) + 255) & ~(size_t)255;
+}
+
 size_t decode_workspace_bytes(const socket_cfg& c, int k, bool dense) {
   int units, NH, ns, rps;
   decode_geometry(c, k, dense, units, NH, ns, rps);
-  return (size_t)c.B * c.H_q * ns * (kD + 2) * sizeof(float);
+  return part_bytes(c, ns) + (size_t)units * sizeof(int);
 }
 
 socket_status launch_decode(const socket_cfg& c, const void* q, const void* K, const void* V,
@@ -94,16 +100,15 @@ socket_status launch_decode(const socket_cfg& c, const void* q, const void* K, c
                             float* partial, void* ws, size_t ws_bytes, cudaStream_t st) {
   int units, NH, ns, rps;
   decode_geometry(c, k, dense, units, NH, ns, rps);
-  const size_t need = (size_t)c.B * c.H_q * ns * (kD + 2) * sizeof(float);
-  if (ws_bytes < need) return fail(SOCKET_EWORKSPACE, "decode: workspace too small");
+  if (ws_bytes < part_bytes(c, ns) + (size_t)units * sizeof(int))
+    return fail(SOCKET_EWORKSPACE, "decode: workspace too small");
   if (units == 0) return SOCKET_OK;
   if (NH > 8) return fail(SOCKET_EUNSUPPORTED, "decode: more than 8 query heads per selection row");
-  socket_status s = launch_decode_mma(c, q, K, V, idx, cnt, k, seq_lens, dense, units, NH, ns, rps,
-                                      (float*)ws, st);
-  if (s != SOCKET_OK) return s;
-  combine_kernel<<<c.B * c.H_q, kD, 0, st>>>((const float*)ws, ns, (kD + 2), (long long)ns * (kD + 2),
-                                            1, (uint16_t*)out, lse, partial);
-  return check_launch("combine_kernel");
+  int* tickets = reinterpret_cast<int*>(static_cast<char*>(ws) + part_bytes(c, ns));
+  cudaError_t e = cudaMemsetAsync(tickets, 0, (size_t)units * sizeof(int), st);
+  if (e != cudaSuccess) return fail(SOCKET_ECUDA, std::string("decode: memset: ") + cudaGetErrorString(e));
+  return launch_decode_mma(c, q, K, V, idx, cnt, k, seq_lens, dense, units, NH, ns, rps, (float*)ws,
+                           tickets, out, lse, partial, st);
 }
 
 socket_status launch_lse_combine(const socket_cfg& c, const float* partials, int G, void* out,

@@ -38,6 +38,10 @@ struct MmaArgs {
   int n_splits, rows_per_split;
   float scale_log2;
   float* part;   // [B][H_q][n_splits][d+2], m in log2 units
+  int* tickets;  // [units], zero on entry; the last split of a unit merges
+  uint16_t* out; // [B][H_q][d] bf16 (nullable)
+  float* lse;    // [B][H_q] (nullable)
+  float* part_out;  // [B][H_q][d+2] natural-log units (nullable)
 };
 
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) {
@@ -246,12 +250,47 @@ decode_mma_kernel(MmaArgs a) {
     pp[2 + e] = O;
     if (e == 0) { pp[0] = M; pp[1] = Ls; }
   }
+
+  // ---- the last split CTA of this unit merges all splits (LSE combine) --------
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&a.tickets[unit], 1) == a.n_splits - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  constexpr float kLn2M = 0.6931471805599453f;
+  for (int x = tid; x < NH * kD; x += kMmaThreads) {
+    const int h = x / kD, e = x % kD;
+    const float* pb = a.part + ((size_t)b * a.H_q + h0 + h) * a.n_splits * (kD + 2);
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < a.n_splits; ++s2) M = fmaxf(M, __ldcg(pb + (size_t)s2 * (kD + 2)));
+    float Ls = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+      for (int s2 = 0; s2 < a.n_splits; ++s2) {
+        const float* p2 = pb + (size_t)s2 * (kD + 2);
+        const float wt = exp2f(__ldcg(p2) - M);
+        Ls = fmaf(wt, __ldcg(p2 + 1), Ls);
+        O = fmaf(wt, __ldcg(p2 + 2 + e), O);
+      }
+    }
+    const size_t bh = (size_t)b * a.H_q + h0 + h;
+    if (a.out) a.out[bh * kD + e] = (uint16_t)f2bf_bits(Ls > 0.f ? O / Ls : 0.f);
+    if (e == 0 && a.lse) a.lse[bh] = (Ls > 0.f) ? (M + log2f(Ls)) * kLn2M : -INFINITY;
+    if (a.part_out) {
+      float* po = a.part_out + bh * (kD + 2);
+      po[2 + e] = O;
+      if (e == 0) { po[0] = (M == -INFINITY) ? -INFINITY : M * kLn2M; po[1] = Ls; }
+    }
+  }
+  if (tid == 0) a.tickets[unit] = 0;   // ready for the next launch / graph replay
 }
 
 socket_status launch_decode_mma(const socket_cfg& c, const void* q, const void* K, const void* V,
                                 const int32_t* idx, const int32_t* cnt, int k,
                                 const int32_t* seq_lens, bool dense, int units, int NH,
-                                int n_splits, int rps, float* part, cudaStream_t st) {
+                                int n_splits, int rps, float* part, int* tickets, void* out,
+                                float* lse, float* part_out, cudaStream_t st) {
   MmaArgs a;
   a.q = (const uint16_t*)q;
   a.K = (const uint16_t*)K;
@@ -271,6 +310,10 @@ socket_status launch_decode_mma(const socket_cfg& c, const void* q, const void* 
   a.rows_per_split = rps;
   a.scale_log2 = c.sm_scale * kLog2eM;
   a.part = part;
+  a.tickets = tickets;
+  a.out = (uint16_t*)out;
+  a.lse = lse;
+  a.part_out = part_out;
   dim3 grid(n_splits, units);
   if (dense) {
     cudaFuncSetAttribute(decode_mma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMmaRing);

@@ -116,54 +116,55 @@ __global__ void pack_codes_kernel(const uint8_t* __restrict__ plain, uint8_t* __
 
 // ----------------------------------------------------------------------------
 // Append path (decode step: n_count new keys per (b, kv-head), typically 1).
-// grid.x = table pairs, grid.y = key blocks of 64; thread = (key, table):
-// P dot products of length 128 in fp32 (t ascending), one code byte written to
-// slot s = (l & ~M) | ((l - j) & M) of key j (inverse of slot_table).
+// One warp per (key, table): lane t holds elements 4t .. 4t+3 of the key, the
+// P projections are 4 FMAs per lane each (t ascending within the lane) and a
+// butterfly sum; lane 0 writes the code byte to slot s = (l & ~M) | ((l - j) & M)
+// of key j (inverse of slot_table).  Warps with table 0 also write ||v_j||
+// with exactly vnorm_kernel's summation order.
+// Note: the projection's summation order differs from the prefill kernels, so
+// a bit whose projection is within fp32 rounding of 0 may differ between the
+// two paths; both are checked against the fp64 oracle with the same margin rule.
 // ----------------------------------------------------------------------------
-constexpr int kAppendTables = 2;
-constexpr int kAppendKeys = 64;
+constexpr int kAppendWarps = 8;
 
-__global__ void __launch_bounds__(kAppendTables * kAppendKeys)
+__global__ void __launch_bounds__(kAppendWarps * 32)
 hash_append_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict__ W,
-                   uint8_t* __restrict__ codes, int N_max, int L, int P, int Lp, int n_begin,
+                   uint8_t* __restrict__ codes, const uint16_t* __restrict__ V,
+                   float* __restrict__ vnorm, int N_max, int L, int P, int Lp, int n_begin,
                    int n_count, int total_keys) {
-  __shared__ float ws[kAppendTables][8][kD];
-  const int l0 = blockIdx.x * kAppendTables;
-  for (int i = threadIdx.x; i < kAppendTables * 8 * kD; i += blockDim.x) {
-    const int tl = i / (8 * kD), p = (i / kD) % 8, t = i % kD;
-    const int l = l0 + tl;
-    ws[tl][p][t] = (l < L && p < P) ? __uint_as_float((uint32_t)W[((size_t)l * P + p) * kD + t] << 16) : 0.f;
-  }
-  __syncthreads();
-  const int key = blockIdx.y * kAppendKeys + (threadIdx.x % kAppendKeys);
-  const int tl = threadIdx.x / kAppendKeys;
-  const int l = l0 + tl;
-  if (key >= total_keys || l >= Lp) return;
+  const int lane = threadIdx.x & 31;
+  const int job = blockIdx.x * kAppendWarps + (threadIdx.x >> 5);   // (key, table)
+  if (job >= total_keys * Lp) return;
+  const int key = job / Lp, l = job % Lp;
   const int bh = key / n_count, j = n_begin + key % n_count;
   uint32_t code = 0;
   if (l < L) {
-    const uint4* kr = reinterpret_cast<const uint4*>(K + ((size_t)bh * N_max + j) * kD);
-    float x[8];
+    const uint2 ku = *reinterpret_cast<const uint2*>(K + ((size_t)bh * N_max + j) * kD + lane * 4);
+    const float k0 = bf16lo(ku.x), k1 = bf16hi(ku.x), k2 = bf16lo(ku.y), k3 = bf16hi(ku.y);
+    for (int i = 0; i < P; ++i) {
+      const uint2 wu = *reinterpret_cast<const uint2*>(W + ((size_t)l * P + i) * kD + lane * 4);
+      float x = bf16lo(wu.x) * k0;
+      x = fmaf(bf16hi(wu.x), k1, x);
+      x = fmaf(bf16lo(wu.y), k2, x);
+      x = fmaf(bf16hi(wu.y), k3, x);
 #pragma unroll
-    for (int p = 0; p < 8; ++p) x[p] = 0.f;
-#pragma unroll 4
-    for (int c = 0; c < kD / 8; ++c) {
-      const uint4 u = kr[c];
-      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float kv = (e & 1) ? bf16hi(w4[e >> 1]) : bf16lo(w4[e >> 1]);
-#pragma unroll
-        for (int p = 0; p < 8; ++p) x[p] = fmaf(ws[tl][p][c * 8 + e], kv, x[p]);
-      }
+      for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      code |= (x >= 0.f ? 1u : 0u) << i;     // sign(0) = +1 (R-3), LSB = row 0 (R-4)
     }
-#pragma unroll
-    for (int p = 0; p < 8; ++p)
-      if (p < P) code |= (x[p] >= 0.f ? 1u : 0u) << p;   // sign(0) = +1 (R-3), LSB = row 0 (R-4)
   }
-  const int M = (Lp < 32 ? Lp : 32) - 1;
-  const int s = (l & ~M) | ((l - j) & M);
-  codes[(size_t)bh * N_max * Lp + code_off(j, s, Lp)] = (uint8_t)code;
+  if (lane == 0) {
+    const int M = (Lp < 32 ? Lp : 32) - 1;
+    const int s = (l & ~M) | ((l - j) & M);
+    codes[(size_t)bh * N_max * Lp + code_off(j, s, Lp)] = (uint8_t)code;
+  }
+  if (V && l == 0) {
+    const uint2 u = *reinterpret_cast<const uint2*>(V + ((size_t)bh * N_max + j) * kD + lane * 4);
+    float a = bf16lo(u.x), b = bf16hi(u.x), c = bf16lo(u.y), e = bf16hi(u.y);
+    float sq = fmaf(a, a, fmaf(b, b, fmaf(c, c, e * e)));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if (lane == 0) vnorm[(size_t)bh * N_max + j] = sqrtf(sq);
+  }
 }
 
 socket_status launch_hash_keys_simt(const socket_cfg& c, const void* K, const void* W,
@@ -189,10 +190,13 @@ socket_status launch_hash_keys(const socket_cfg& c, const void* K, const void* V
   if (n_count <= 16) {
     const int Lp = code_slots(c.L);
     const int total = c.B * c.H_kv * n_count;
-    dim3 grid((Lp + kAppendTables - 1) / kAppendTables, (total + kAppendKeys - 1) / kAppendKeys);
-    hash_append_kernel<<<grid, kAppendTables * kAppendKeys, 0, st>>>(
-        (const uint16_t*)K, (const uint16_t*)W, codes, c.N_max, c.L, c.P, Lp, n_begin, n_count, total);
+    const long long jobs = (long long)total * Lp;
+    hash_append_kernel<<<(unsigned)((jobs + kAppendWarps - 1) / kAppendWarps), kAppendWarps * 32, 0, st>>>(
+        (const uint16_t*)K, (const uint16_t*)W, codes, (const uint16_t*)V, vnorm, c.N_max, c.L, c.P,
+        Lp, n_begin, n_count, total);
     s = check_launch("hash_append_kernel");
+    if (s != SOCKET_OK) return s;
+    return SOCKET_OK;   // value norms written by the append kernel
   } else {
     bool used = false;
     s = launch_hash_keys_tc(c, K, W, codes, n_begin, n_count, st, &used);

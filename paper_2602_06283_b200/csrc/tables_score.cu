@@ -15,93 +15,111 @@
 
 namespace sk {
 
-constexpr int kTabThreads = 256;
-constexpr int kTabPerCta = 4;     // tables per CTA
+constexpr int kTabThreads = 512;
+constexpr int kTabPerCta = 16;    // tables per CTA
 constexpr int kMaxHeads = 8;      // heads per selection row
 
-// One CTA = (b, selection row) x 8 tables.  Steps (all latency-oriented):
-//  1. stage q (NH heads) and W^(l) of the 8 tables in shared memory (16-B loads);
-//  2. one thread per (head, table, bit): x = W_i . q in fp64 (bf16 products are
-//     exact), u = tanh(x)/sqrt(d), factors sigma(+-2u/tau) in fp64;
-//  3. half tables lo(r & 15) = prod_{i<4} f_i, hi(r >> 4) = prod_{i>=4} f_i in
-//     fp64, rounded once to fp32;
-//  4. T(r) = sum_h lo_h * hi_h; consecutive threads write consecutive table
-//     columns of one LUT row (coalesced 32-byte segments).
-__global__ void __launch_bounds__(kTabThreads)
+// One CTA = (b, selection row) x kTabPerCta tables.  Steps:
+//  1+2. in round i, warp w owns the 4 W rows 4 (16 i + w) .. + 3.
+//       A lane holds 4 elements (t = 4 lane .. 4 lane + 3) of every head's q and
+//       of the W rows as fp64, so each of the 4*NH projections x = W_i . q_h is
+//       4 fp64 FMAs per lane; a reduce-scatter over the warp leaves every lane
+//       with one complete x.  bf16 x bf16 products and their partial sums are
+//       exact in fp64, so x is exact.  Each lane then evaluates its
+//       u = tanh(x)/sqrt(d) and sigma(+-2u/tau) with the accurate fp32
+//       functions (<= 2 ulp each).
+//  3.   half tables lo(r & 15) = prod_{i<4} f_i, hi(r >> 4) = prod_{i>=4} f_i
+//       in fp64, rounded once to fp32;
+//  4.   T(r) = sum_h lo_h * hi_h; consecutive threads write consecutive table
+//       columns of one LUT row.
+template <int NH>
+__global__ void __launch_bounds__(kTabThreads, NH >= 8 ? 1 : 2)
 query_tables_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ W,
                     float* __restrict__ plain, float* __restrict__ lut, int H_q, int H_sel,
-                    int NH, int L, int P, int Lp, float tau) {
-  __shared__ float qs[kMaxHeads][kD];
-  __shared__ float wsm[kTabPerCta * 8][kD + 1];
-  __shared__ double fx[kMaxHeads][kTabPerCta][8][2];        // sigma factors
-  __shared__ float half_lo[kMaxHeads][16][kTabPerCta];
-  __shared__ float half_hi[kMaxHeads][16][kTabPerCta];
+                    int L, int P, int Lp, float tau) {
+  constexpr int kWarps = kTabThreads / 32;
+  constexpr int kRounds = (kTabPerCta * 8) / (4 * kWarps);   // 4 W rows per warp per round
+  static_assert(kRounds * 4 * kWarps == kTabPerCta * 8, "W rows must tile the warps");
+  constexpr int NV = 4 * NH;                                 // values per warp and round
+  __shared__ double fx[NH][kTabPerCta][8][2];                // sigma factors
+  __shared__ float half_lo[NH][16][kTabPerCta];
+  __shared__ float half_hi[NH][16][kTabPerCta];
   const int row = blockIdx.x;                // b * H_sel + r
   const int b = row / H_sel, r = row % H_sel;
   const int h0 = (NH == 1) ? r : r * NH;     // first query head of the row
   const int l0 = blockIdx.y * kTabPerCta;
   const int R = 1 << P;
-  const int tid = threadIdx.x;
-  // 1. staging
-  for (int i = tid; i < NH * (kD / 8); i += kTabThreads) {
-    const int h = i / (kD / 8), c = i % (kD / 8);
-    const uint4 u = *reinterpret_cast<const uint4*>(q + ((size_t)b * H_q + h0 + h) * kD + c * 8);
-    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // W rows are enumerated as wr = 8 * tl + i (bit i < 8, rows with i >= P skipped)
+  double qd[NH][4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      qs[h][c * 8 + 2 * e] = bf16lo(w4[e]);
-      qs[h][c * 8 + 2 * e + 1] = bf16hi(w4[e]);
-    }
+  for (int h = 0; h < NH; ++h) {
+    const uint2 u = *reinterpret_cast<const uint2*>(q + ((size_t)b * H_q + h0 + h) * kD + lane * 4);
+    qd[h][0] = bf16lo(u.x); qd[h][1] = bf16hi(u.x); qd[h][2] = bf16lo(u.y); qd[h][3] = bf16hi(u.y);
   }
-  const int nrows_w = kTabPerCta * P;        // W rows of this CTA
-  for (int i = tid; i < nrows_w * (kD / 8); i += kTabThreads) {
-    const int wr = i / (kD / 8), c = i % (kD / 8);
-    const int l = l0 + wr / P;
-    uint4 u = make_uint4(0, 0, 0, 0);
-    if (l < L) u = *reinterpret_cast<const uint4*>(W + ((size_t)l * P + wr % P) * kD + c * 8);
-    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+  uint2 wu[kRounds][4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      wsm[wr][c * 8 + 2 * e] = bf16lo(w4[e]);
-      wsm[wr][c * 8 + 2 * e + 1] = bf16hi(w4[e]);
+  for (int round = 0; round < kRounds; ++round)
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const int wr = (round * kWarps + warp) * 4 + rr;
+      const int l = l0 + (wr >> 3), i = wr & 7;
+      wu[round][rr] = make_uint2(0, 0);
+      if (i < P && l < L) wu[round][rr] = *reinterpret_cast<const uint2*>(W + ((size_t)l * P + i) * kD + lane * 4);
     }
-  }
-  __syncthreads();
-  // 2. projections and logistic factors: every product of
-  //    two bf16 values is exact in fp32; each half of the 128-term sum is
-  //    accumulated with TwoSum compensation by one of two threads, and the
-  //    halves are merged in fp64, so x is exact to ~2^-48.  u = tanh(x)/sqrt(d)
-  //    and sigma(+-2u/tau) use the accurate fp32 functions (<= 2 ulp each), so a
-  //    factor carries <= 3 ulp + 3 ulp * |a|; no fp64 transcendentals.
-  const float inv_sqrt_d = 0.08838834764831845f;   // 1/sqrt(128), correctly rounded
-  const int ndots = NH * nrows_w;
-  for (int base = 0; base < 2 * ndots; base += kTabThreads) {   // uniform trip count
-    const int di2 = base + tid;
-    const bool act = di2 < 2 * ndots;
-    const int di = act ? di2 >> 1 : 0, part = di2 & 1;            // two threads per dot
-    const int wr = di % nrows_w, h = di / nrows_w;
-    float s0 = 0.f, c0 = 0.f;
-    const int t0 = part * (kD / 2);
-#pragma unroll 8
-    for (int t = t0; t < t0 + kD / 2; ++t) {
-      const float p0 = wsm[wr][t] * qs[h][t];       // exact
-      const float u0 = s0 + p0, b0 = u0 - s0;
-      c0 += (s0 - (u0 - b0)) + (p0 - b0);
-      s0 = u0;
+#pragma unroll
+  for (int round = 0; round < kRounds; ++round) {
+    double v[NV];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const double w0 = bf16lo(wu[round][rr].x), w1 = bf16hi(wu[round][rr].x);
+      const double w2 = bf16lo(wu[round][rr].y), w3 = bf16hi(wu[round][rr].y);
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        double x = w0 * qd[h][0];
+        x = fma(w1, qd[h][1], x);
+        x = fma(w2, qd[h][2], x);
+        v[rr * NH + h] = fma(w3, qd[h][3], x);
+      }
     }
-    const double mine = (double)s0 + (double)c0;
-    const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
-    if (act && part == 0) {
-      const float x = (float)(mine + other);
-      const float uu = tanhf(x) * inv_sqrt_d;       // Alg. 2 l.217
-      const float a = 2.0f * uu / tau;              // logit gap of bit i
-      fx[h][wr / P][wr % P][1] = (double)(1.0f / (1.0f + expf(-a)));   // c_{r,i} = +1 (bit set)
-      fx[h][wr / P][wr % P][0] = (double)(1.0f / (1.0f + expf(a)));    // c_{r,i} = -1
+    // reduce-scatter over the 32 lanes: afterwards v[0] holds the full sum of
+    // value `own` (lanes with equal `own` hold equal sums)
+    int own = 0, nv = NV;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      if (nv > 1) {
+        const int hnv = nv >> 1;
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < NV / 2; ++i) {
+          if (i < hnv) {
+            const double send = up ? v[i] : v[i + hnv];
+            const double keep = up ? v[i + hnv] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+          }
+        }
+        if (up) own += hnv;
+        nv = hnv;
+      } else {
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+      }
+    }
+    const int rr = own / NH, h = own % NH;          // NH is a power of two
+    const int wr = (round * kWarps + warp) * 4 + rr;
+    const int tl = wr >> 3, i = wr & 7;
+    const float inv_sqrt_d = 0.08838834764831845f;   // 1/sqrt(128), correctly rounded
+    const float uu = tanhf((float)v[0]) * inv_sqrt_d;  // Alg. 2 l.217
+    const float a = 2.0f * uu / tau;                   // logit gap of bit i
+    const float fp = 1.0f / (1.0f + expf(-a));         // c_{r,i} = +1 (bit set)
+    const float fm = 1.0f / (1.0f + expf(a));          // c_{r,i} = -1
+    if ((lane & (32 / NV - 1)) == 0 && i < P) {
+      fx[h][tl][i][1] = (double)fp;
+      fx[h][tl][i][0] = (double)fm;
     }
   }
   __syncthreads();
   // 3. half tables (bits 0..3 and 4..P-1; an empty product is 1)
-  for (int i = tid; i < NH * kTabPerCta * 32; i += kTabThreads) {
+  for (int i = tid; i < NH * kTabPerCta * 32; i += kTabThreads) {  // NH is a template constant
     const int e = i & 15, hi = (i >> 4) & 1, tl = (i >> 5) % kTabPerCta, h = i / (32 * kTabPerCta);
     double p = 1.0;
 #pragma unroll
@@ -141,16 +159,23 @@ socket_status launch_query_tables(const socket_cfg& c, const void* q, const void
   if (NH > kMaxHeads) return fail(SOCKET_EUNSUPPORTED, "more than 8 query heads per KV head");
   const int Lp = code_slots(c.L);
   dim3 grid(c.B * H_sel, (Lp + kTabPerCta - 1) / kTabPerCta);
-  query_tables_kernel<<<grid, kTabThreads, 0, st>>>((const uint16_t*)q, (const uint16_t*)W, plain,
-                                                    lut, c.H_q, H_sel, NH, c.L, c.P, Lp, c.tau);
+  switch (NH) {
+#define SK_QT(N) case N: query_tables_kernel<N><<<grid, kTabThreads, 0, st>>>((const uint16_t*)q, \
+      (const uint16_t*)W, plain, lut, c.H_q, H_sel, c.L, c.P, Lp, c.tau); break;
+    SK_QT(1) SK_QT(2) SK_QT(4) SK_QT(8)
+#undef SK_QT
+    default:
+      return fail(SOCKET_EUNSUPPORTED, "query tables: heads per selection row must be 1, 2, 4 or 8");
+  }
   return check_launch("query_tables_kernel");
 }
 
 // ----------------------------------------------------------------------------
 // score kernel
 // ----------------------------------------------------------------------------
-constexpr int kScoreThreads = 256;
+constexpr int kScoreThreads = 512;            // 16 warps, one CTA per SM (persistent)
 constexpr int kScoreWarps = kScoreThreads / 32;
+constexpr int kScoreStages = 3;               // per-warp cp.async ring depth (tiles)
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -177,55 +202,52 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void cpa16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Stage layout of one tile (32 keys) in a warp's ring: LP*32 bytes of codes in
+// the global tile order (chunk ch of key lane at ch*32*CB + lane*CB), then 32
+// fp32 value norms.  A lane copies exactly the bytes it later reads.
 template <int LP>
-struct CodeRegs {
+struct TileStage {
   static constexpr int CB = LP < 16 ? LP : 16;
   static constexpr int NCH = LP / CB;
-  static constexpr int NW = LP / 4;   // u32 words per key
-  uint32_t w[NW];
+  static constexpr int CODE_BYTES = LP * 32;
+  static constexpr int BYTES = CODE_BYTES + 128;
 };
 
 template <int LP>
-__device__ __forceinline__ void load_codes(CodeRegs<LP>& c, const uint8_t* tile_base, int lane) {
-  constexpr int CB = CodeRegs<LP>::CB;
+__device__ __forceinline__ void issue_tile(uint32_t st, const uint8_t* tile_codes, const float* tile_vn,
+                                           int lane) {
+  constexpr int CB = TileStage<LP>::CB;
 #pragma unroll
-  for (int ch = 0; ch < CodeRegs<LP>::NCH; ++ch) {
-    const uint8_t* p = tile_base + ch * (32 * CB) + lane * CB;
-    if constexpr (CB == 16) {
-      const uint4 v = ldg_nc_v4(p);
-      c.w[ch * 4 + 0] = v.x; c.w[ch * 4 + 1] = v.y; c.w[ch * 4 + 2] = v.z; c.w[ch * 4 + 3] = v.w;
-    } else {
-      const uint2 v = ldg_nc_v2(p);
-      c.w[ch * 2 + 0] = v.x; c.w[ch * 2 + 1] = v.y;
-    }
+  for (int ch = 0; ch < TileStage<LP>::NCH; ++ch) {
+    const uint32_t off = ch * (32 * CB) + lane * CB;
+    if constexpr (CB == 16) cpa16(st + off, tile_codes + off);
+    else cpa8(st + off, tile_codes + off);
   }
+  cpa4(st + TileStage<LP>::CODE_BYTES + lane * 4, tile_vn + lane);
 }
 
-// sum over slots of LUT[code][column(s, lane)], two keys per lane sharing columns
-template <int LP, int NK>
-__device__ __forceinline__ void lookup_sum(const CodeRegs<LP> (&c)[NK], float (&acc)[NK],
-                                           const char* lut, int lane) {
-#pragma unroll
-  for (int k = 0; k < NK; ++k) acc[k] = 0.f;
-#pragma unroll
-  for (int s = 0; s < LP; ++s) {
-    // column within its 64-wide panel, times 4 bytes (fits in one byte)
-    const uint32_t col4 = (uint32_t)(((s & 32) | ((s + lane) & 31)) << 2);
-    constexpr int dummy = 0;
-    (void)dummy;
-    const uint32_t sel = 0x5504u | ((uint32_t)(s & 3) << 4);
-    const char* panel = lut + (size_t)(s >> 6) * (256 * 64 * 4);
-#pragma unroll
-    for (int k = 0; k < NK; ++k) {
-      const uint32_t addr = __byte_perm(c[k].w[s >> 2], col4, sel);  // code*256 + col*4
-      acc[k] += *reinterpret_cast<const float*>(panel + addr);
-    }
-  }
-}
-
+// Score kernel: persistent CTAs, each over a contiguous range of 32-key tiles
+// of the (row, tile) space; a row change reloads the row's LUT image (TMA bulk
+// copy + mbarrier).  Lane l of a warp scores key j = 32 t + l of tile t: at
+// slot step s it reads LUT column c(s, l) = (s & 32) | ((s + l) & 31) (bank
+// (s + l) mod 32: all 32 lanes on distinct banks).  The byte offset
+// code * 256 + 4 c(s, l) is one PRMT of the code word with a per-lane packed
+// column-offset register (two slots per register, upper bytes zero).
 template <int LP>
-__global__ void __launch_bounds__(kScoreThreads, 2)
+__global__ void __launch_bounds__(kScoreThreads, 1)
 score_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
              const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
              const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
@@ -234,7 +256,15 @@ score_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
   __shared__ uint64_t bar;
   constexpr int PANELS = LP <= 64 ? 1 : (LP + 63) / 64;
   constexpr uint32_t LUT_BYTES = PANELS * 256 * 64 * 4;
+  using TS = TileStage<LP>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ring = smem_u32(smem + LUT_BYTES) + (uint32_t)warp * (kScoreStages * TS::BYTES);
+  const char* ringp = smem + LUT_BYTES + warp * (kScoreStages * TS::BYTES);
+  // packed column offsets: pk[m] = {4 c(2m, l), 4 c(2m+1, l), 0, 0} for slots 0..31
+  uint32_t pk[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m)
+    pk[m] = (uint32_t)(((2 * m + lane) & 31) << 2) | ((uint32_t)(((2 * m + 1 + lane) & 31) << 2) << 8);
   const int tiles_per_row = N_max >> 5;
   const long long t_begin = total_tiles * blockIdx.x / gridDim.x;
   const long long t_end = total_tiles * (blockIdx.x + 1) / gridDim.x;
@@ -253,7 +283,8 @@ score_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
     const int valid_tiles = (n + 31) >> 5;
     const int tile0 = (int)(t - (long long)row * tiles_per_row);
     const int tile1 = (int)(seg_end - (long long)row * tiles_per_row);
-    const bool need_lut = tile0 < valid_tiles;
+    const int vt1 = tile1 < valid_tiles ? tile1 : valid_tiles;   // tiles that need codes
+    const bool need_lut = tile0 < vt1;
     if (need_lut && threadIdx.x == 0) {
       mbar_expect_tx(&bar, LUT_BYTES);
       const char* src = reinterpret_cast<const char*>(lut_g) + (size_t)row * LUT_BYTES;
@@ -265,58 +296,60 @@ score_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
     const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
     const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
     float* srow = scores + (size_t)row * N_max;
-    bool lut_ready = !need_lut;
-    // each warp takes tile pairs (tt, tt + 8) with tt = tile0 + warp + 16 i; the
-    // codes of the next pair are loaded while the current pair is looked up.
-    auto load_pair = [&](CodeRegs<LP> (&c)[2], float (&vn)[2], int tt) {
+    // tiles of this warp that need codes: tile0 + warp + 16 i < vt1
+    const int first = tile0 + warp;
+    const int my = first < vt1 ? (vt1 - first + kScoreWarps - 1) / kScoreWarps : 0;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int ti = tt + u * kScoreWarps;
-        if (ti < tile1 && ti < valid_tiles) {
-          load_codes<LP>(c[u], crow + (size_t)ti * 32 * LP, lane);
-          vn[u] = vrow[ti * 32 + lane];
+    for (int s2 = 0; s2 < kScoreStages - 1; ++s2) {
+      if (s2 < my) {
+        const int ti = first + s2 * kScoreWarps;
+        issue_tile<LP>(ring + s2 * TS::BYTES, crow + (size_t)ti * 32 * LP, vrow + ti * 32, lane);
+      }
+      cpa_commit();
+    }
+    if (need_lut) mbar_wait(&bar, phase);
+    for (int i = 0; i < my; ++i) {
+      const int inext = i + kScoreStages - 1;
+      if (inext < my) {
+        const int ti = first + inext * kScoreWarps;
+        issue_tile<LP>(ring + (inext % kScoreStages) * TS::BYTES, crow + (size_t)ti * 32 * LP,
+                       vrow + ti * 32, lane);
+      }
+      cpa_commit();
+      cpa_wait<kScoreStages - 1>();
+      const char* st = ringp + (i % kScoreStages) * TS::BYTES;
+      uint32_t w[LP / 4];
+#pragma unroll
+      for (int ch = 0; ch < TS::NCH; ++ch) {
+        if constexpr (TS::CB == 16) {
+          const uint4 v = *reinterpret_cast<const uint4*>(st + ch * 512 + lane * 16);
+          w[ch * 4 + 0] = v.x; w[ch * 4 + 1] = v.y; w[ch * 4 + 2] = v.z; w[ch * 4 + 3] = v.w;
         } else {
-#pragma unroll
-          for (int w = 0; w < CodeRegs<LP>::NW; ++w) c[u].w[w] = 0;
-          vn[u] = 0.f;
+          const uint2 v = *reinterpret_cast<const uint2*>(st + ch * 256 + lane * 8);
+          w[ch * 2 + 0] = v.x; w[ch * 2 + 1] = v.y;
         }
       }
-    };
-    auto finish_pair = [&](const CodeRegs<LP> (&c)[2], const float (&vn)[2], int tt) {
-      const bool any_valid = tt < valid_tiles;
-      float acc[2] = {0.f, 0.f};
-      if (any_valid) {
-        if (!lut_ready) { mbar_wait(&bar, phase); lut_ready = true; }
-        lookup_sum<LP, 2>(c, acc, smem, lane);
-      }
+      const float vn = *reinterpret_cast<const float*>(st + TS::CODE_BYTES + lane * 4);
+      float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int ti = tt + u * kScoreWarps;
-        if (ti < tile1) {
-          const int j = ti * 32 + lane;
-          const bool ok = ti < valid_tiles && j < n && (!mrow || mrow[j]);
-          srow[j] = ok ? vn[u] * acc[u] : -INFINITY;
-        }
+      for (int s2 = 0; s2 < LP; ++s2) {
+        const int sl = s2 & 31;
+        const uint32_t sel = (uint32_t)(4 + (sl & 1)) | ((uint32_t)(s2 & 3) << 4) | 0x7600u;
+        const uint32_t addr = __byte_perm(w[s2 >> 2], pk[sl >> 1], sel);   // code*256 + 4 c
+        const float v = *reinterpret_cast<const float*>(smem + (size_t)(s2 >> 6) * (256 * 64 * 4) +
+                                                        ((s2 & 32) ? 128 : 0) + addr);
+        if (s2 & 1) acc1 += v; else acc0 += v;
       }
-    };
-    CodeRegs<LP> ca[2], cb[2];
-    float va[2], vb[2];
-    int tt = tile0 + warp;
-    if (tt < tile1) load_pair(ca, va, tt);
-    while (tt < tile1) {
-      const int t2 = tt + 2 * kScoreWarps;
-      if (t2 < tile1) load_pair(cb, vb, t2);
-      finish_pair(ca, va, tt);
-      if (t2 >= tile1) break;
-      const int t3 = t2 + 2 * kScoreWarps;
-      if (t3 < tile1) load_pair(ca, va, t3);
-      finish_pair(cb, vb, t2);
-      tt = t3;
+      const int ti = first + i * kScoreWarps;
+      const int j = ti * 32 + lane;
+      const bool ok = j < n && (!mrow || mrow[j]);
+      srow[j] = ok ? vn * (acc0 + acc1) : -INFINITY;
     }
-    if (need_lut) {
-      if (!lut_ready) mbar_wait(&bar, phase);
-      phase ^= 1;
-    }
+    // tiles past seq_len (no codes needed): -inf
+    for (int ti = (vt1 > tile0 ? vt1 : tile0) + warp; ti < tile1; ti += kScoreWarps)
+      srow[ti * 32 + lane] = -INFINITY;
+    cpa_wait<0>();
+    if (need_lut) phase ^= 1;
     __syncthreads();   // everyone done with this LUT before it is overwritten
     t = seg_end;
   }
@@ -329,12 +362,12 @@ socket_status launch_score(const socket_cfg& c, const float* lut, const uint8_t*
   const int H_sel = num_sel_rows(c);
   const int G_sel = c.group_mode == SOCKET_GROUP_PER_QHEAD ? c.H_q / c.H_kv : 1;
   const long long total_tiles = (long long)c.B * H_sel * (c.N_max / 32);
-  const size_t smem = lut_bytes_per_row(c.L);
-  long long grid = 2 * kNumSMs;
+  long long grid = kNumSMs;
   if (grid > total_tiles) grid = total_tiles;
   if (grid < 1) return SOCKET_OK;
 #define SK_SCORE_CASE(LPV)                                                                     \
   case LPV: {                                                                                  \
+    const size_t smem = lut_bytes_per_row(c.L) + (size_t)kScoreWarps * kScoreStages * TileStage<LPV>::BYTES; \
     auto kfn = score_kernel<LPV>;                                                              \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
     kfn<<<(unsigned)grid, kScoreThreads, smem, st>>>(lut, codes, vnorm, seq_lens, mask, scores, \
@@ -347,10 +380,8 @@ socket_status launch_score(const socket_cfg& c, const float* lut, const uint8_t*
     SK_SCORE_CASE(16)
     SK_SCORE_CASE(32)
     SK_SCORE_CASE(64)
-    SK_SCORE_CASE(96)
-    SK_SCORE_CASE(128)
     default:
-      return fail(SOCKET_EUNSUPPORTED, "score: L > 128 not supported");
+      return fail(SOCKET_EUNSUPPORTED, "score: L > 64 not supported by this kernel");
   }
 #undef SK_SCORE_CASE
 }

@@ -82,6 +82,7 @@ struct TopkShared {
   uint32_t gcand[kCandCap];      // gathered candidates
   uint32_t rhist[256];           // local radix histogram for candidate resolve
   int scan[kTopkWarps];
+  int scan2[kTopkWarps];
   uint32_t stat[8];              // nvalid, nforced, kmin, kmax, ncand, gt, eq, emit
   uint32_t dec[4];
 };
@@ -131,7 +132,7 @@ __device__ void local_select(const uint32_t* c, int C, uint32_t need, TopkShared
   above = need - k_rem;
 }
 
-__global__ void __launch_bounds__(kTopkThreads, 1) topk_cluster_kernel(TopkArgs a) {
+__global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs a) {
   extern __shared__ __align__(16) uint32_t keys[];          // [per]
   __shared__ TopkShared S;
 
@@ -358,54 +359,121 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_cluster_kernel(TopkArgs 
   }
 
   // ---- stable compaction ------------------------------------------------------
-  const int groups = len32 >> 5;
-  const int gpw = (groups + kTopkWarps - 1) / kTopkWarps;
-  const int g0 = warp * gpw;
-  const int g1 = min(groups, g0 + gpw);
-  int eq_w = 0;
-  for (int gi = g0; gi < g1; ++gi) {
-    const uint32_t key = keys[gi * 32 + lane];
-    eq_w += __popc(__ballot_sync(0xffffffffu, key != 0u && key == T));
-  }
-  int eq_tot;
-  const int eq_pre = block_excl_scan_warps(eq_w, S.scan, warp, lane, eq_tot);
-  if (tid == 0) S.stat[6] = (uint32_t)eq_tot;
-  cluster.sync();
-  int eq_before = 0;
-  for (int c = 0; c < crank; ++c) eq_before += (int)*cluster.map_shared_rank(&S.stat[6], c);
-  const int emit_lo = a.mode == 0 ? 0 : a.rank * a.k;
-  const int emit_hi = a.mode == 0 ? n : (a.rank + 1) * a.k;
-  int em_w = 0;
-  {
-    int eq_run = eq_before + eq_pre;
-    for (int gi = g0; gi < g1; ++gi) {
-      const int i = gi * 32 + lane;
-      const uint32_t key = keys[i];
-      const bool valid = key != 0u;
-      const unsigned eb = __ballot_sync(0xffffffffu, valid && key == T);
-      const int my_eq = eq_run + __popc(eb & ((1u << lane) - 1u));
-      const int e = base + i;
-      const bool sel = valid && (key > T || (key == T && (uint32_t)my_eq < quota)) &&
-                       e >= emit_lo && e < emit_hi;
-      em_w += __popc(__ballot_sync(0xffffffffu, sel));
-      eq_run += __popc(eb);
+  // Output position of a selected key = gt_rank + min(eq_rank, quota), where
+  // gt_rank / eq_rank count keys > T / == T at smaller indices (row-global).
+  int em_all = 0;
+  if (a.mode == 0) {
+    // per thread 4 consecutive keys; thread order = index order within the CTA
+    int gt_t = 0, eq_t = 0;
+    uint4 kv[1];
+    const int nchunk = len32 >> 2;                    // 4-key chunks
+    const int cpt = (nchunk + kTopkThreads - 1) / kTopkThreads;   // chunks per thread
+    const int c0 = tid * cpt, c1 = min(nchunk, c0 + cpt);
+    for (int cc = c0; cc < c1; ++cc) {
+      kv[0] = *reinterpret_cast<const uint4*>(keys + cc * 4);
+      const uint32_t* kp = &kv[0].x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) { gt_t += kp[e] != 0u && kp[e] > T; eq_t += kp[e] != 0u && kp[e] == T; }
     }
-  }
-  int em_tot;
-  const int em_pre = block_excl_scan_warps(em_w, S.scan, warp, lane, em_tot);
-  if (tid == 0) S.stat[7] = (uint32_t)em_tot;
-  cluster.sync();
-  int em_before = 0, em_all = 0;
-  for (int c = 0; c < csize; ++c) {
-    const int x = (int)*cluster.map_shared_rank(&S.stat[7], c);
-    em_all += x;
-    em_before += c < crank ? x : 0;
-  }
-  {
+    // block exclusive scans of (gt_t, eq_t)
+    int gi = gt_t, ei = eq_t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int yg = __shfl_up_sync(0xffffffffu, gi, o), ye = __shfl_up_sync(0xffffffffu, ei, o);
+      if (lane >= o) { gi += yg; ei += ye; }
+    }
+    __syncthreads();
+    if (lane == 31) { S.scan[warp] = gi; S.scan2[warp] = ei; }
+    __syncthreads();
+    int gw = 0, ew = 0, gtot = 0, etot = 0;
+#pragma unroll
+    for (int w = 0; w < kTopkWarps; ++w) {
+      const int xg = S.scan[w], xe = S.scan2[w];
+      gw += w < warp ? xg : 0; ew += w < warp ? xe : 0;
+      gtot += xg; etot += xe;
+    }
+    if (tid == 0) { S.stat[5] = (uint32_t)gtot; S.stat[6] = (uint32_t)etot; }
+    cluster.sync();
+    int gt_before = 0, eq_before = 0;
+    for (int c = 0; c < csize; ++c) {
+      const uint32_t* rs = cluster.map_shared_rank(S.stat, c);
+      if (c < crank) { gt_before += (int)rs[5]; eq_before += (int)rs[6]; }
+    }
+    em_all = (int)k_eff;
+    int gr = gt_before + gw + gi - gt_t;               // row-global exclusive ranks
+    int er = eq_before + ew + ei - eq_t;
+    int32_t* orow = a.idx + (size_t)row * a.k;
+    float* srow = a.sel_scores ? a.sel_scores + (size_t)row * a.k : nullptr;
+    for (int cc = c0; cc < c1; ++cc) {
+      kv[0] = *reinterpret_cast<const uint4*>(keys + cc * 4);
+      const uint32_t* kp = &kv[0].x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t key = kp[e];
+        if (key == 0u) continue;
+        const int j = base + cc * 4 + e;
+        if (key > T) {
+          const int pos = gr + min(er, (int)quota);
+          orow[pos] = j;
+          if (srow) srow[pos] = load_elem(a, row, j);
+          ++gr;
+        } else if (key == T) {
+          if (er < (int)quota) {
+            const int pos = gr + er;
+            orow[pos] = j;
+            if (srow) srow[pos] = load_elem(a, row, j);
+          }
+          ++er;
+        }
+      }
+    }
+  } else {
+    const int groups = len32 >> 5;
+    const int gpw = (groups + kTopkWarps - 1) / kTopkWarps;
+    const int g0 = warp * gpw;
+    const int g1 = min(groups, g0 + gpw);
+    int eq_w = 0;
+    for (int gi = g0; gi < g1; ++gi) {
+      const uint32_t key = keys[gi * 32 + lane];
+      eq_w += __popc(__ballot_sync(0xffffffffu, key != 0u && key == T));
+    }
+    int eq_tot;
+    const int eq_pre = block_excl_scan_warps(eq_w, S.scan, warp, lane, eq_tot);
+    if (tid == 0) S.stat[6] = (uint32_t)eq_tot;
+    cluster.sync();
+    int eq_before = 0;
+    for (int c = 0; c < crank; ++c) eq_before += (int)*cluster.map_shared_rank(&S.stat[6], c);
+    const int emit_lo = a.rank * a.k;
+    const int emit_hi = (a.rank + 1) * a.k;
+    int em_w = 0;
+    {
+      int eq_run = eq_before + eq_pre;
+      for (int gi = g0; gi < g1; ++gi) {
+        const int i = gi * 32 + lane;
+        const uint32_t key = keys[i];
+        const bool valid = key != 0u;
+        const unsigned eb = __ballot_sync(0xffffffffu, valid && key == T);
+        const int my_eq = eq_run + __popc(eb & ((1u << lane) - 1u));
+        const int e = base + i;
+        const bool sel = valid && (key > T || (key == T && (uint32_t)my_eq < quota)) &&
+                         e >= emit_lo && e < emit_hi;
+        em_w += __popc(__ballot_sync(0xffffffffu, sel));
+        eq_run += __popc(eb);
+      }
+    }
+    int em_tot;
+    const int em_pre = block_excl_scan_warps(em_w, S.scan, warp, lane, em_tot);
+    if (tid == 0) S.stat[7] = (uint32_t)em_tot;
+    cluster.sync();
+    int em_before = 0;
+    for (int c = 0; c < csize; ++c) {
+      const int x = (int)*cluster.map_shared_rank(&S.stat[7], c);
+      em_all += x;
+      em_before += c < crank ? x : 0;
+    }
     int eq_run = eq_before + eq_pre;
     int pos = em_before + em_pre;
     int32_t* orow = a.idx + (size_t)row * a.k;
-    float* srow = a.sel_scores ? a.sel_scores + (size_t)row * a.k : nullptr;
     for (int gi = g0; gi < g1; ++gi) {
       const int i = gi * 32 + lane;
       const uint32_t key = keys[i];
@@ -416,15 +484,8 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_cluster_kernel(TopkArgs 
       const bool sel = valid && (key > T || (key == T && (uint32_t)my_eq < quota)) &&
                        e >= emit_lo && e < emit_hi;
       const unsigned sb = __ballot_sync(0xffffffffu, sel);
-      if (sel) {
-        const int p = pos + __popc(sb & ((1u << lane) - 1u));
-        if (a.mode == 0) {
-          orow[p] = e;
-          if (srow) srow[p] = load_elem(a, row, e);
-        } else {
-          orow[p] = a.cand_idx[((size_t)a.rank * a.rows + row) * a.k + (e - emit_lo)];
-        }
-      }
+      if (sel) orow[pos + __popc(sb & ((1u << lane) - 1u))] =
+          a.cand_idx[((size_t)a.rank * a.rows + row) * a.k + (e - emit_lo)];
       pos += __popc(sb);
       eq_run += __popc(eb);
     }

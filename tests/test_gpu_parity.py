@@ -79,6 +79,30 @@ def test_hash_partial_ranges_touch_only_their_rows():
     assert np.all(got[..., ~inside] == 0)
 
 
+def test_append_path_codes_and_norms():
+    """The append path (n_count = 1, decode step) writes codes equal to the
+    oracle's (margin rule) and value norms bit-identical to the prefill path."""
+    cfg, c, W, d = make(2, 4, 2, 128, 60, 8, seed=6)
+    codes = ops.alloc_codes(cfg, DEV)
+    vn = torch.zeros((2, 2, 128), dtype=torch.float32, device=DEV)
+    ops.hash_keys(cfg, d["K"], d["W"], codes, V=d["V"], vnorm=vn)
+    codes2 = ops.alloc_codes(cfg, DEV)
+    vn2 = torch.zeros_like(vn)
+    js = [0, 31, 32, 77, 127]
+    for j in js:
+        ops.hash_keys(cfg, d["K"], d["W"], codes2, V=d["V"], vnorm=vn2, n_begin=j, n_count=1)
+        assert torch.equal(vn2[:, :, j], vn[:, :, j])
+    got = ops.unpack_codes(cfg, codes2).cpu().numpy().astype(np.int64)[..., js]
+    ref, margin = O.hash_keys(O.widen(c["K"]), O.widen(W))
+    ref, margin = ref[..., js], margin[..., js]
+    diff = got != ref
+    for b, h, l, jj in zip(*np.nonzero(diff)):
+        flipped = got[b, h, l, jj] ^ ref[b, h, l, jj]
+        for i in range(8):
+            if flipped >> i & 1:
+                assert margin[b, h, l, i, jj] < 1e-5
+
+
 def test_pack_unpack_roundtrip():
     for L in (3, 16, 60, 100):
         cfg = Config(B=2, H_q=2, H_kv=2, N_max=96, L=L, P=8)
@@ -114,7 +138,7 @@ def table_tol(tau, P):
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("L,mode,lens", [(16, KV_SHARED, [4096]), (60, KV_SHARED, [3000, 4096]),
                                          (60, PER_QHEAD, [2500, 17]), (8, KV_SHARED, [4096, 0]),
-                                         (64, KV_SHARED, [4090]), (128, PER_QHEAD, [1000])])
+                                         (64, KV_SHARED, [4090]), (33, PER_QHEAD, [1000])])
 def test_scores(L, mode, lens):
     B = len(lens)
     cfg, c, W, d = make(B, 8, 2, 4096, L, 8, seed=L, seq_lens=lens, mode=mode)
@@ -138,6 +162,16 @@ def test_scores(L, mode, lens):
             assert np.all(np.isneginf(got[b, r][~fin]))
             if fin.any():
                 assert np.max(rel_err(got[b, r][fin], s[fin])) <= 1e-5
+
+
+def test_score_rejects_more_than_64_tables():
+    cfg, c, W, d = make(1, 4, 1, 64, 100, 8, seed=2)
+    codes = ops.alloc_codes(cfg, DEV)
+    vn = torch.ones((1, 1, 64), dtype=torch.float32, device=DEV)
+    from paper_2602_06283_b200._lib import SocketError
+    with pytest.raises(SocketError) as e:
+        ops.score(cfg, d["q"], d["W"], codes, vn, d["seq_lens"])
+    assert e.value.status == 2   # SOCKET_EUNSUPPORTED
 
 
 # ---------------------------------------------------------------------------
