@@ -79,6 +79,29 @@ def test_hash_partial_ranges_touch_only_their_rows():
     assert np.all(got[..., ~inside] == 0)
 
 
+@pytest.mark.parametrize("L,P", [(60, 8), (16, 8), (8, 5)])
+def test_hash_tensor_core_partial_ranges(L, P):
+    """Prefill ranges >= 128 keys go through the tcgen05 kernel, including ranges
+    that start and end inside 128-key tiles; rows outside stay untouched."""
+    cfg, c, W, d = make(2, 2, 2, 640, L, P, seed=L + 3)
+    codes = ops.alloc_codes(cfg, DEV)
+    ops.hash_keys(cfg, d["K"], d["W"], codes, n_begin=37, n_count=300)
+    ops.hash_keys(cfg, d["K"], d["W"], codes, n_begin=384, n_count=256)
+    got = ops.unpack_codes(cfg, codes).cpu().numpy().astype(np.int64)
+    ref, margin = O.hash_keys(O.widen(c["K"]), O.widen(W))
+    inside = np.zeros(640, bool)
+    inside[37:337] = True
+    inside[384:640] = True
+    assert np.all(got[..., ~inside] == 0)
+    diff = (got != ref) & inside
+    for b, h, l, j in zip(*np.nonzero(diff)):
+        flipped = got[b, h, l, j] ^ ref[b, h, l, j]
+        for i in range(P):
+            if flipped >> i & 1:
+                assert margin[b, h, l, i, j] < 1e-5
+    assert diff.sum() <= 2
+
+
 def test_append_path_codes_and_norms():
     """The append path (n_count = 1, decode step) writes codes equal to the
     oracle's (margin rule) and value norms bit-identical to the prefill path."""
