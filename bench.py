@@ -35,6 +35,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "sparse-decode tokens/s at 32K/128K ctx vs dense; score+attn HBM GB/s vs peak"
 
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernels
+# at the default workload, from the committed ncu --set full capture
+# (profiles/r1/ncu_summary.md); None = not captured for this configuration.
+TRAFFIC = {}
+try:
+    _t = json.load(open(os.path.join(ROOT, "profiles", "r1", "traffic.json")))
+    TRAFFIC = {k: v for k, v in _t.items() if isinstance(v, (int, float))}
+except Exception:
+    pass
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -223,6 +233,22 @@ def run_ours(a):
     prefill_s = time.perf_counter() - t0
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    # prefill key hashing (Alg. 1) on the tensor cores: codes only (the projection
+    # GEMM), timed with events; algorithmic flops = 2 * keys * d * L * P
+    def prefill_codes():
+        ops.hash_keys(cfg, K, W, dec.codes, n_begin=0, n_count=N)
+    pre_ms = _time(prefill_codes, flush, stream, 2, 5)
+    pre_flops = 2.0 * B * 8 * N * 128 * L * P
+    bf16_peak = 1654.9
+    try:
+        bf16_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
+    except Exception:
+        pass
+    prefill = {"kernel": "hash_keys_tc (tcgen05)", "ms": round(pre_ms, 4),
+               "TFLOP/s": round(pre_flops / (pre_ms * 1e-3) / 1e12, 1),
+               "frac_of_bf16_peak": round(pre_flops / (pre_ms * 1e-3) / 1e12 / bf16_peak, 4),
+               "keys": B * 8 * N, "flops": pre_flops,
+               "hbm_GB/s": round(B * 8 * N * (256 + L * ((P + 7) // 8)) / (pre_ms * 1e-3) / 1e9, 1)}
 
     def barrier():
         if world > 1:
@@ -237,7 +263,7 @@ def run_ours(a):
         return t.item()
 
     # ---- (1) graph-replayed step: headline ---------------------------------------
-    dec.capture(q, lens, append_pos=N - 1)
+    dec.capture(q, lens, append=True)
     for _ in range(a.warmup):
         flush.zero_()
         dec.replay()
@@ -255,40 +281,57 @@ def run_ours(a):
     clk = clocks.stop()
     step_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / a.steps
     step_ms = max_over_ranks(step_ms)
-    launches_per_step = 5   # append-hash, query tables, score, top-k, decode (+1 memset node)
+    launches_per_step = 4   # fused prologue (append + tables), score, top-k, decode
 
-    # ---- (2) eager step with per-stage events: kernel shares + roofline ----------
-    stage_names = ["append_hash", "tables+score", "topk", "sparse_decode+combine"]
-    stage_ms = {s: 0.0 for s in stage_names}
-    for it in range(a.warmup + a.steps):
-        flush.zero_()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        ev[0].record(stream)
-        ops.hash_keys(cfg, K, W, dec.codes, V=V, vnorm=dec.vnorm, n_begin=N - 1, n_count=1)
-        ev[1].record(stream)
-        ops.score(cfg, q, W, dec.codes, dec.vnorm, lens, out=dec.scores, ws=dec.ws_score)
-        ev[2].record(stream)
-        ops.topk(cfg, dec.scores, lens, k, idx=dec.idx, cnt=dec.cnt)
-        ev[3].record(stream)
-        ops.sparse_decode(cfg, q, K, V, dec.idx, dec.cnt, k, out=dec.out, lse=dec.lse, ws=dec.ws_dec)
-        ev[4].record(stream)
-        torch.cuda.synchronize()
-        if it >= a.warmup:
-            for i, s in enumerate(stage_names):
-                stage_ms[s] += ev[i].elapsed_time(ev[i + 1]) / a.steps
+    # ---- (2) per-kernel timing: each stage's call launched R times back to back
+    # between two events on its stream (L2 flushed before each burst), so a
+    # kernel's average duration excludes host launch gaps.  The headline above
+    # uses the fused call; these give each kernel's share and roofline.
+    stage_names = ["append_hash", "tables", "score", "topk", "sparse_decode"]
+    lut = ops.workspace(cfg, _lib.OP_SCORE, 1, dev)
+    ops.build_lut(cfg, q, W, lut)
+    calls = {
+        "append_hash": lambda: ops.hash_keys(cfg, K, W, dec.codes, V=V, vnorm=dec.vnorm,
+                                             n_begin=N - 1, n_count=1),
+        "tables": lambda: ops.build_lut(cfg, q, W, lut),
+        "score": lambda: ops.score_lut(cfg, lut, dec.codes, dec.vnorm, lens, out=dec.scores),
+        "topk": lambda: ops.topk(cfg, dec.scores, lens, k, idx=dec.idx, cnt=dec.cnt),
+        "sparse_decode": lambda: ops.sparse_decode(cfg, q, K, V, dec.idx, dec.cnt, k, out=dec.out,
+                                                   lse=dec.lse, ws=dec.ws_dec),
+    }
+    R = 10
+    stage_ms = {}
+    for s_ in stage_names:
+        fn = calls[s_]
+        for _ in range(a.warmup):
+            fn()
+        tot = 0.0
+        reps = max(1, a.steps // 5)
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(R):
+                fn()
+            e1.record(stream)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1) / R
+        stage_ms[s_] = tot / reps
     eager_ms = sum(stage_ms.values())
     ab = algorithmic_bytes(B, N, L, P, k, H_sel=cfg.H_sel)
     hbm, peak_src = peaks()
     stages = {}
-    for s, key in (("tables+score", "score"), ("topk", "topk"), ("sparse_decode+combine", "sparse_decode")):
-        gbs = ab[key] / (stage_ms[s] * 1e-3) / 1e9
-        stages[s] = {"ms": round(stage_ms[s], 5), "alg_bytes": ab[key], "GB/s": round(gbs, 1),
-                     "frac": round(gbs / hbm, 4), "share": round(stage_ms[s] / eager_ms, 4)}
-    stages["append_hash"] = {"ms": round(stage_ms["append_hash"], 5),
-                             "share": round(stage_ms["append_hash"] / eager_ms, 4)}
-    dom = max(("tables+score", "sparse_decode+combine"), key=lambda s: stage_ms[s])
-    roof = {"bound": "hbm", "kernel": dom, "achieved": stages[dom]["GB/s"], "peak": hbm,
-            "unit": "GB/s", "frac": stages[dom]["frac"], "traffic": None, "peak_source": peak_src}
+    for s_, key in (("score", "score"), ("topk", "topk"), ("sparse_decode", "sparse_decode")):
+        gbs = ab[key] / (stage_ms[s_] * 1e-3) / 1e9
+        stages[s_] = {"ms": round(stage_ms[s_], 5), "alg_bytes": ab[key], "GB/s": round(gbs, 1),
+                      "frac": round(gbs / hbm, 4), "share": round(stage_ms[s_] / eager_ms, 4)}
+    for s_ in ("append_hash", "tables"):
+        stages[s_] = {"ms": round(stage_ms[s_], 5), "share": round(stage_ms[s_] / eager_ms, 4)}
+    dom = max(("score", "sparse_decode"), key=lambda s_: stage_ms[s_])
+    kern = {"score": "score_kernel", "sparse_decode": "decode_mma_kernel"}[dom]
+    roof = {"bound": "hbm", "kernel": kern, "achieved": stages[dom]["GB/s"], "peak": hbm,
+            "unit": "GB/s", "frac": stages[dom]["frac"], "traffic": TRAFFIC.get(kern),
+            "peak_source": peak_src}
 
     # ---- (3) dense comparators on the same cache ---------------------------------
     dense = {}
@@ -312,7 +355,7 @@ def run_ours(a):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) bf16 q/K/V and projections)", "config": cfgd,
         "roofline": roof, "stages": stages, "eager_ms_per_step": round(eager_ms, 5),
-        "gpu_launches": launches_per_step * a.steps, "clocks": clk,
+        "gpu_launches": launches_per_step * a.steps, "clocks": clk, "prefill": prefill,
         "e2e": {"value": round(B * world / (e2e_ms * 1e-3), 1), "unit": "tokens/s",
                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]},
     }
@@ -409,7 +452,7 @@ def end_to_end(a, cfg, dec, q, K, V, lens, N, flush, stream, dev):
         q_d.copy_(q_h, non_blocking=True)
         K[:, :, N - 1].copy_(k_new, non_blocking=True)
         V[:, :, N - 1].copy_(v_new, non_blocking=True)
-        out, _ = dec.step(q_d, lens, append_pos=N - 1)
+        out, _ = dec.step(q_d, lens, append=True)
         out_h.copy_(out, non_blocking=True)
 
     ms = _time(step, flush, stream, a.warmup, a.steps)

@@ -13,6 +13,7 @@
  *   sparse flash-decode        Eq. 2 P:169-174, P:271, P:309, P:701   socket_sparse_decode
  *   LSE combine of partials    (Flash-Decode split merge)      socket_lse_combine
  *   dense decode (k = n)       Eq. 1 P:16-22                          socket_dense_decode
+ *   whole decode step          P:259-271                              socket_decode_step
  *   sequence-shard resolve     exact global top-k over shards         socket_topk_resolve
  *
  * Conventions (all entry points)
@@ -126,7 +127,8 @@ enum {
   SOCKET_OP_TOPK = 3,
   SOCKET_OP_SPARSE_DECODE = 4,
   SOCKET_OP_DENSE_DECODE = 5,
-  SOCKET_OP_RESOLVE = 6
+  SOCKET_OP_RESOLVE = 6,
+  SOCKET_OP_DECODE_STEP = 7
 };
 size_t socket_workspace_bytes(const socket_cfg* cfg, int32_t op, int32_t k);
 
@@ -167,6 +169,32 @@ socket_status socket_score(const socket_cfg* cfg, const void* q, const void* W,
                            const uint8_t* codes, const float* vnorm, const int32_t* seq_lens,
                            const uint8_t* mask, float* scores, void* ws, size_t ws_bytes,
                            void* stream);
+
+/* The two halves of socket_score, for callers that schedule them separately:
+ * socket_build_lut writes the Alg. 2 tables of every (b, selection row) as the
+ * score kernel's shared-memory image (opaque layout) into `lut`, which must
+ * hold socket_workspace_bytes(cfg, SOCKET_OP_SCORE, 0) bytes; socket_score_lut
+ * computes Eq. 4 + Alg. 4 scores from it (same semantics as socket_score). */
+socket_status socket_build_lut(const socket_cfg* cfg, const void* q, const void* W, void* lut,
+                               size_t lut_bytes, void* stream);
+socket_status socket_score_lut(const socket_cfg* cfg, const void* lut, const uint8_t* codes,
+                               const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
+                               float* scores, void* stream);
+
+/* One whole SOCKET decode step, as one call with internal fusion:
+ *   if append_last != 0: Alg. 1 on the newest key j = seq_lens[b] - 1 of every
+ *     (b, kv head) (codes + vnorm; the new key is a candidate, reading R-18),
+ *     in the same launch as the Alg. 2 table build;
+ *   then scores (Eq. 4 / Alg. 4, written to `scores`), TopK with sink/window
+ *   (idx, cnt as socket_topk) and sparse attention (out, lse as
+ *   socket_sparse_decode), chained with programmatic dependent launch.
+ * Requires L <= 64.  ws: socket_workspace_bytes(cfg, SOCKET_OP_DECODE_STEP, k). */
+socket_status socket_decode_step(const socket_cfg* cfg, const void* q, const void* K,
+                                 const void* V, const void* W, uint8_t* codes, float* vnorm,
+                                 const int32_t* seq_lens, const uint8_t* mask,
+                                 int32_t append_last, int32_t k, int32_t sink, int32_t window,
+                                 float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
+                                 void* ws, size_t ws_bytes, void* stream);
 
 /* Alg. 3 l.244 TopK with forced sink / local window: per (b, row),
  * with n = seq_lens[b] and valid = (scores != -inf) & (j < n):

@@ -14,14 +14,15 @@ LIB_PATH = os.path.join(HERE, "libsocket_b200.so")
 
 SOCKET_OK, SOCKET_EINVAL, SOCKET_EUNSUPPORTED, SOCKET_ECUDA, SOCKET_EWORKSPACE = range(5)
 GROUP_KV_SHARED, GROUP_PER_QHEAD = 0, 1
-OP_HASH, OP_TABLES, OP_SCORE, OP_TOPK, OP_SPARSE_DECODE, OP_DENSE_DECODE, OP_RESOLVE = range(7)
+OP_HASH, OP_TABLES, OP_SCORE, OP_TOPK, OP_SPARSE_DECODE, OP_DENSE_DECODE, OP_RESOLVE, OP_DECODE_STEP = range(8)
 
 # every symbol include/socket_b200.h declares (tests check the export table)
 EXPORTS = (
     "socket_code_slots", "socket_codes_bytes", "socket_workspace_bytes", "socket_hash_keys",
     "socket_pack_codes", "socket_unpack_codes", "socket_query_tables", "socket_score",
     "socket_topk", "socket_sparse_decode", "socket_lse_combine", "socket_dense_decode",
-    "socket_topk_resolve", "socket_last_error", "socket_version",
+    "socket_topk_resolve", "socket_last_error", "socket_version", "socket_build_lut",
+    "socket_score_lut", "socket_decode_step",
 )
 
 
@@ -69,6 +70,10 @@ def lib():
         "socket_lse_combine": (i32, [cfgp, P, i32, P, P, P]),
         "socket_dense_decode": (i32, [cfgp, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
         "socket_topk_resolve": (i32, [cfgp, P, P, i32, i32, i32, P, P, P, ctypes.c_size_t, P]),
+        "socket_build_lut": (i32, [cfgp, P, P, P, ctypes.c_size_t, P]),
+        "socket_score_lut": (i32, [cfgp, P, P, P, P, P, P, P]),
+        "socket_decode_step": (i32, [cfgp, P, P, P, P, P, P, P, P, i32, i32, i32, i32, P, P, P, P,
+                                     P, P, ctypes.c_size_t, P]),
         "socket_last_error": (ctypes.c_char_p, []),
         "socket_version": (i32, []),
     }

@@ -79,6 +79,8 @@ size_t socket_workspace_bytes(const socket_cfg* c, int32_t op, int32_t k) {
       return align16(decode_workspace_bytes(*c, k > 0 ? k : 1, false));
     case SOCKET_OP_DENSE_DECODE:
       return align16(decode_workspace_bytes(*c, 1, true));
+    case SOCKET_OP_DECODE_STEP:
+      return align16(decode_step_workspace_bytes(*c, k > 0 ? k : 1));
     default:
       return 0;
   }
@@ -141,6 +143,60 @@ socket_status socket_score(const socket_cfg* cfg, const void* q, const void* W,
   float* lut = static_cast<float*>(ws);
   SK_CHECK(launch_query_tables(*cfg, q, W, nullptr, lut, S(stream)));
   return launch_score(*cfg, lut, codes, vnorm, seq_lens, mask, scores, S(stream));
+}
+
+socket_status socket_build_lut(const socket_cfg* cfg, const void* q, const void* W, void* lut,
+                               size_t lut_bytes, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(q);
+  SK_NONNULL(W);
+  SK_NONNULL(lut);
+  if (lut_bytes < socket_workspace_bytes(cfg, SOCKET_OP_SCORE, 0))
+    return fail(SOCKET_EWORKSPACE, "build_lut: buffer too small");
+  if (cfg->B == 0) return SOCKET_OK;
+  return launch_query_tables(*cfg, q, W, nullptr, static_cast<float*>(lut), S(stream));
+}
+
+socket_status socket_score_lut(const socket_cfg* cfg, const void* lut, const uint8_t* codes,
+                               const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
+                               float* scores, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(lut);
+  SK_NONNULL(codes);
+  SK_NONNULL(vnorm);
+  SK_NONNULL(seq_lens);
+  SK_NONNULL(scores);
+  if (cfg->B == 0 || cfg->N_max == 0) return SOCKET_OK;
+  return launch_score(*cfg, static_cast<const float*>(lut), codes, vnorm, seq_lens, mask, scores,
+                      S(stream));
+}
+
+socket_status socket_decode_step(const socket_cfg* cfg, const void* q, const void* K,
+                                 const void* V, const void* W, uint8_t* codes, float* vnorm,
+                                 const int32_t* seq_lens, const uint8_t* mask,
+                                 int32_t append_last, int32_t k, int32_t sink, int32_t window,
+                                 float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(q);
+  SK_NONNULL(K);
+  SK_NONNULL(V);
+  SK_NONNULL(W);
+  SK_NONNULL(codes);
+  SK_NONNULL(vnorm);
+  SK_NONNULL(seq_lens);
+  SK_NONNULL(scores);
+  SK_NONNULL(idx);
+  SK_NONNULL(cnt);
+  SK_NONNULL(out);
+  SK_NONNULL(ws);
+  if (k <= 0) return fail(SOCKET_EINVAL, "k must be >= 1");
+  if (k > cfg->N_max) return fail(SOCKET_EINVAL, "k > N_max");
+  if (sink < 0 || window < 0 || (long long)sink + window > k)
+    return fail(SOCKET_EINVAL, "need 0 <= sink, window and sink + window <= k");
+  if (cfg->B == 0 || cfg->N_max == 0) return SOCKET_OK;
+  return launch_decode_step(*cfg, q, K, V, W, codes, vnorm, seq_lens, mask, append_last != 0, k,
+                            sink, window, scores, idx, cnt, out, lse, ws, ws_bytes, S(stream));
 }
 
 socket_status socket_topk(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,

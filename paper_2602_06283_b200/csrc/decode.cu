@@ -53,7 +53,7 @@ socket_status launch_decode_mma(const socket_cfg& c, const void* q, const void* 
                                 const int32_t* idx, const int32_t* cnt, int k,
                                 const int32_t* seq_lens, bool dense, int units, int NH,
                                 int n_splits, int rps, float* part, int* tickets, void* out,
-                                float* lse, float* part_out, cudaStream_t st);
+                                float* lse, float* part_out, cudaStream_t st, bool pdl);
 
 // Split geometry: rows per split is a multiple of `gran` (rows one CTA consumes
 // per round), at most `max_rps` (index staging), and the grid aims at
@@ -108,7 +108,30 @@ socket_status launch_decode(const socket_cfg& c, const void* q, const void* K, c
   cudaError_t e = cudaMemsetAsync(tickets, 0, (size_t)units * sizeof(int), st);
   if (e != cudaSuccess) return fail(SOCKET_ECUDA, std::string("decode: memset: ") + cudaGetErrorString(e));
   return launch_decode_mma(c, q, K, V, idx, cnt, k, seq_lens, dense, units, NH, ns, rps, (float*)ws,
-                           tickets, out, lse, partial, st);
+                           tickets, out, lse, partial, st, false);
+}
+
+// Sparse decode inside socket_decode_step: no ticket memset (the step prologue
+// clears the tickets), PDL launch.  With tickets_out != nullptr it only
+// reports where the tickets live and how many units there are (no launch).
+socket_status launch_decode_pdl(const socket_cfg& c, const void* q, const void* K, const void* V,
+                                const int32_t* idx, const int32_t* cnt, int k, void* out,
+                                float* lse, void* ws, size_t ws_bytes, cudaStream_t st, bool pdl,
+                                int** tickets_out, int* n_units) {
+  int units, NH, ns, rps;
+  decode_geometry(c, k, false, units, NH, ns, rps);
+  if (ws_bytes < part_bytes(c, ns) + (size_t)units * sizeof(int))
+    return fail(SOCKET_EWORKSPACE, "decode: workspace too small");
+  if (NH > 8) return fail(SOCKET_EUNSUPPORTED, "decode: more than 8 query heads per selection row");
+  int* tickets = reinterpret_cast<int*>(static_cast<char*>(ws) + part_bytes(c, ns));
+  if (tickets_out) {
+    *tickets_out = tickets;
+    *n_units = units;
+    return SOCKET_OK;
+  }
+  if (units == 0) return SOCKET_OK;
+  return launch_decode_mma(c, q, K, V, idx, cnt, k, nullptr, false, units, NH, ns, rps, (float*)ws,
+                           tickets, out, lse, nullptr, st, pdl);
 }
 
 socket_status launch_lse_combine(const socket_cfg& c, const float* partials, int G, void* out,

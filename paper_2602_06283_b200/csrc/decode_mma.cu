@@ -93,6 +93,7 @@ decode_mma_kernel(MmaArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
 
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: idx / cnt of the predecessor
   const int n_rows = DENSE ? a.seq_lens[b] : a.cnt[unit];
   const int i_begin = split * a.rows_per_split;
   const int i_end = min(i_begin + a.rows_per_split, n_rows);
@@ -290,7 +291,7 @@ socket_status launch_decode_mma(const socket_cfg& c, const void* q, const void* 
                                 const int32_t* idx, const int32_t* cnt, int k,
                                 const int32_t* seq_lens, bool dense, int units, int NH,
                                 int n_splits, int rps, float* part, int* tickets, void* out,
-                                float* lse, float* part_out, cudaStream_t st) {
+                                float* lse, float* part_out, cudaStream_t st, bool pdl) {
   MmaArgs a;
   a.q = (const uint16_t*)q;
   a.K = (const uint16_t*)K;
@@ -314,14 +315,25 @@ socket_status launch_decode_mma(const socket_cfg& c, const void* q, const void* 
   a.out = (uint16_t*)out;
   a.lse = lse;
   a.part_out = part_out;
-  dim3 grid(n_splits, units);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_splits, units);
+  cfg.blockDim = dim3(kMmaThreads);
+  cfg.dynamicSmemBytes = kMmaRing;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e;
   if (dense) {
     cudaFuncSetAttribute(decode_mma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMmaRing);
-    decode_mma_kernel<true><<<grid, kMmaThreads, kMmaRing, st>>>(a);
+    e = cudaLaunchKernelEx(&cfg, decode_mma_kernel<true>, a);
   } else {
     cudaFuncSetAttribute(decode_mma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMmaRing);
-    decode_mma_kernel<false><<<grid, kMmaThreads, kMmaRing, st>>>(a);
+    e = cudaLaunchKernelEx(&cfg, decode_mma_kernel<false>, a);
   }
+  if (e != cudaSuccess) return fail(SOCKET_ECUDA, std::string("decode launch: ") + cudaGetErrorString(e));
   return check_launch("decode_mma_kernel");
 }
 

@@ -5,20 +5,10 @@
 // prefills lives in hash_tc.cu; this file holds the CUDA-core path used for
 // small ranges (the per-step append of a decode step, n_count = 1) and for
 // configurations the tcgen05 kernel does not tile, plus the layout converters.
-#include "internal.cuh"
+#include "step_dev.cuh"
 
 namespace sk {
 
-// Byte offset of (row-local key j, slot s) inside one (b, kv-head) code region.
-__device__ __forceinline__ size_t code_off(int j, int s, int Lp) {
-  const int CB = Lp < 16 ? Lp : 16;
-  return ((size_t)(j >> 5) * (Lp / CB) + s / CB) * (32 * CB) + (j & 31) * CB + (s % CB);
-}
-// table held by slot s of key j
-__device__ __forceinline__ int slot_table(int s, int j, int Lp) {
-  const int M = (Lp < 32 ? Lp : 32) - 1;
-  return (s & ~M) | ((s + j) & M);
-}
 
 // ----------------------------------------------------------------------------
 // CUDA-core hash: one CTA = one 32-key tile of one (b, kv-head); warp w
@@ -114,17 +104,6 @@ __global__ void pack_codes_kernel(const uint8_t* __restrict__ plain, uint8_t* __
   }
 }
 
-// ----------------------------------------------------------------------------
-// Append path (decode step: n_count new keys per (b, kv-head), typically 1).
-// One warp per (key, table): lane t holds elements 4t .. 4t+3 of the key, the
-// P projections are 4 FMAs per lane each (t ascending within the lane) and a
-// butterfly sum; lane 0 writes the code byte to slot s = (l & ~M) | ((l - j) & M)
-// of key j (inverse of slot_table).  Warps with table 0 also write ||v_j||
-// with exactly vnorm_kernel's summation order.
-// Note: the projection's summation order differs from the prefill kernels, so
-// a bit whose projection is within fp32 rounding of 0 may differ between the
-// two paths; both are checked against the fp64 oracle with the same margin rule.
-// ----------------------------------------------------------------------------
 constexpr int kAppendWarps = 8;
 
 __global__ void __launch_bounds__(kAppendWarps * 32)
@@ -132,39 +111,8 @@ hash_append_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict__ 
                    uint8_t* __restrict__ codes, const uint16_t* __restrict__ V,
                    float* __restrict__ vnorm, int N_max, int L, int P, int Lp, int n_begin,
                    int n_count, int total_keys) {
-  const int lane = threadIdx.x & 31;
-  const int job = blockIdx.x * kAppendWarps + (threadIdx.x >> 5);   // (key, table)
-  if (job >= total_keys * Lp) return;
-  const int key = job / Lp, l = job % Lp;
-  const int bh = key / n_count, j = n_begin + key % n_count;
-  uint32_t code = 0;
-  if (l < L) {
-    const uint2 ku = *reinterpret_cast<const uint2*>(K + ((size_t)bh * N_max + j) * kD + lane * 4);
-    const float k0 = bf16lo(ku.x), k1 = bf16hi(ku.x), k2 = bf16lo(ku.y), k3 = bf16hi(ku.y);
-    for (int i = 0; i < P; ++i) {
-      const uint2 wu = *reinterpret_cast<const uint2*>(W + ((size_t)l * P + i) * kD + lane * 4);
-      float x = bf16lo(wu.x) * k0;
-      x = fmaf(bf16hi(wu.x), k1, x);
-      x = fmaf(bf16lo(wu.y), k2, x);
-      x = fmaf(bf16hi(wu.y), k3, x);
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      code |= (x >= 0.f ? 1u : 0u) << i;     // sign(0) = +1 (R-3), LSB = row 0 (R-4)
-    }
-  }
-  if (lane == 0) {
-    const int M = (Lp < 32 ? Lp : 32) - 1;
-    const int s = (l & ~M) | ((l - j) & M);
-    codes[(size_t)bh * N_max * Lp + code_off(j, s, Lp)] = (uint8_t)code;
-  }
-  if (V && l == 0) {
-    const uint2 u = *reinterpret_cast<const uint2*>(V + ((size_t)bh * N_max + j) * kD + lane * 4);
-    float a = bf16lo(u.x), b = bf16hi(u.x), c = bf16lo(u.y), e = bf16hi(u.y);
-    float sq = fmaf(a, a, fmaf(b, b, fmaf(c, c, e * e)));
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    if (lane == 0) vnorm[(size_t)bh * N_max + j] = sqrtf(sq);
-  }
+  append_warp_job(K, W, codes, V, vnorm, N_max, L, P, Lp, n_begin, n_count, total_keys, 0, nullptr, 1,
+                  blockIdx.x * kAppendWarps + (threadIdx.x >> 5), threadIdx.x & 31);
 }
 
 socket_status launch_hash_keys_simt(const socket_cfg& c, const void* K, const void* W,

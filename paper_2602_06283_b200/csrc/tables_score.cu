@@ -11,145 +11,18 @@
 // score_kernel: streams the tiled codes with 128-bit loads, lane = key j mod
 // 32.  At slot step s lane l reads LUT column (s & 32) | ((s + l) & 31), so the
 // 32 lanes hit 32 distinct banks (conflict-free).
-#include "internal.cuh"
+#include "step_dev.cuh"
 
 namespace sk {
 
-constexpr int kTabThreads = 512;
-constexpr int kTabPerCta = 16;    // tables per CTA
-constexpr int kMaxHeads = 8;      // heads per selection row
 
-// One CTA = (b, selection row) x kTabPerCta tables.  Steps:
-//  1+2. in round i, warp w owns the 4 W rows 4 (16 i + w) .. + 3.
-//       A lane holds 4 elements (t = 4 lane .. 4 lane + 3) of every head's q and
-//       of the W rows as fp64, so each of the 4*NH projections x = W_i . q_h is
-//       4 fp64 FMAs per lane; a reduce-scatter over the warp leaves every lane
-//       with one complete x.  bf16 x bf16 products and their partial sums are
-//       exact in fp64, so x is exact.  Each lane then evaluates its
-//       u = tanh(x)/sqrt(d) and sigma(+-2u/tau) with the accurate fp32
-//       functions (<= 2 ulp each).
-//  3.   half tables lo(r & 15) = prod_{i<4} f_i, hi(r >> 4) = prod_{i>=4} f_i
-//       in fp64, rounded once to fp32;
-//  4.   T(r) = sum_h lo_h * hi_h; consecutive threads write consecutive table
-//       columns of one LUT row.
 template <int NH>
 __global__ void __launch_bounds__(kTabThreads, NH >= 8 ? 1 : 2)
 query_tables_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ W,
                     float* __restrict__ plain, float* __restrict__ lut, int H_q, int H_sel,
                     int L, int P, int Lp, float tau) {
-  constexpr int kWarps = kTabThreads / 32;
-  constexpr int kRounds = (kTabPerCta * 8) / (4 * kWarps);   // 4 W rows per warp per round
-  static_assert(kRounds * 4 * kWarps == kTabPerCta * 8, "W rows must tile the warps");
-  constexpr int NV = 4 * NH;                                 // values per warp and round
-  __shared__ double fx[NH][kTabPerCta][8][2];                // sigma factors
-  __shared__ float half_lo[NH][16][kTabPerCta];
-  __shared__ float half_hi[NH][16][kTabPerCta];
-  const int row = blockIdx.x;                // b * H_sel + r
-  const int b = row / H_sel, r = row % H_sel;
-  const int h0 = (NH == 1) ? r : r * NH;     // first query head of the row
-  const int l0 = blockIdx.y * kTabPerCta;
-  const int R = 1 << P;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // W rows are enumerated as wr = 8 * tl + i (bit i < 8, rows with i >= P skipped)
-  double qd[NH][4];
-#pragma unroll
-  for (int h = 0; h < NH; ++h) {
-    const uint2 u = *reinterpret_cast<const uint2*>(q + ((size_t)b * H_q + h0 + h) * kD + lane * 4);
-    qd[h][0] = bf16lo(u.x); qd[h][1] = bf16hi(u.x); qd[h][2] = bf16lo(u.y); qd[h][3] = bf16hi(u.y);
-  }
-  uint2 wu[kRounds][4];
-#pragma unroll
-  for (int round = 0; round < kRounds; ++round)
-#pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      const int wr = (round * kWarps + warp) * 4 + rr;
-      const int l = l0 + (wr >> 3), i = wr & 7;
-      wu[round][rr] = make_uint2(0, 0);
-      if (i < P && l < L) wu[round][rr] = *reinterpret_cast<const uint2*>(W + ((size_t)l * P + i) * kD + lane * 4);
-    }
-#pragma unroll
-  for (int round = 0; round < kRounds; ++round) {
-    double v[NV];
-#pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      const double w0 = bf16lo(wu[round][rr].x), w1 = bf16hi(wu[round][rr].x);
-      const double w2 = bf16lo(wu[round][rr].y), w3 = bf16hi(wu[round][rr].y);
-#pragma unroll
-      for (int h = 0; h < NH; ++h) {
-        double x = w0 * qd[h][0];
-        x = fma(w1, qd[h][1], x);
-        x = fma(w2, qd[h][2], x);
-        v[rr * NH + h] = fma(w3, qd[h][3], x);
-      }
-    }
-    // reduce-scatter over the 32 lanes: afterwards v[0] holds the full sum of
-    // value `own` (lanes with equal `own` hold equal sums)
-    int own = 0, nv = NV;
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      if (nv > 1) {
-        const int hnv = nv >> 1;
-        const bool up = (lane & off) != 0;
-#pragma unroll
-        for (int i = 0; i < NV / 2; ++i) {
-          if (i < hnv) {
-            const double send = up ? v[i] : v[i + hnv];
-            const double keep = up ? v[i + hnv] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-          }
-        }
-        if (up) own += hnv;
-        nv = hnv;
-      } else {
-        v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
-      }
-    }
-    const int rr = own / NH, h = own % NH;          // NH is a power of two
-    const int wr = (round * kWarps + warp) * 4 + rr;
-    const int tl = wr >> 3, i = wr & 7;
-    const float inv_sqrt_d = 0.08838834764831845f;   // 1/sqrt(128), correctly rounded
-    const float uu = tanhf((float)v[0]) * inv_sqrt_d;  // Alg. 2 l.217
-    const float a = 2.0f * uu / tau;                   // logit gap of bit i
-    const float fp = 1.0f / (1.0f + expf(-a));         // c_{r,i} = +1 (bit set)
-    const float fm = 1.0f / (1.0f + expf(a));          // c_{r,i} = -1
-    if ((lane & (32 / NV - 1)) == 0 && i < P) {
-      fx[h][tl][i][1] = (double)fp;
-      fx[h][tl][i][0] = (double)fm;
-    }
-  }
-  __syncthreads();
-  // 3. half tables (bits 0..3 and 4..P-1; an empty product is 1)
-  for (int i = tid; i < NH * kTabPerCta * 32; i += kTabThreads) {  // NH is a template constant
-    const int e = i & 15, hi = (i >> 4) & 1, tl = (i >> 5) % kTabPerCta, h = i / (32 * kTabPerCta);
-    double p = 1.0;
-#pragma unroll
-    for (int bit = 0; bit < 4; ++bit) {
-      const int ib = hi * 4 + bit;
-      if (ib < P) p *= fx[h][tl][ib][(e >> bit) & 1];
-    }
-    if (hi) half_hi[h][e][tl] = (float)p; else half_lo[h][e][tl] = (float)p;
-  }
-  __syncthreads();
-  // 4. entries: thread -> (row rr, table tl) with tl fastest
-  const int panels = Lp <= 64 ? 1 : (Lp + 63) / 64;
-  float* lrow = lut ? lut + (size_t)row * panels * (256 * 64) : nullptr;
-  for (int e = tid; e < 256 * kTabPerCta; e += kTabThreads) {
-    const int tl = e % kTabPerCta, rr = e / kTabPerCta;
-    const int l = l0 + tl;
-    if (l >= Lp) continue;
-    float T = 0.f;
-    if (l < L && rr < R) {
-      for (int h = 0; h < NH; ++h) T = fmaf(half_lo[h][rr & 15][tl], half_hi[h][rr >> 4][tl], T);
-      if (plain) plain[((size_t)row * L + l) * R + rr] = T;
-    }
-    if (lrow) {
-      if (Lp >= 32) {
-        lrow[(size_t)(l >> 6) * (256 * 64) + rr * 64 + (l & 63)] = T;
-      } else {
-        for (int cc = l; cc < 32; cc += Lp) lrow[rr * 64 + cc] = T;
-      }
-    }
-  }
+  __shared__ TablesSmem<NH> S;
+  tables_cta<NH>(q, W, plain, lut, H_q, H_sel, L, P, Lp, tau, blockIdx.x, blockIdx.y * kTabPerCta, S);
 }
 
 socket_status launch_query_tables(const socket_cfg& c, const void* q, const void* W,
@@ -268,6 +141,7 @@ score_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
   const int tiles_per_row = N_max >> 5;
   const long long t_begin = total_tiles * blockIdx.x / gridDim.x;
   const long long t_end = total_tiles * (blockIdx.x + 1) / gridDim.x;
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: LUT / codes of the predecessor
   if (threadIdx.x == 0) mbar_init(&bar, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
@@ -355,9 +229,9 @@ score_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
   }
 }
 
-socket_status launch_score(const socket_cfg& c, const float* lut, const uint8_t* codes,
-                           const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
-                           float* scores, cudaStream_t st) {
+socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint8_t* codes,
+                               const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
+                               float* scores, cudaStream_t st, bool pdl) {
   const int Lp = code_slots(c.L);
   const int H_sel = num_sel_rows(c);
   const int G_sel = c.group_mode == SOCKET_GROUP_PER_QHEAD ? c.H_q / c.H_kv : 1;
@@ -365,14 +239,24 @@ socket_status launch_score(const socket_cfg& c, const float* lut, const uint8_t*
   long long grid = kNumSMs;
   if (grid > total_tiles) grid = total_tiles;
   if (grid < 1) return SOCKET_OK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kScoreThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
 #define SK_SCORE_CASE(LPV)                                                                     \
   case LPV: {                                                                                  \
     const size_t smem = lut_bytes_per_row(c.L) + (size_t)kScoreWarps * kScoreStages * TileStage<LPV>::BYTES; \
     auto kfn = score_kernel<LPV>;                                                              \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
-    kfn<<<(unsigned)grid, kScoreThreads, smem, st>>>(lut, codes, vnorm, seq_lens, mask, scores, \
-                                                      H_sel, c.H_kv, G_sel, c.N_max,           \
-                                                      total_tiles);                            \
+    cfg.dynamicSmemBytes = smem;                                                               \
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, lut, codes, vnorm, seq_lens, mask, scores, H_sel, \
+                                       c.H_kv, G_sel, c.N_max, total_tiles);                   \
+    if (e != cudaSuccess) return fail(SOCKET_ECUDA, std::string("score launch: ") + cudaGetErrorString(e)); \
     return check_launch("score_kernel");                                                       \
   }
   switch (Lp) {
@@ -384,6 +268,12 @@ socket_status launch_score(const socket_cfg& c, const float* lut, const uint8_t*
       return fail(SOCKET_EUNSUPPORTED, "score: L > 64 not supported by this kernel");
   }
 #undef SK_SCORE_CASE
+}
+
+socket_status launch_score(const socket_cfg& c, const float* lut, const uint8_t* codes,
+                           const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
+                           float* scores, cudaStream_t st) {
+  return launch_score_pdl(c, lut, codes, vnorm, seq_lens, mask, scores, st, false);
 }
 
 }  // namespace sk

@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
   extern __shared__ __align__(16) uint32_t keys[];          // [per]
   __shared__ TopkShared S;
 
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: scores of the predecessor
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
   const int csize = (int)cluster.num_blocks();
@@ -363,27 +364,30 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
   // gt_rank / eq_rank count keys > T / == T at smaller indices (row-global).
   int em_all = 0;
   if (a.mode == 0) {
-    // per thread 4 consecutive keys; thread order = index order within the CTA
-    int gt_t = 0, eq_t = 0;
-    uint4 kv[1];
-    const int nchunk = len32 >> 2;                    // 4-key chunks
-    const int cpt = (nchunk + kTopkThreads - 1) / kTopkThreads;   // chunks per thread
-    const int c0 = tid * cpt, c1 = min(nchunk, c0 + cpt);
-    for (int cc = c0; cc < c1; ++cc) {
-      kv[0] = *reinterpret_cast<const uint4*>(keys + cc * 4);
-      const uint32_t* kp = &kv[0].x;
+    // warp w owns a contiguous block of 4-key chunks; in each round the warp's
+    // lanes read 32 consecutive chunks (conflict-free 16-byte loads), so index
+    // order = (round, lane, element)
+    const int nchunk = len32 >> 2;
+    const int cpw = ((nchunk + kTopkWarps - 1) / kTopkWarps + 31) & ~31;   // chunks per warp
+    const int c0 = warp * cpw, c1 = min(nchunk, c0 + cpw);
+    int gt_w = 0, eq_w = 0;
+    for (int cc = c0 + lane; cc - lane < c1; cc += 32) {
+      uint4 kv = make_uint4(0, 0, 0, 0);
+      if (cc < c1) kv = *reinterpret_cast<const uint4*>(keys + cc * 4);
+      const uint32_t* kp = &kv.x;
+      int g = 0, e = 0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) { gt_t += kp[e] != 0u && kp[e] > T; eq_t += kp[e] != 0u && kp[e] == T; }
+      for (int x = 0; x < 4; ++x) { g += kp[x] != 0u && kp[x] > T; e += kp[x] != 0u && kp[x] == T; }
+      gt_w += g;
+      eq_w += e;
     }
-    // block exclusive scans of (gt_t, eq_t)
-    int gi = gt_t, ei = eq_t;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int yg = __shfl_up_sync(0xffffffffu, gi, o), ye = __shfl_up_sync(0xffffffffu, ei, o);
-      if (lane >= o) { gi += yg; ei += ye; }
+    for (int o = 16; o >= 1; o >>= 1) {
+      gt_w += __shfl_xor_sync(0xffffffffu, gt_w, o);
+      eq_w += __shfl_xor_sync(0xffffffffu, eq_w, o);
     }
     __syncthreads();
-    if (lane == 31) { S.scan[warp] = gi; S.scan2[warp] = ei; }
+    if (lane == 0) { S.scan[warp] = gt_w; S.scan2[warp] = eq_w; }
     __syncthreads();
     int gw = 0, ew = 0, gtot = 0, etot = 0;
 #pragma unroll
@@ -395,23 +399,34 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
     if (tid == 0) { S.stat[5] = (uint32_t)gtot; S.stat[6] = (uint32_t)etot; }
     cluster.sync();
     int gt_before = 0, eq_before = 0;
-    for (int c = 0; c < csize; ++c) {
+    for (int c = 0; c < crank; ++c) {
       const uint32_t* rs = cluster.map_shared_rank(S.stat, c);
-      if (c < crank) { gt_before += (int)rs[5]; eq_before += (int)rs[6]; }
+      gt_before += (int)rs[5];
+      eq_before += (int)rs[6];
     }
     em_all = (int)k_eff;
-    int gr = gt_before + gw + gi - gt_t;               // row-global exclusive ranks
-    int er = eq_before + ew + ei - eq_t;
+    int gbase = gt_before + gw, ebase = eq_before + ew;   // ranks at the start of the round
     int32_t* orow = a.idx + (size_t)row * a.k;
     float* srow = a.sel_scores ? a.sel_scores + (size_t)row * a.k : nullptr;
-    for (int cc = c0; cc < c1; ++cc) {
-      kv[0] = *reinterpret_cast<const uint4*>(keys + cc * 4);
-      const uint32_t* kp = &kv[0].x;
+    for (int cc = c0 + lane; cc - lane < c1; cc += 32) {
+      uint4 kv = make_uint4(0, 0, 0, 0);
+      if (cc < c1) kv = *reinterpret_cast<const uint4*>(keys + cc * 4);
+      const uint32_t* kp = &kv.x;
+      int g = 0, e = 0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t key = kp[e];
+      for (int x = 0; x < 4; ++x) { g += kp[x] != 0u && kp[x] > T; e += kp[x] != 0u && kp[x] == T; }
+      int gi = g, ei = e;                          // inclusive scans over lanes
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int yg = __shfl_up_sync(0xffffffffu, gi, o), ye = __shfl_up_sync(0xffffffffu, ei, o);
+        if (lane >= o) { gi += yg; ei += ye; }
+      }
+      int gr = gbase + gi - g, er = ebase + ei - e;   // exclusive ranks of this lane's first key
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const uint32_t key = kp[x];
         if (key == 0u) continue;
-        const int j = base + cc * 4 + e;
+        const int j = base + cc * 4 + x;
         if (key > T) {
           const int pos = gr + min(er, (int)quota);
           orow[pos] = j;
@@ -419,13 +434,14 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
           ++gr;
         } else if (key == T) {
           if (er < (int)quota) {
-            const int pos = gr + er;
-            orow[pos] = j;
-            if (srow) srow[pos] = load_elem(a, row, j);
+            orow[gr + er] = j;
+            if (srow) srow[gr + er] = load_elem(a, row, j);
           }
           ++er;
         }
       }
+      gbase += __shfl_sync(0xffffffffu, gi, 31);
+      ebase += __shfl_sync(0xffffffffu, ei, 31);
     }
   } else {
     const int groups = len32 >> 5;
@@ -501,7 +517,7 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
   cluster.sync();   // keep shared memory alive until every CTA finished remote reads
 }
 
-static socket_status launch_topk_common(TopkArgs a, int n_max_row, cudaStream_t st) {
+static socket_status launch_topk_common(TopkArgs a, int n_max_row, cudaStream_t st, bool pdl = false) {
   // cluster size: enough CTAs to keep the machine busy, slices fit in smem
   const size_t kMaxSlice = 40 * 1024;   // keys per CTA (160 KB)
   int cs = 1;
@@ -520,21 +536,23 @@ static socket_status launch_topk_common(TopkArgs a, int n_max_row, cudaStream_t 
   cfg.blockDim = dim3(kTopkThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, a);
   if (e != cudaSuccess) return fail(SOCKET_ECUDA, std::string("topk launch: ") + cudaGetErrorString(e));
   return check_launch("topk_cluster_kernel");
 }
 
-socket_status launch_topk(const socket_cfg& c, const float* scores, const int32_t* seq_lens,
-                          int k, int sink, int window, int32_t* idx, int32_t* cnt,
-                          float* sel_scores, cudaStream_t st) {
+socket_status launch_topk_pdl(const socket_cfg& c, const float* scores, const int32_t* seq_lens,
+                              int k, int sink, int window, int32_t* idx, int32_t* cnt,
+                              float* sel_scores, cudaStream_t st, bool pdl) {
   TopkArgs a = {};
   a.mode = 0;
   a.scores = scores;
@@ -549,7 +567,13 @@ socket_status launch_topk(const socket_cfg& c, const float* scores, const int32_
   a.cnt = cnt;
   a.sel_scores = sel_scores;
   if (a.rows == 0) return SOCKET_OK;
-  return launch_topk_common(a, c.N_max, st);
+  return launch_topk_common(a, c.N_max, st, pdl);
+}
+
+socket_status launch_topk(const socket_cfg& c, const float* scores, const int32_t* seq_lens,
+                          int k, int sink, int window, int32_t* idx, int32_t* cnt,
+                          float* sel_scores, cudaStream_t st) {
+  return launch_topk_pdl(c, scores, seq_lens, k, sink, window, idx, cnt, sel_scores, st, false);
 }
 
 socket_status launch_topk_resolve(const socket_cfg& c, const float* cand_scores,

@@ -146,6 +146,51 @@ def score(cfg: Config, q, W, codes, vnorm, seq_lens, mask=None, out=None, ws=Non
     return out
 
 
+def build_lut(cfg: Config, q, W, lut=None):
+    """Alg. 2 tables as the score kernel's shared-memory image (opaque buffer)."""
+    if lut is None:
+        lut = workspace(cfg, _lib.OP_SCORE, 1, q.device)
+    c = cfg.c()
+    check(lib().socket_build_lut(ctypes.byref(c), _p(q), _p(W), _p(lut), lut.numel(), _stream(q)))
+    return lut
+
+
+def score_lut(cfg: Config, lut, codes, vnorm, seq_lens, mask=None, out=None):
+    """Eq. 4 + Alg. 4 scores from a LUT built by build_lut."""
+    if out is None:
+        out = torch.empty((cfg.B, cfg.H_sel, cfg.N_max), dtype=torch.float32, device=lut.device)
+    c = cfg.c()
+    check(lib().socket_score_lut(ctypes.byref(c), _p(lut), _p(codes), _p(vnorm), _p(seq_lens),
+                                 _p(mask), _p(out), _stream(lut)))
+    return out
+
+
+def decode_step(cfg: Config, q, K, V, W, codes, vnorm, seq_lens, k: int, append: bool = True,
+                sink: int = 0, window: int = 0, mask=None, scores=None, idx=None, cnt=None,
+                out=None, lse=None, ws=None):
+    """One fused decode step (append-hash of key seq_lens[b]-1, tables, scores,
+    top-k, sparse decode) -- socket_decode_step."""
+    dev = q.device
+    if scores is None:
+        scores = torch.empty((cfg.B, cfg.H_sel, cfg.N_max), dtype=torch.float32, device=dev)
+    if idx is None:
+        idx = torch.empty((cfg.B, cfg.H_sel, k), dtype=torch.int32, device=dev)
+    if cnt is None:
+        cnt = torch.empty((cfg.B, cfg.H_sel), dtype=torch.int32, device=dev)
+    if out is None:
+        out = torch.empty((cfg.B, cfg.H_q, cfg.d), dtype=torch.bfloat16, device=dev)
+    if lse is None:
+        lse = torch.empty((cfg.B, cfg.H_q), dtype=torch.float32, device=dev)
+    if ws is None:
+        ws = workspace(cfg, _lib.OP_DECODE_STEP, k, dev)
+    c = cfg.c()
+    check(lib().socket_decode_step(ctypes.byref(c), _p(q), _p(K), _p(V), _p(W), _p(codes), _p(vnorm),
+                                   _p(seq_lens), _p(mask), int(bool(append)), k, sink, window,
+                                   _p(scores), _p(idx), _p(cnt), _p(out), _p(lse), _p(ws),
+                                   ws.numel(), _stream(q)))
+    return out, lse
+
+
 def topk(cfg: Config, scores, seq_lens, k: int, sink: int = 0, window: int = 0,
          idx=None, cnt=None, sel_scores=None, want_scores: bool = False):
     """Alg. 3 l.244 TopK: idx [B][H_sel][k] ascending (-1 past cnt), cnt [B][H_sel]."""

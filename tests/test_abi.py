@@ -80,10 +80,10 @@ def test_invalid_arguments_rejected(L):
     assert L.socket_topk(ctypes.byref(c), d, d, 0, 0, 0, d, d, None, None, 0, None) == 1
     assert L.socket_topk(ctypes.byref(c), d, d, 4, 3, 2, d, d, None, None, 0, None) == 1
     assert L.socket_topk(ctypes.byref(c), d, d, 65, 0, 0, d, d, None, None, 0, None) == 1
-    # score with too small workspace
-    need = L.socket_workspace_bytes(ctypes.byref(c), 2, 0)
+    # sparse decode with too small a workspace (checked on the host, no launch)
+    need = L.socket_workspace_bytes(ctypes.byref(c), 4, 16)
     assert need > 0
-    assert L.socket_score(ctypes.byref(c), d, d, d, d, d, None, d, d, need - 1, None) == 4
+    assert L.socket_sparse_decode(ctypes.byref(c), d, d, d, d, d, 16, d, None, None, d, 16, None) == 4
     # resolve rank out of range
     assert L.socket_topk_resolve(ctypes.byref(c), d, d, 2, 2, 4, d, d, None, 0, None) == 1
     # null cfg
@@ -96,4 +96,6 @@ def test_workspace_sizes(L):
     assert L.socket_workspace_bytes(ctypes.byref(c), 2, 0) == 2 * 8 * 65536
     c2 = _cfg(B=2, H_q=32, H_kv=8, N_max=32768, L=60, group_mode=1)
     assert L.socket_workspace_bytes(ctypes.byref(c2), 2, 0) == 2 * 32 * 65536
-    assert L.socket_workspace_bytes(ctypes.byref(c), 4, 3277) > 0
+    # decode: split partials (m, l, o[128]) per (b, q head, split) + one ticket per unit
+    w = L.socket_workspace_bytes(ctypes.byref(c), 4, 3277)
+    assert w >= 2 * 32 * 130 * 4 + 2 * 8 * 4

@@ -357,8 +357,8 @@ def test_cuda_graph_replay_matches_eager():
     cfg, c, W, d = make(2, 8, 2, 2048, 60, 8, seed=31)
     dec = SocketDecoder(cfg, d["W"], d["K"], d["V"], k=205)
     dec.prefill()
-    out_e, lse_e = [t.clone() for t in dec.step(d["q"], d["seq_lens"], append_pos=2047)]
-    dec.capture(d["q"], d["seq_lens"], append_pos=2047)
+    out_e, lse_e = [t.clone() for t in dec.step(d["q"], d["seq_lens"], append=True)]
+    dec.capture(d["q"], d["seq_lens"], append=True)
     out_g, lse_g = dec.replay()
     torch.cuda.synchronize()
     assert torch.equal(out_e, out_g) and torch.equal(lse_e, lse_g)     # deterministic
@@ -407,7 +407,7 @@ def test_full_size_c2_sampled(B, k):
     lens = torch.full((B,), N, dtype=torch.int32, device=DEV)
     dec = SocketDecoder(cfg, W, K, V, k=k)
     dec.prefill()
-    out, lse = dec.step(q, lens, append_pos=N - 1)
+    out, lse = dec.step(q, lens, append=True)
     torch.cuda.synchronize()
     rng = np.random.default_rng(0)
     for (b, g) in [(0, 0), (B - 1, 7), (int(rng.integers(B)), int(rng.integers(8)))]:
@@ -427,3 +427,54 @@ def test_full_size_c2_sampled(B, k):
         for h in range(4):
             y, _ = O.sparse_attention(qf[h], Kf, Vf, S_gpu, cfg.scale)
             assert np.max(np.abs(out[b, g * 4 + h].float().cpu().numpy() - y)) <= 2e-3
+
+
+def test_decode_step_fused_matches_unfused():
+    """socket_decode_step (fused prologue + PDL chain) is bit-identical to the
+    stage-by-stage calls."""
+    cfg, c, W, d = make(2, 8, 2, 4096, 60, 8, seed=41)
+    a = SocketDecoder(cfg, d["W"], d["K"].clone(), d["V"].clone(), k=409)
+    b = SocketDecoder(cfg, d["W"], d["K"].clone(), d["V"].clone(), k=409)
+    a.prefill()
+    b.prefill()
+    oa, la = [t.clone() for t in a.step(d["q"], d["seq_lens"], append=True)]
+    ob, lb = [t.clone() for t in b.step_unfused(d["q"], d["seq_lens"], append=True)]
+    assert torch.equal(a.codes, b.codes) and torch.equal(a.vnorm, b.vnorm)
+    assert torch.equal(a.scores, b.scores)
+    assert torch.equal(a.idx, b.idx) and torch.equal(a.cnt, b.cnt)
+    assert torch.equal(oa, ob) and torch.equal(la, lb)
+
+
+def test_decode_step_ragged_sink_window_mask_vs_oracle():
+    """Fused step with ragged lengths (the append hashes key seq_lens[b]-1 of each
+    sequence), sink/window forcing and a key mask, against the oracle."""
+    lens = [3000, 4096, 1]
+    cfg, c, W, d = make(3, 8, 2, 4096, 16, 8, seed=43, seq_lens=lens)
+    k, sink, window = 300, 4, 16
+    dec = SocketDecoder(cfg, d["W"], d["K"], d["V"], k=k, sink=sink, window=window)
+    dec.prefill(n_tokens=4096)
+    mask = torch.ones((3, 4096), dtype=torch.uint8, device=DEV)
+    mask[:, 100:200] = 0
+    out, lse = dec.step(d["q"], d["seq_lens"], append=True, mask=mask)
+    ref = O.decode_step(c["q"], c["K"], c["V"], W, c["seq_lens"], tau=0.5, k=k, sm_scale=cfg.scale,
+                        sink=sink, window=window, mask=mask.cpu().numpy())
+    q, K, V = O.widen(c["q"]), O.widen(c["K"]), O.widen(c["V"])
+    idx, cnt = dec.idx.cpu().numpy(), dec.cnt.cpu().numpy()
+    sc = dec.scores.cpu().numpy()
+    for b in range(3):
+        for r in range(2):
+            s_ref = ref["scores"][(b, r)]
+            fin = np.isfinite(s_ref)
+            assert np.array_equal(np.isfinite(sc[b, r]), fin)
+            assert np.max(rel_err(sc[b, r][fin], s_ref[fin])) <= 1e-5
+            S_ref = ref["sel"][(b, r)]
+            S = idx[b, r, :cnt[b, r]]
+            assert len(S) == len(S_ref)
+            kth = np.sort(s_ref[S_ref])[0] if len(S_ref) else 0
+            for j in np.setxor1d(S, S_ref):
+                assert abs(s_ref[j] - kth) <= 1e-5 * abs(kth)
+            forced = [j for j in range(lens[b]) if (j < sink or j >= lens[b] - window) and mask[b, j]]
+            assert set(forced) <= set(S.tolist())
+            for h in range(r * 4, r * 4 + 4):
+                y, _ = O.sparse_attention(q[b, h], K[b, r], V[b, r], S, cfg.scale)
+                assert np.max(np.abs(out[b, h].float().cpu().numpy() - y)) <= 2e-3

@@ -380,3 +380,15 @@ def test_soft_ranking_beats_hard_on_gaussian_keys():
         soft_p.append(len(truth & set(O.topk_select(ws, k, N))) / k)
         hard_p.append(len(truth & set(O.topk_select(wh, k, N))) / k)
     assert np.mean(soft_p) > np.mean(hard_p)
+
+
+def test_golden_table6_defaults_are_the_build_defaults():
+    """tests/golden/table6_defaults.json: the build's defaults P=8,
+    L=60 and tau in [0.3, 0.7] come from Table 6."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table6_defaults.json")))
+    from paper_2602_06283_b200.ops import Config
+    c = Config(B=1, H_q=1, H_kv=1, N_max=32)
+    row = g["rows"][0]
+    assert (c.P, c.L) == (row["P"], row["L"]) and row["tau"][0] <= c.tau <= row["tau"][1]

@@ -36,7 +36,7 @@ dec.prefill()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(a.steps):
     flush.zero_()
-    dec.step(q, lens, append_pos=N - 1)
+    dec.step(q, lens, append=True)
     if a.dense:
         from paper_2602_06283_b200 import ops
         ops.dense_decode(cfg, q, K, V, lens)
