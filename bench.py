@@ -134,7 +134,7 @@ def peaks():
 # ---------------------------------------------------------------------------
 # CPU oracle (reference arm / cpu_baseline): one (b, kv-head) unit at a time
 # ---------------------------------------------------------------------------
-def oracle_units(a, k, seconds):
+def oracle_units(a, k, seconds, units=None, skip=0):
     import numpy as np
 
     import datagen
@@ -145,9 +145,7 @@ def oracle_units(a, k, seconds):
     Wb = datagen.make_projections(4242, L, P, 128)
     codes, _ = O.hash_keys(O.widen(c["K"]), O.widen(Wb))   # prefill: not part of a step
     mode = O.GROUP_KV_SHARED if a.mode == "kv_shared" else O.GROUP_PER_QHEAD
-    t0 = time.perf_counter()
-    units = 0
-    while True:
+    def one_unit():
         # one decode step of one (b, kv-head) unit: append-hash of the newest key,
         # tables, scores, top-k, attention of the group's 4 query heads
         kn, _ = O.hash_keys(O.widen(c["K"][0, 0, N - 1:N]), O.widen(Wb))
@@ -155,10 +153,24 @@ def oracle_units(a, k, seconds):
         rows = [(0, 0)] if mode == O.GROUP_KV_SHARED else [(0, h) for h in range(4)]
         O.decode_step(c["q"], c["K"], c["V"], Wb, c["seq_lens"], tau=a.tau, k=k,
                       sm_scale=1 / math.sqrt(128), group_mode=mode, codes=codes, rows=rows)
-        units += 1
+
+    if units is not None:                  # fixed number of samples, first `skip` untimed
+        for _ in range(skip):
+            one_unit()
+        t0 = time.perf_counter()
+        for _ in range(units - skip):
+            one_unit()
         el = time.perf_counter() - t0
-        if el >= seconds:
-            break
+        units = units - skip
+    else:                                  # time-bounded sample
+        t0 = time.perf_counter()
+        units = 0
+        while True:
+            one_unit()
+            units += 1
+            el = time.perf_counter() - t0
+            if el >= seconds:
+                break
     per_unit = el / units
     step_units = a.batch * 8                    # (b, kv-head) units of one full step
     t_step = per_unit * step_units
@@ -174,11 +186,14 @@ def oracle_units(a, k, seconds):
 
 
 def run_reference(a):
+    """Reference arm of this tier: the CPU oracle.  Each of the W + K steps is a
+    bounded sample -- one (b, kv-head) unit of the decode step -- timed on the
+    host; the K timed units are extrapolated to the full step (B * 8 units)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cfg, k = workload(a)
-    cb = oracle_units(a, k, a.cpu_seconds)
+    cb = oracle_units(a, k, 0.0, units=a.warmup + a.steps, skip=a.warmup)
     line = {"metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": cb["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
