@@ -8,6 +8,8 @@
 // The split kernel (tensor-core mma.sync, decode_mma.cu) writes one partial
 // (m, l, o) per (b, head, split); the last split CTA of each unit merges them
 // (combine_kernel serves socket_lse_combine across sequence shards).
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace sk {
@@ -81,7 +83,9 @@ static void decode_geometry(const socket_cfg& c, int k, bool dense, int& units, 
   const int H_sel = per_q ? c.H_q : c.H_kv;
   units = c.B * H_sel;
   NH = per_q ? 1 : c.H_q / c.H_kv;
-  pick_splits(units, dense ? c.N_max : k, kMmaGran, kMmaMaxRps, 4 * kNumSMs, n_splits, rps);
+  const char* tune = getenv("SOCKET_DECODE_TARGET");   // tuning experiments only
+  const int target = tune ? atoi(tune) : kNumSMs;   // one CTA per SM (tools/tune_step.py)
+  pick_splits(units, dense ? c.N_max : k, kMmaGran, kMmaMaxRps, target, n_splits, rps);
 }
 
 static size_t part_bytes(const socket_cfg& c, int ns) {

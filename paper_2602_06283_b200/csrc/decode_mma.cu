@@ -261,26 +261,72 @@ decode_mma_kernel(MmaArgs a) {
   if (!s_last) return;
   __threadfence();
   constexpr float kLn2M = 0.6931471805599453f;
-  for (int x = tid; x < NH * kD; x += kMmaThreads) {
-    const int h = x / kD, e = x % kD;
-    const float* pb = a.part + ((size_t)b * a.H_q + h0 + h) * a.n_splits * (kD + 2);
+  // (a) per head: M = max_s m_s, split weights w_s = 2^(m_s - M) into smem (the
+  //     ring is free now), L = sum_s w_s l_s.  One warp per head, lanes over splits.
+  const int ns = a.n_splits;
+  float* sw = reinterpret_cast<float*>(ring);                 // [NH][ns] weights
+  float* sML = sw + NH * ns;                                  // [NH][2]  M, L
+  const size_t pstride = (size_t)ns * (kD + 2);
+  for (int h = warp; h < NH; h += kMmaWarps) {
+    const float* pb = a.part + ((size_t)b * a.H_q + h0 + h) * pstride;
     float M = -INFINITY;
-    for (int s2 = 0; s2 < a.n_splits; ++s2) M = fmaxf(M, __ldcg(pb + (size_t)s2 * (kD + 2)));
-    float Ls = 0.f, O = 0.f;
-    if (M != -INFINITY) {
-      for (int s2 = 0; s2 < a.n_splits; ++s2) {
-        const float* p2 = pb + (size_t)s2 * (kD + 2);
-        const float wt = exp2f(__ldcg(p2) - M);
-        Ls = fmaf(wt, __ldcg(p2 + 1), Ls);
-        O = fmaf(wt, __ldcg(p2 + 2 + e), O);
+    for (int s2 = lane; s2 < ns; s2 += 32) M = fmaxf(M, __ldcg(pb + (size_t)s2 * (kD + 2)));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float Ls = 0.f;
+    for (int s2 = lane; s2 < ns; s2 += 32) {
+      const float* p2 = pb + (size_t)s2 * (kD + 2);
+      const float wt = (M == -INFINITY) ? 0.f : exp2f(__ldcg(p2) - M);
+      sw[h * ns + s2] = wt;
+      Ls = fmaf(wt, __ldcg(p2 + 1), Ls);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, o);
+    if (lane == 0) { sML[2 * h] = M; sML[2 * h + 1] = Ls; }
+  }
+  __syncthreads();
+  // (b) each thread owns 4 consecutive dims of one head and streams the split
+  //     partials with independent float2 loads (the row pitch d + 2 keeps 8-byte
+  //     alignment), 8 splits in flight
+  for (int x = tid; x < NH * (kD / 4); x += kMmaThreads) {
+    const int h = x / (kD / 4), e = (x % (kD / 4)) * 4;
+    const float* pb = a.part + ((size_t)b * a.H_q + h0 + h) * pstride + 2 + e;
+    const float* wh = sw + h * ns;
+    float O0 = 0.f, O1 = 0.f, O2 = 0.f, O3 = 0.f;
+    int s2 = 0;
+    for (; s2 + 8 <= ns; s2 += 8) {
+      float2 u[8], v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        u[j] = __ldcg(reinterpret_cast<const float2*>(pb + (size_t)(s2 + j) * (kD + 2)));
+        v[j] = __ldcg(reinterpret_cast<const float2*>(pb + (size_t)(s2 + j) * (kD + 2) + 2));
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float wt = wh[s2 + j];
+        O0 = fmaf(wt, u[j].x, O0); O1 = fmaf(wt, u[j].y, O1);
+        O2 = fmaf(wt, v[j].x, O2); O3 = fmaf(wt, v[j].y, O3);
       }
     }
+    for (; s2 < ns; ++s2) {
+      const float2 u = __ldcg(reinterpret_cast<const float2*>(pb + (size_t)s2 * (kD + 2)));
+      const float2 v = __ldcg(reinterpret_cast<const float2*>(pb + (size_t)s2 * (kD + 2) + 2));
+      const float wt = wh[s2];
+      O0 = fmaf(wt, u.x, O0); O1 = fmaf(wt, u.y, O1);
+      O2 = fmaf(wt, v.x, O2); O3 = fmaf(wt, v.y, O3);
+    }
+    const float M = sML[2 * h], Ls = sML[2 * h + 1];
     const size_t bh = (size_t)b * a.H_q + h0 + h;
-    if (a.out) a.out[bh * kD + e] = (uint16_t)f2bf_bits(Ls > 0.f ? O / Ls : 0.f);
+    if (a.out) {
+      uint2 pk;
+      pk.x = pack_bf16(Ls > 0.f ? O0 / Ls : 0.f, Ls > 0.f ? O1 / Ls : 0.f);
+      pk.y = pack_bf16(Ls > 0.f ? O2 / Ls : 0.f, Ls > 0.f ? O3 / Ls : 0.f);
+      *reinterpret_cast<uint2*>(a.out + bh * kD + e) = pk;
+    }
     if (e == 0 && a.lse) a.lse[bh] = (Ls > 0.f) ? (M + log2f(Ls)) * kLn2M : -INFINITY;
     if (a.part_out) {
       float* po = a.part_out + bh * (kD + 2);
-      po[2 + e] = O;
+      po[2 + e] = O0; po[3 + e] = O1; po[4 + e] = O2; po[5 + e] = O3;
       if (e == 0) { po[0] = (M == -INFINITY) ? -INFINITY : M * kLn2M; po[1] = Ls; }
     }
   }
@@ -315,6 +361,8 @@ socket_status launch_decode_mma(const socket_cfg& c, const void* q, const void* 
   a.out = (uint16_t*)out;
   a.lse = lse;
   a.part_out = part_out;
+  if ((size_t)NH * n_splits * sizeof(float) + 64 > (size_t)kMmaRing)
+    return fail(SOCKET_EUNSUPPORTED, "decode: too many splits for the in-kernel LSE merge");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_splits, units);
   cfg.blockDim = dim3(kMmaThreads);

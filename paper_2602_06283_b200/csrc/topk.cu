@@ -20,6 +20,7 @@
 //   a 4-pass MSB radix select over the whole cluster (8-bit digits) is used.
 // A stable ballot compaction then writes the selected indices in ascending order.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -31,6 +32,22 @@ constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int kBins = 2048;
 constexpr int kCandCap = 2048;
+
+#ifdef SK_TRACE
+// phase stamps (clock64 of thread 0 of every CTA), read by tools/trace_topk.py
+__device__ unsigned long long g_topk_trace[4096 * 16];
+#define TK_TRACE(i)                                                                          \
+  do {                                                                                       \
+    if (threadIdx.x == 0) {                                                                  \
+      const int cta = blockIdx.y * gridDim.x + blockIdx.x;                                   \
+      if (cta < 4096) g_topk_trace[cta * 16 + (i)] = clock64();                              \
+    }                                                                                        \
+  } while (0)
+#else
+#define TK_TRACE(i) \
+  do {              \
+  } while (0)
+#endif
 
 struct TopkArgs {
   // mode 0: scores [rows][N_max], n = seq_lens[b]
@@ -75,15 +92,23 @@ __device__ __forceinline__ int block_excl_scan_warps(int v, int* sh, int warp, i
   return pre;
 }
 
-struct TopkShared {
-  uint32_t hist[kBins];          // local histogram (also radix fallback buffers)
-  uint32_t ghist[kBins];         // cluster-summed histogram
-  uint32_t cand[kCandCap];       // local candidates
-  uint32_t gcand[kCandCap];      // gathered candidates
+struct __align__(16) TopkShared {
+  uint32_t hist[kBins];          // local histogram (radix fallback: two 256-bin buffers)
+  uint32_t cand[kCandCap];       // local candidates: keys of the target bin
+  uint32_t cidx[kCandCap];       // their slice-local indices
+  uint32_t gcand[kCandCap];      // candidates gathered from the cluster, rank-major
   uint32_t rhist[256];           // local radix histogram for candidate resolve
   int scan[kTopkWarps];
   int scan2[kTopkWarps];
-  uint32_t stat[8];              // nvalid, nforced, kmin, kmax, ncand, gt, eq, emit
+  uint32_t wab[kTopkWarps];      // per warp: keys strictly above the target bin (forced included)
+  uint32_t wgt[kTopkWarps];      // per warp: local candidates > T
+  uint32_t weq[kTopkWarps];      // per warp: local candidates == T
+  uint32_t roff[17];             // gathered-candidate offset of every rank
+  uint32_t rab[16];              // above-bin count of every rank
+  uint32_t glob[4];              // cluster totals: nvalid, nforced, kmin, kmax
+  uint32_t coarse[64];           // local histogram folded into 64 coarse bins (read remotely)
+  uint32_t acc[2];               // lower ranks' candidates > T / == T
+  alignas(16) uint32_t stat[8];  // nvalid, nforced, kmin, kmax, ncand, above, gt, eq (read remotely)
   uint32_t dec[4];
 };
 
@@ -133,28 +158,37 @@ __device__ void local_select(const uint32_t* c, int C, uint32_t need, TopkShared
 }
 
 __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs a) {
-  extern __shared__ __align__(16) uint32_t keys[];          // [per]
+  extern __shared__ __align__(16) uint32_t keys[];          // [per], per % 128 == 0
   __shared__ TopkShared S;
+  constexpr unsigned kFull = 0xffffffffu;
 
+  TK_TRACE(0);
   asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: scores of the predecessor
+  TK_TRACE(1);
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
   const int csize = (int)cluster.num_blocks();
   const int row = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned lt = (1u << lane) - 1u;
   const int b = row / a.H_sel;
   const int n = a.mode == 0 ? a.seq_lens[b] : a.G * a.k;
   const int base = crank * a.per;
   int len = n - base;
   len = len < 0 ? 0 : (len > a.per ? a.per : len);
   const int len32 = (len + 31) & ~31;
+  const int len128 = (len + 127) & ~127;
+  // warp w owns the rounds [r0, r1) of 128 keys; round r covers keys r*128 + x*32 + lane
+  const int nr = len128 >> 7;
+  const int rpw = max(1, (nr + kTopkWarps - 1) / kTopkWarps);
+  const int r0 = warp * rpw, r1 = min(nr, r0 + rpw);
 
   // ---- 0. load slice as keys (4 elements per thread per step) ---------------
   uint32_t nvalid = 0, nforced = 0, kmin = 0xFFFFFFFFu, kmax = 0u;
   if (a.mode == 0) {
     const float* src = a.scores + (size_t)row * a.N_max + base;   // 128-B aligned
     constexpr int U = 4;                                          // float4 loads in flight
-    for (int i0 = tid * 4; i0 < len32; i0 += kTopkThreads * 4 * U) {
+    for (int i0 = tid * 4; i0 < len128; i0 += kTopkThreads * 4 * U) {
       float4 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -170,7 +204,7 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int i4 = i0 + u * kTopkThreads * 4;
-        if (i4 >= len32) break;
+        if (i4 >= len128) break;
         const float vs[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
         uint4 kk;
         uint32_t* kp = &kk.x;
@@ -186,7 +220,7 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
       }
     }
   } else {
-    for (int i = tid; i < len32; i += kTopkThreads) {
+    for (int i = tid; i < len128; i += kTopkThreads) {
       uint32_t key = 0;
       if (i < len) key = make_key(load_elem(a, row, base + i), base + i, n, 0, 0, 1);
       keys[i] = key;
@@ -195,14 +229,16 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
     }
   }
   if (tid < 8) S.stat[tid] = (tid == 2) ? 0xFFFFFFFFu : 0u;   // kmin starts at +max
+  if (tid < kTopkWarps) { S.wgt[tid] = 0; S.weq[tid] = 0; }
+  if (tid < 2) S.acc[tid] = 0;
   for (int i = tid; i < kBins; i += kTopkThreads) S.hist[i] = 0;
   __syncthreads();
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
-    nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
-    nforced += __shfl_xor_sync(0xffffffffu, nforced, o);
-    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    nvalid += __shfl_xor_sync(kFull, nvalid, o);
+    nforced += __shfl_xor_sync(kFull, nforced, o);
+    kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
   }
   if (lane == 0) {
     atomicAdd(&S.stat[0], nvalid);
@@ -210,16 +246,28 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
     atomicMin(&S.stat[2], kmin);
     atomicMax(&S.stat[3], kmax);
   }
+  TK_TRACE(2);
   cluster.sync();
-  uint32_t tvalid = 0, tforced = 0, gmin = 0xFFFFFFFFu, gmax = 0;
-  for (int c = 0; c < csize; ++c) {
-    const uint32_t* rs = cluster.map_shared_rank(S.stat, c);
-    tvalid += rs[0];
-    tforced += rs[1];
-    gmin = min(gmin, rs[2]);
-    gmax = max(gmax, rs[3]);
+  // ---- 1. cluster totals: lane r of warp 0 reads rank r's statistics ----------
+  if (warp == 0) {
+    uint32_t v0 = 0, v1 = 0, v2 = 0xFFFFFFFFu, v3 = 0;
+    if (lane < csize) {
+      const uint4 rs = *reinterpret_cast<const uint4*>(cluster.map_shared_rank(S.stat, lane));
+      v0 = rs.x; v1 = rs.y; v2 = rs.z; v3 = rs.w;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      v0 += __shfl_xor_sync(kFull, v0, o);
+      v1 += __shfl_xor_sync(kFull, v1, o);
+      v2 = min(v2, __shfl_xor_sync(kFull, v2, o));
+      v3 = max(v3, __shfl_xor_sync(kFull, v3, o));
+    }
+    if (lane == 0) { S.glob[0] = v0; S.glob[1] = v1; S.glob[2] = v2; S.glob[3] = v3; }
   }
+  __syncthreads();
+  const uint32_t tvalid = S.glob[0], tforced = S.glob[1], gmin = S.glob[2], gmax = S.glob[3];
   const uint32_t k_eff = min((uint32_t)a.k, tvalid);
+  TK_TRACE(3);
 
   // ---- find T and quota --------------------------------------------------------
   uint32_t T = 0, quota = 0;            // select keys > T, plus `quota` keys == T
@@ -232,74 +280,171 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
     done = true;
   }
   const uint32_t need = k_eff - tforced;  // rank among regular keys (>= 1 when !done)
-  bool fallback = false;
+  bool fallback = false, counted = false;
   if (!done) {
     // 2. adaptive histogram over [gmin, gmax]
     // bin = (key - gmin) >> sh with the smallest sh that maps [gmin, gmax] into
     // kBins bins: monotone and exact (no division)
     const uint32_t span = gmax - gmin;
     const int sh = span < (uint32_t)kBins ? 0 : (32 - __clz(span)) - 11;
-    for (int i = tid; i < len32; i += kTopkThreads) {
-      const uint32_t key = keys[i];
-      if (key != 0u && key != 0xFFFFFFFFu) {
-        atomicAdd(&S.hist[(key - gmin) >> sh], 1u);
-      }
-    }
-    cluster.sync();
-    for (int i = tid; i < kBins; i += kTopkThreads) {
-      uint32_t s = 0;
-      for (int c = 0; c < csize; ++c) s += *cluster.map_shared_rank(&S.hist[i], c);
-      S.ghist[i] = s;
-    }
-    __syncthreads();
-    // suffix scan over bins (descending): each warp owns 128 bins, lane 4 of them
-    {
-      const int b0 = kBins - 1 - (warp * 128 + lane * 4);
-      uint32_t c4[4], tot = 0;
+    for (int i = tid * 4; i < len128; i += kTopkThreads * 4) {
+      const uint4 kv = *reinterpret_cast<const uint4*>(keys + i);
+      const uint32_t k4[4] = {kv.x, kv.y, kv.z, kv.w};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) { c4[q] = S.ghist[b0 - q]; tot += c4[q]; }
+      for (int e = 0; e < 4; ++e)
+        if (k4[e] != 0u && k4[e] != 0xFFFFFFFFu) atomicAdd(&S.hist[(k4[e] - gmin) >> sh], 1u);
+    }
+    // coarse histogram: 64 bins of 32 fine bins each (thread t folds bins 4t..4t+3,
+    // 8 lanes per coarse bin)
+    __syncthreads();
+    {
+      const uint4 h = *reinterpret_cast<const uint4*>(&S.hist[tid * 4]);
+      uint32_t cs4 = h.x + h.y + h.z + h.w;
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) cs4 += __shfl_xor_sync(kFull, cs4, o);
+      if ((lane & 7) == 0) S.coarse[tid >> 3] = cs4;
+    }
+    TK_TRACE(4);
+    cluster.sync();
+    TK_TRACE(5);
+    // cluster sums, coarse then fine (DSMEM: csize x (64 + 32) words per CTA), each
+    // followed by a descending suffix scan that locates the bin of rank `need`
+    if (warp == 0) {
+      uint32_t c0 = 0, c1 = 0;                 // coarse bins 63 - 2 lane, 62 - 2 lane
+      for (int r = 0; r < csize; ++r) {
+        const uint32_t* rc = cluster.map_shared_rank(S.coarse, r);
+        c0 += rc[63 - 2 * lane];
+        c1 += rc[62 - 2 * lane];
+      }
+      const uint32_t tot = c0 + c1;
       uint32_t inc = tot;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        const uint32_t y = __shfl_up_sync(kFull, inc, o);
         if (lane >= o) inc += y;
       }
-      if (lane == 31) S.scan[warp] = (int)inc;
-      __syncthreads();
-      uint32_t wpre = 0;
-      for (int w = 0; w < warp; ++w) wpre += (uint32_t)S.scan[w];
-      const uint32_t excl = wpre + inc - tot;
-      if (excl < need && excl + tot >= need) {
-        uint32_t run = excl;
-        for (int q = 0; q < 4; ++q) {
-          if (run + c4[q] >= need) { S.dec[0] = (uint32_t)(b0 - q); S.dec[1] = need - run; S.dec[2] = c4[q]; break; }
-          run += c4[q];
-        }
+      const uint32_t excl = inc - tot;         // keys in coarse bins above mine
+      const unsigned hit = __ballot_sync(kFull, excl < need && inc >= need);
+      const int hl = __ffs(hit) - 1;
+      const uint32_t ex_h = __shfl_sync(kFull, excl, hl), c0_h = __shfl_sync(kFull, c0, hl);
+      const bool first = ex_h + c0_h >= need;
+      const int cb = first ? 63 - 2 * hl : 62 - 2 * hl;
+      const uint32_t need_c = need - (first ? ex_h : ex_h + c0_h);   // rank inside coarse bin cb
+      // fine bins of cb: lane l holds bin cb*32 + 31 - l (descending)
+      const int fb = cb * 32 + 31 - lane;
+      uint32_t f = 0;
+      for (int r = 0; r < csize; ++r) f += cluster.map_shared_rank(S.hist, r)[fb];
+      uint32_t finc = f;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, finc, o);
+        if (lane >= o) finc += y;
       }
-      __syncthreads();
+      const uint32_t fex = finc - f;
+      if (fex < need_c && finc >= need_c) { S.dec[0] = (uint32_t)fb; S.dec[1] = need_c - fex; S.dec[2] = f; }
     }
+    __syncthreads();
     const uint32_t bstar = S.dec[0], need2 = S.dec[1], C = S.dec[2];
+    TK_TRACE(6);
     if (C <= (uint32_t)kCandCap) {
-      // 3. gather the bin's keys from every CTA, resolve T exactly
-      for (int i = tid; i < len32; i += kTopkThreads) {
-        const uint32_t key = keys[i];
-        if (key != 0u && key != 0xFFFFFFFFu && ((key - gmin) >> sh) == bstar) {
-          const uint32_t pos = atomicAdd(&S.stat[4], 1u);
-          S.cand[pos] = key;
+      // 3. candidate pass: keys of bin bstar -> S.cand (+ slice index); per warp the
+      //    number of keys strictly above the bin (all of them are > T, forced included)
+      uint32_t ab = 0;
+      for (int r = r0; r < r1; ++r) {
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const int i = r * 128 + x * 32 + lane;
+          const uint32_t key = keys[i];
+          const bool reg = key != 0u && key != 0xFFFFFFFFu;
+          const uint32_t bin = (key - gmin) >> sh;
+          ab += __popc(__ballot_sync(kFull, key == 0xFFFFFFFFu || (reg && bin > bstar)));
+          const unsigned cm = __ballot_sync(kFull, reg && bin == bstar);
+          if (cm) {
+            uint32_t slot0 = 0;
+            if (lane == 0) slot0 = atomicAdd(&S.stat[4], (uint32_t)__popc(cm));
+            slot0 = __shfl_sync(kFull, slot0, 0);
+            if ((cm >> lane) & 1u) {
+              const uint32_t sl = slot0 + __popc(cm & lt);
+              S.cand[sl] = key;
+              S.cidx[sl] = (uint32_t)i;
+            }
+          }
         }
       }
+      if (lane == 0) { S.wab[warp] = ab; atomicAdd(&S.stat[5], ab); }
+      TK_TRACE(7);
       cluster.sync();
-      uint32_t off = 0;
-      for (int c = 0; c < csize; ++c) {
-        const uint32_t nc = *cluster.map_shared_rank(&S.stat[4], c);
-        const uint32_t* rc = cluster.map_shared_rank(S.cand, c);
-        for (uint32_t i = tid; i < nc; i += kTopkThreads) S.gcand[off + i] = rc[i];
-        off += nc;
+      TK_TRACE(8);
+      // gather every rank's candidates (rank-major) and above-bin counts
+      if (warp == 0) {
+        uint32_t nc = 0, rab = 0;
+        if (lane < csize) {
+          const uint32_t* rs = cluster.map_shared_rank(S.stat, lane);
+          nc = rs[4];
+          rab = rs[5];
+        }
+        uint32_t inc = nc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (lane < csize) { S.roff[lane + 1] = inc; S.rab[lane] = rab; }
+        if (lane == 0) S.roff[0] = 0;
       }
       __syncthreads();
+      for (int i = tid; i < (int)C; i += kTopkThreads) {
+        int r = 0;
+        while (r + 1 < csize && S.roff[r + 1] <= (uint32_t)i) ++r;
+        S.gcand[i] = cluster.map_shared_rank(S.cand, r)[i - (int)S.roff[r]];
+      }
+      __syncthreads();
+      // T = the need2-th largest candidate, above = candidates > T
       uint32_t above;
-      local_select(S.gcand, (int)C, need2, S, tid, warp, lane, T, above);
+      if (C <= 1024u) {
+        // rank counting: candidate i is T iff #greater < need2 <= #greater + #equal
+        for (int i = tid; i < (int)C; i += kTopkThreads) {
+          const uint32_t me = S.gcand[i];
+          uint32_t gt = 0, eq = 0;
+          int j = 0;
+          for (; j + 4 <= (int)C; j += 4) {
+            const uint4 v = *reinterpret_cast<const uint4*>(&S.gcand[j]);
+            gt += (v.x > me) + (v.y > me) + (v.z > me) + (v.w > me);
+            eq += (v.x == me) + (v.y == me) + (v.z == me) + (v.w == me);
+          }
+          for (; j < (int)C; ++j) { gt += S.gcand[j] > me; eq += S.gcand[j] == me; }
+          if (gt < need2 && gt + eq >= need2) { S.dec[0] = me; S.dec[1] = gt; }   // ties write equal values
+        }
+        __syncthreads();
+        T = S.dec[0];
+        above = S.dec[1];
+      } else {
+        local_select(S.gcand, (int)C, need2, S, tid, warp, lane, T, above);
+      }
       quota = need2 - above;
+      TK_TRACE(9);
+      // keys > T / == T before this CTA and per warp, from the candidate lists alone
+      uint32_t gtb = 0, eqb = 0;
+      for (int i = tid; i < (int)S.roff[crank]; i += kTopkThreads) {
+        const uint32_t cv = S.gcand[i];
+        gtb += cv > T;
+        eqb += cv == T;
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        gtb += __shfl_xor_sync(kFull, gtb, o);
+        eqb += __shfl_xor_sync(kFull, eqb, o);
+      }
+      if (lane == 0 && (gtb | eqb)) { atomicAdd(&S.acc[0], gtb); atomicAdd(&S.acc[1], eqb); }
+      const int nloc = (int)S.stat[4];
+      for (int i = tid; i < nloc; i += kTopkThreads) {
+        const uint32_t cv = S.cand[i];
+        const int w = (int)(S.cidx[i] >> 7) / rpw;
+        if (cv > T) atomicAdd(&S.wgt[w], 1u);
+        else if (cv == T) atomicAdd(&S.weq[w], 1u);
+      }
+      __syncthreads();
+      counted = true;
     } else {
       fallback = true;
     }
@@ -319,7 +464,7 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
         const uint32_t key = keys[i];
         const bool m = key != 0u && key != 0xFFFFFFFFu && (key & hmask) == (prefix & hmask);
         const uint32_t bin = m ? ((key >> shift) & 255u) : 256u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+        const uint32_t peers = __match_any_sync(kFull, bin);
         if (m && lane == __ffs(peers) - 1) atomicAdd(&hb[bin], (uint32_t)__popc(peers));
       }
       cluster.sync();
@@ -336,11 +481,11 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
         uint32_t inc = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+          const uint32_t y = __shfl_up_sync(kFull, inc, o);
           if (lane >= o) inc += y;
         }
         const uint32_t excl = inc - tot;
-        const unsigned hbits = __ballot_sync(0xffffffffu, excl < k_rem && inc >= k_rem);
+        const unsigned hbits = __ballot_sync(kFull, excl < k_rem && inc >= k_rem);
         if (lane == __ffs(hbits) - 1) {
           uint32_t run = excl;
           for (int q = 0; q < 8; ++q) {
@@ -363,85 +508,69 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
   // Output position of a selected key = gt_rank + min(eq_rank, quota), where
   // gt_rank / eq_rank count keys > T / == T at smaller indices (row-global).
   int em_all = 0;
+  TK_TRACE(10);
   if (a.mode == 0) {
-    // warp w owns a contiguous block of 4-key chunks; in each round the warp's
-    // lanes read 32 consecutive chunks (conflict-free 16-byte loads), so index
-    // order = (round, lane, element)
-    const int nchunk = len32 >> 2;
-    const int cpw = ((nchunk + kTopkWarps - 1) / kTopkWarps + 31) & ~31;   // chunks per warp
-    const int c0 = warp * cpw, c1 = min(nchunk, c0 + cpw);
-    int gt_w = 0, eq_w = 0;
-    for (int cc = c0 + lane; cc - lane < c1; cc += 32) {
-      uint4 kv = make_uint4(0, 0, 0, 0);
-      if (cc < c1) kv = *reinterpret_cast<const uint4*>(keys + cc * 4);
-      const uint32_t* kp = &kv.x;
-      int g = 0, e = 0;
+    int gbase, ebase;   // row-global ranks of this warp's first key
+    if (counted) {
+      uint32_t gb = S.acc[0], eb = S.acc[1];
+      for (int r = 0; r < crank; ++r) gb += S.rab[r];
+      uint32_t gw = 0, ew = 0;
+      for (int w = 0; w < warp; ++w) { gw += S.wab[w] + S.wgt[w]; ew += S.weq[w]; }
+      gbase = (int)(gb + gw);
+      ebase = (int)(eb + ew);
+    } else {
+      // everything / only forced keys selected, or the radix fallback: count pass
+      uint32_t g = 0, e = 0;
+      for (int r = r0; r < r1; ++r) {
 #pragma unroll
-      for (int x = 0; x < 4; ++x) { g += kp[x] != 0u && kp[x] > T; e += kp[x] != 0u && kp[x] == T; }
-      gt_w += g;
-      eq_w += e;
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      gt_w += __shfl_xor_sync(0xffffffffu, gt_w, o);
-      eq_w += __shfl_xor_sync(0xffffffffu, eq_w, o);
-    }
-    __syncthreads();
-    if (lane == 0) { S.scan[warp] = gt_w; S.scan2[warp] = eq_w; }
-    __syncthreads();
-    int gw = 0, ew = 0, gtot = 0, etot = 0;
-#pragma unroll
-    for (int w = 0; w < kTopkWarps; ++w) {
-      const int xg = S.scan[w], xe = S.scan2[w];
-      gw += w < warp ? xg : 0; ew += w < warp ? xe : 0;
-      gtot += xg; etot += xe;
-    }
-    if (tid == 0) { S.stat[5] = (uint32_t)gtot; S.stat[6] = (uint32_t)etot; }
-    cluster.sync();
-    int gt_before = 0, eq_before = 0;
-    for (int c = 0; c < crank; ++c) {
-      const uint32_t* rs = cluster.map_shared_rank(S.stat, c);
-      gt_before += (int)rs[5];
-      eq_before += (int)rs[6];
-    }
-    em_all = (int)k_eff;
-    int gbase = gt_before + gw, ebase = eq_before + ew;   // ranks at the start of the round
-    int32_t* orow = a.idx + (size_t)row * a.k;
-    float* srow = a.sel_scores ? a.sel_scores + (size_t)row * a.k : nullptr;
-    for (int cc = c0 + lane; cc - lane < c1; cc += 32) {
-      uint4 kv = make_uint4(0, 0, 0, 0);
-      if (cc < c1) kv = *reinterpret_cast<const uint4*>(keys + cc * 4);
-      const uint32_t* kp = &kv.x;
-      int g = 0, e = 0;
-#pragma unroll
-      for (int x = 0; x < 4; ++x) { g += kp[x] != 0u && kp[x] > T; e += kp[x] != 0u && kp[x] == T; }
-      int gi = g, ei = e;                          // inclusive scans over lanes
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int yg = __shfl_up_sync(0xffffffffu, gi, o), ye = __shfl_up_sync(0xffffffffu, ei, o);
-        if (lane >= o) { gi += yg; ei += ye; }
-      }
-      int gr = gbase + gi - g, er = ebase + ei - e;   // exclusive ranks of this lane's first key
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        const uint32_t key = kp[x];
-        if (key == 0u) continue;
-        const int j = base + cc * 4 + x;
-        if (key > T) {
-          const int pos = gr + min(er, (int)quota);
-          orow[pos] = j;
-          if (srow) srow[pos] = load_elem(a, row, j);
-          ++gr;
-        } else if (key == T) {
-          if (er < (int)quota) {
-            orow[gr + er] = j;
-            if (srow) srow[gr + er] = load_elem(a, row, j);
-          }
-          ++er;
+        for (int x = 0; x < 4; ++x) {
+          const uint32_t key = keys[r * 128 + x * 32 + lane];
+          g += __popc(__ballot_sync(kFull, key > T));
+          e += __popc(__ballot_sync(kFull, key != 0u && key == T));
         }
       }
-      gbase += __shfl_sync(0xffffffffu, gi, 31);
-      ebase += __shfl_sync(0xffffffffu, ei, 31);
+      if (lane == 0) { S.scan[warp] = (int)g; S.scan2[warp] = (int)e; }
+      __syncthreads();
+      uint32_t gw = 0, ew = 0, gtot = 0, etot = 0;
+#pragma unroll
+      for (int w = 0; w < kTopkWarps; ++w) {
+        const uint32_t xg = (uint32_t)S.scan[w], xe = (uint32_t)S.scan2[w];
+        gw += w < warp ? xg : 0u; ew += w < warp ? xe : 0u;
+        gtot += xg; etot += xe;
+      }
+      if (tid == 0) { S.stat[6] = gtot; S.stat[7] = etot; }
+      cluster.sync();
+      uint32_t gb = 0, eb = 0;
+      for (int r = 0; r < crank; ++r) {
+        const uint32_t* rs = cluster.map_shared_rank(S.stat, r);
+        gb += rs[6];
+        eb += rs[7];
+      }
+      gbase = (int)(gb + gw);
+      ebase = (int)(eb + ew);
+    }
+    TK_TRACE(11);
+    em_all = (int)k_eff;
+    int32_t* orow = a.idx + (size_t)row * a.k;
+    float* srow = a.sel_scores ? a.sel_scores + (size_t)row * a.k : nullptr;
+    const int q = (int)quota;
+    for (int r = r0; r < r1; ++r) {
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int i = r * 128 + x * 32 + lane;
+        const uint32_t key = keys[i];
+        const bool isgt = key > T, iseq = key != 0u && key == T;
+        const unsigned gm = __ballot_sync(kFull, isgt), em = __ballot_sync(kFull, iseq);
+        const int gr = gbase + __popc(gm & lt), er = ebase + __popc(em & lt);
+        const int j = base + i;
+        if (isgt || (iseq && er < q)) {
+          const int pos = gr + min(er, q);
+          orow[pos] = j;
+          if (srow) srow[pos] = load_elem(a, row, j);
+        }
+        gbase += __popc(gm);
+        ebase += __popc(em);
+      }
     }
   } else {
     const int groups = len32 >> 5;
@@ -506,6 +635,7 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
       eq_run += __popc(eb);
     }
   }
+  TK_TRACE(12);
   if (crank == 0) {
     int32_t* orow = a.idx + (size_t)row * a.k;
     for (int p = em_all + tid; p < a.k; p += kTopkThreads) {
@@ -514,17 +644,27 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
     }
     if (tid == 0) a.cnt[row] = em_all;
   }
+  TK_TRACE(13);
   cluster.sync();   // keep shared memory alive until every CTA finished remote reads
+  TK_TRACE(14);
 }
+
+#ifdef SK_TRACE
+extern "C" int socket_debug_topk_trace(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_topk_trace, (size_t)n * sizeof(unsigned long long));
+}
+#endif
 
 static socket_status launch_topk_common(TopkArgs a, int n_max_row, cudaStream_t st, bool pdl = false) {
   // cluster size: enough CTAs to keep the machine busy, slices fit in smem
   const size_t kMaxSlice = 40 * 1024;   // keys per CTA (160 KB)
   int cs = 1;
-  while (cs < 16 && ((size_t)(n_max_row + cs - 1) / cs > kMaxSlice || a.rows * cs < kNumSMs))
+  const char* tune = getenv("SOCKET_TOPK_MIN_CTAS");   // tuning experiments only
+  const int min_ctas = tune ? atoi(tune) : kNumSMs;
+  while (cs < 16 && ((size_t)(n_max_row + cs - 1) / cs > kMaxSlice || a.rows * cs < min_ctas))
     cs *= 2;
   int per = (n_max_row + cs - 1) / cs;
-  per = (per + 31) & ~31;
+  per = (per + 127) & ~127;
   if ((size_t)per > kMaxSlice) return fail(SOCKET_EUNSUPPORTED, "topk: row too long for one cluster");
   a.per = per;
   const size_t smem = (size_t)per * sizeof(uint32_t);
