@@ -71,19 +71,60 @@ hash_keys_simt_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict
   }
 }
 
-// ||v_j||_2: one warp per row, lane sums 4 elements, fixed butterfly order.
-__global__ void vnorm_kernel(const uint16_t* __restrict__ V, float* __restrict__ vnorm,
-                             int N_max, int n_begin, int n_count, int rows_total) {
+// ||v_j||_2.  A warp handles 32 consecutive rows: lane t holds elements
+// 4t .. 4t+3 of every row (same per-lane fma order as append_cta) and the 32
+// lane partials of the 32 rows are summed by a recursive-halving
+// reduce-scatter, which pairs lanes exactly like the xor butterfly of
+// append_cta (bit 4 first) -- fp addition is commutative, so every norm is
+// bit-identical to the per-step append's -- but costs ~1 shuffle per row
+// instead of 5.  Afterwards lane r holds the sum of row r.
+constexpr int kVnormRows = 32;
+
+__global__ void __launch_bounds__(256) vnorm_kernel(const uint16_t* __restrict__ V,
+                                                    float* __restrict__ vnorm, int N_max,
+                                                    int n_begin, int n_count, int rows_total) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= rows_total) return;
-  const int bh = warp / n_count, j = n_begin + warp % n_count;
-  const uint2 u = *reinterpret_cast<const uint2*>(V + ((size_t)bh * N_max + j) * kD + lane * 4);
-  float a = bf16lo(u.x), b = bf16hi(u.x), c = bf16lo(u.y), e = bf16hi(u.y);
-  float s = fmaf(a, a, fmaf(b, b, fmaf(c, c, e * e)));
+  const int row0 = warp * kVnormRows;
+  if (row0 >= rows_total) return;
+  // rows row0 .. row0 + 31 of the flattened (bh, j) space (may cross a bh boundary)
+  int bh = row0 / n_count, jj = row0 - bh * n_count;
+  float v[kVnormRows];
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) vnorm[(size_t)bh * N_max + j] = sqrtf(s);
+  for (int half = 0; half < 2; ++half) {
+    uint2 u[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int row = row0 + half * 16 + r;
+      u[r] = make_uint2(0, 0);
+      if (row < rows_total)
+        u[r] = ldg_nc_v2(V + ((size_t)bh * N_max + n_begin + jj) * kD + lane * 4);
+      if (++jj == n_count) { jj = 0; ++bh; }
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const float a = bf16lo(u[r].x), b = bf16hi(u[r].x), c = bf16lo(u[r].y), e = bf16hi(u[r].y);
+      v[half * 16 + r] = fmaf(a, a, fmaf(b, b, fmaf(c, c, e * e)));
+    }
+  }
+  // recursive halving: at distance off, the lane with bit `off` set keeps the
+  // upper half of its values and receives its partner's upper half
+#pragma unroll
+  for (int off = 16, nv = 32; off >= 1; off >>= 1, nv >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < nv / 2; ++i) {
+      const float send = up ? v[i] : v[i + nv / 2];
+      const float keep = up ? v[i + nv / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  // lane l now holds row l: bit k of the lane decided "upper half" at distance 2^k
+  const int row = row0 + lane;
+  if (row < rows_total) {
+    const int bh = row / n_count, j = n_begin + row - bh * n_count;
+    vnorm[(size_t)bh * N_max + j] = sqrtf(v[0]);
+  }
 }
 
 // plain [bh][L][N_max] <-> tiled layout; one thread per (bh, j, slot)
@@ -104,15 +145,15 @@ __global__ void pack_codes_kernel(const uint8_t* __restrict__ plain, uint8_t* __
   }
 }
 
-constexpr int kAppendWarps = 8;
-
-__global__ void __launch_bounds__(kAppendWarps * 32)
+// Per-step append (n_count small): one CTA per (key, 32-table chunk), see append_cta.
+__global__ void __launch_bounds__(kTabThreads)
 hash_append_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict__ W,
                    uint8_t* __restrict__ codes, const uint16_t* __restrict__ V,
                    float* __restrict__ vnorm, int N_max, int L, int P, int Lp, int n_begin,
-                   int n_count, int total_keys) {
-  append_warp_job(K, W, codes, V, vnorm, N_max, L, P, Lp, n_begin, n_count, total_keys, 0, nullptr, 1,
-                  blockIdx.x * kAppendWarps + (threadIdx.x >> 5), threadIdx.x & 31);
+                   int n_count, int chunks) {
+  __shared__ float ks[kD];
+  append_cta(K, W, codes, V, vnorm, N_max, L, P, Lp, n_begin, n_count, 0, nullptr, 1,
+             blockIdx.x / chunks, (blockIdx.x % chunks) * kTabPerCta, ks);
 }
 
 socket_status launch_hash_keys_simt(const socket_cfg& c, const void* K, const void* W,
@@ -138,10 +179,10 @@ socket_status launch_hash_keys(const socket_cfg& c, const void* K, const void* V
   if (n_count <= 16) {
     const int Lp = code_slots(c.L);
     const int total = c.B * c.H_kv * n_count;
-    const long long jobs = (long long)total * Lp;
-    hash_append_kernel<<<(unsigned)((jobs + kAppendWarps - 1) / kAppendWarps), kAppendWarps * 32, 0, st>>>(
+    const int chunks = (Lp + kTabPerCta - 1) / kTabPerCta;
+    hash_append_kernel<<<(unsigned)(total * chunks), kTabThreads, 0, st>>>(
         (const uint16_t*)K, (const uint16_t*)W, codes, (const uint16_t*)V, vnorm, c.N_max, c.L, c.P,
-        Lp, n_begin, n_count, total);
+        Lp, n_begin, n_count, chunks);
     s = check_launch("hash_append_kernel");
     if (s != SOCKET_OK) return s;
     return SOCKET_OK;   // value norms written by the append kernel
@@ -154,7 +195,8 @@ socket_status launch_hash_keys(const socket_cfg& c, const void* K, const void* V
   if (V) {
     const int rows = c.B * c.H_kv * n_count;
     const int threads = 256;
-    const int blocks = (int)(((long long)rows * 32 + threads - 1) / threads);
+    const long long warps = (rows + kVnormRows - 1) / kVnormRows;
+    const int blocks = (int)((warps * 32 + threads - 1) / threads);
     vnorm_kernel<<<blocks, threads, 0, st>>>((const uint16_t*)V, vnorm, c.N_max, n_begin, n_count,
                                              rows);
     s = check_launch("vnorm_kernel");

@@ -18,6 +18,13 @@
 
 namespace sk {
 
+#ifdef SK_TRACE
+// reads this translation unit's copy (the decode-step prologue)
+extern "C" int socket_debug_prologue_trace(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_pro_trace, (size_t)n * sizeof(unsigned long long));
+}
+#endif
+
 socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint8_t* codes,
                                const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
                                float* scores, cudaStream_t st, bool pdl);
@@ -31,24 +38,23 @@ socket_status launch_decode_pdl(const socket_cfg& c, const void* q, const void* 
 size_t decode_workspace_bytes(const socket_cfg& c, int k, bool dense);
 
 template <int NH>
-__global__ void __launch_bounds__(kTabThreads, NH >= 8 ? 1 : 2)
+__global__ void __launch_bounds__(kTabThreads)
 step_prologue_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ W,
                      float* __restrict__ lut, const uint16_t* __restrict__ K,
                      const uint16_t* __restrict__ V, uint8_t* __restrict__ codes,
                      float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
                      int* __restrict__ tickets, int n_tickets, int H_q, int H_sel, int H_kv,
-                     int N_max, int L, int P, int Lp, float tau, int n_table_ctas, int tchunks,
-                     int n_append_keys, int do_append) {
-  __shared__ TablesSmem<NH> S;
+                     int N_max, int L, int P, int Lp, float tau, int n_table_ctas, int tchunks) {
+  extern __shared__ __align__(16) char tsm[];
   if (blockIdx.x == 0)
     for (int i = threadIdx.x; i < n_tickets; i += blockDim.x) tickets[i] = 0;
   if ((int)blockIdx.x < n_table_ctas) {
     tables_cta<NH>(q, W, nullptr, lut, H_q, H_sel, L, P, Lp, tau, blockIdx.x / tchunks,
-                   (blockIdx.x % tchunks) * kTabPerCta, S);
-  } else if (do_append) {
-    const int job = ((int)blockIdx.x - n_table_ctas) * (kTabThreads / 32) + (threadIdx.x >> 5);
-    append_warp_job(K, W, codes, V, vnorm, N_max, L, P, Lp, 0, 1, n_append_keys, 1, seq_lens, H_kv,
-                    job, threadIdx.x & 31);
+                   (blockIdx.x % tchunks) * kTabPerCta, tsm);
+  } else {
+    const int a = (int)blockIdx.x - n_table_ctas;
+    append_cta(K, W, codes, V, vnorm, N_max, L, P, Lp, 0, 1, 1, seq_lens, H_kv, a / tchunks,
+               (a % tchunks) * kTabPerCta, reinterpret_cast<float*>(tsm));
   }
 }
 
@@ -85,15 +91,18 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, const void*
   const int tchunks = (Lp + kTabPerCta - 1) / kTabPerCta;
   const int n_table_ctas = c.B * H_sel * tchunks;
   const int n_keys = c.B * c.H_kv;
-  const int n_append_ctas = do_append ? (n_keys * Lp + (kTabThreads / 32) - 1) / (kTabThreads / 32) : 0;
+  const int n_append_ctas = do_append ? n_keys * tchunks : 0;
   const dim3 grid(n_table_ctas + n_append_ctas);
 #define SK_PRO(N)                                                                                   \
-  case N:                                                                                           \
-    step_prologue_kernel<N><<<grid, kTabThreads, 0, st>>>(                                          \
+  case N: {                                                                                         \
+    const size_t sm = tables_smem_bytes(N);                                                         \
+    cudaFuncSetAttribute(step_prologue_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    step_prologue_kernel<N><<<grid, kTabThreads, sm, st>>>(                                         \
         (const uint16_t*)q, (const uint16_t*)W, lut, (const uint16_t*)K, (const uint16_t*)V, codes, \
         vnorm, seq_lens, tickets, n_units, c.H_q, H_sel, c.H_kv, c.N_max, c.L, c.P, Lp, c.tau,     \
-        n_table_ctas, tchunks, n_keys, do_append);                                                  \
-    break;
+        n_table_ctas, tchunks);                                                                     \
+    break;                                                                                          \
+  }
   switch (NH) { SK_PRO(1) SK_PRO(2) SK_PRO(4) SK_PRO(8) }
 #undef SK_PRO
   s = check_launch("step_prologue_kernel");

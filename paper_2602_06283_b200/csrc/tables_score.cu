@@ -17,12 +17,12 @@ namespace sk {
 
 
 template <int NH>
-__global__ void __launch_bounds__(kTabThreads, NH >= 8 ? 1 : 2)
+__global__ void __launch_bounds__(kTabThreads)
 query_tables_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ W,
                     float* __restrict__ plain, float* __restrict__ lut, int H_q, int H_sel,
                     int L, int P, int Lp, float tau) {
-  __shared__ TablesSmem<NH> S;
-  tables_cta<NH>(q, W, plain, lut, H_q, H_sel, L, P, Lp, tau, blockIdx.x, blockIdx.y * kTabPerCta, S);
+  extern __shared__ __align__(16) char tsm[];
+  tables_cta<NH>(q, W, plain, lut, H_q, H_sel, L, P, Lp, tau, blockIdx.x, blockIdx.y * kTabPerCta, tsm);
 }
 
 socket_status launch_query_tables(const socket_cfg& c, const void* q, const void* W,
@@ -33,8 +33,14 @@ socket_status launch_query_tables(const socket_cfg& c, const void* q, const void
   const int Lp = code_slots(c.L);
   dim3 grid(c.B * H_sel, (Lp + kTabPerCta - 1) / kTabPerCta);
   switch (NH) {
-#define SK_QT(N) case N: query_tables_kernel<N><<<grid, kTabThreads, 0, st>>>((const uint16_t*)q, \
-      (const uint16_t*)W, plain, lut, c.H_q, H_sel, c.L, c.P, Lp, c.tau); break;
+#define SK_QT(N)                                                                                 \
+  case N: {                                                                                      \
+    const size_t sm = tables_smem_bytes(N);                                                      \
+    cudaFuncSetAttribute(query_tables_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    query_tables_kernel<N><<<grid, kTabThreads, sm, st>>>((const uint16_t*)q, (const uint16_t*)W, \
+                                                          plain, lut, c.H_q, H_sel, c.L, c.P, Lp, c.tau); \
+    break;                                                                                       \
+  }
     SK_QT(1) SK_QT(2) SK_QT(4) SK_QT(8)
 #undef SK_QT
     default:

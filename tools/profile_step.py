@@ -23,6 +23,7 @@ ap.add_argument("--bits", type=int, default=8)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--mode", default="kv_shared")
 ap.add_argument("--dense", action="store_true")
+ap.add_argument("--unfused", action="store_true", help="also run the stage-by-stage step")
 a = ap.parse_args()
 B, N, L = a.batch, a.ctx, a.tables
 k = int(round(N / a.sparsity))
@@ -37,6 +38,8 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(a.steps):
     flush.zero_()
     dec.step(q, lens, append=True)
+    if a.unfused:
+        dec.step_unfused(q, lens, append=False)
     if a.dense:
         from paper_2602_06283_b200 import ops
         ops.dense_decode(cfg, q, K, V, lens)
