@@ -72,10 +72,10 @@ hash_keys_simt_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict
 }
 
 // ||v_j||_2.  A warp handles 32 consecutive rows: lane t holds elements
-// 4t .. 4t+3 of every row (same per-lane fma order as append_cta) and the 32
+// 4t .. 4t+3 of every row (same per-lane fma order as append_tile) and the 32
 // lane partials of the 32 rows are summed by a recursive-halving
 // reduce-scatter, which pairs lanes exactly like the xor butterfly of
-// append_cta (bit 4 first) -- fp addition is commutative, so every norm is
+// append_tile (bit 4 first) -- fp addition is commutative, so every norm is
 // bit-identical to the per-step append's -- but costs ~1 shuffle per row
 // instead of 5.  Afterwards lane r holds the sum of row r.
 constexpr int kVnormRows = 32;
@@ -145,17 +145,6 @@ __global__ void pack_codes_kernel(const uint8_t* __restrict__ plain, uint8_t* __
   }
 }
 
-// Per-step append (n_count small): one CTA per (key, 32-table chunk), see append_cta.
-__global__ void __launch_bounds__(kTabThreads)
-hash_append_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict__ W,
-                   uint8_t* __restrict__ codes, const uint16_t* __restrict__ V,
-                   float* __restrict__ vnorm, int N_max, int L, int P, int Lp, int n_begin,
-                   int n_count, int chunks) {
-  __shared__ float ks[kD];
-  append_cta(K, W, codes, V, vnorm, N_max, L, P, Lp, n_begin, n_count, 0, nullptr, 1,
-             blockIdx.x / chunks, (blockIdx.x % chunks) * kTabPerCta, ks);
-}
-
 socket_status launch_hash_keys_simt(const socket_cfg& c, const void* K, const void* W,
                                     uint8_t* codes, int n_begin, int n_count, cudaStream_t st) {
   const int Lp = code_slots(c.L);
@@ -177,15 +166,18 @@ socket_status launch_hash_keys(const socket_cfg& c, const void* K, const void* V
   if (n_count == 0) return SOCKET_OK;
   socket_status s = SOCKET_OK;
   if (n_count <= 16) {
-    const int Lp = code_slots(c.L);
     const int total = c.B * c.H_kv * n_count;
-    const int chunks = (Lp + kTabPerCta - 1) / kTabPerCta;
-    hash_append_kernel<<<(unsigned)(total * chunks), kTabThreads, 0, st>>>(
-        (const uint16_t*)K, (const uint16_t*)W, codes, (const uint16_t*)V, vnorm, c.N_max, c.L, c.P,
-        Lp, n_begin, n_count, chunks);
-    s = check_launch("hash_append_kernel");
-    if (s != SOCKET_OK) return s;
-    return SOCKET_OK;   // value norms written by the append kernel
+    ProArgs a = {};
+    a.W = (const uint16_t*)W;
+    a.K = (const uint16_t*)K;
+    a.V = (const uint16_t*)V;
+    a.codes = codes;
+    a.vnorm = vnorm;
+    a.n_keys = total;
+    a.n_begin = n_begin;
+    a.n_count = n_count;
+    a.append_last = 0;
+    return launch_prologue(c, a, false, st);   // value norms written by the append tiles
   } else {
     bool used = false;
     s = launch_hash_keys_tc(c, K, W, codes, n_begin, n_count, st, &used);

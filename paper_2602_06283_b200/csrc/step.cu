@@ -37,25 +37,33 @@ socket_status launch_decode_pdl(const socket_cfg& c, const void* q, const void* 
                                 int** tickets_out, int* n_units);
 size_t decode_workspace_bytes(const socket_cfg& c, int k, bool dense);
 
-template <int NH>
-__global__ void __launch_bounds__(kTabThreads)
-step_prologue_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ W,
-                     float* __restrict__ lut, const uint16_t* __restrict__ K,
-                     const uint16_t* __restrict__ V, uint8_t* __restrict__ codes,
-                     float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
-                     int* __restrict__ tickets, int n_tickets, int H_q, int H_sel, int H_kv,
-                     int N_max, int L, int P, int Lp, float tau, int n_table_ctas, int tchunks) {
-  extern __shared__ __align__(16) char tsm[];
-  if (blockIdx.x == 0)
-    for (int i = threadIdx.x; i < n_tickets; i += blockDim.x) tickets[i] = 0;
-  if ((int)blockIdx.x < n_table_ctas) {
-    tables_cta<NH>(q, W, nullptr, lut, H_q, H_sel, L, P, Lp, tau, blockIdx.x / tchunks,
-                   (blockIdx.x % tchunks) * kTabPerCta, tsm);
-  } else {
-    const int a = (int)blockIdx.x - n_table_ctas;
-    append_cta(K, W, codes, V, vnorm, N_max, L, P, Lp, 0, 1, 1, seq_lens, H_kv, a / tchunks,
-               (a % tchunks) * kTabPerCta, reinterpret_cast<float*>(tsm));
-  }
+socket_status launch_prologue(const socket_cfg& c, ProArgs a, bool tables, cudaStream_t st) {
+  const int NH = c.group_mode == SOCKET_GROUP_PER_QHEAD ? 1 : c.H_q / c.H_kv;
+  if (tables && NH != 1 && NH != 2 && NH != 4 && NH != 8)
+    return fail(SOCKET_EUNSUPPORTED, "tables: heads per selection row must be 1, 2, 4 or 8");
+  a.B = c.B;
+  a.H_q = c.H_q;
+  a.H_sel = num_sel_rows(c);
+  a.H_kv = c.H_kv;
+  a.N_max = c.N_max;
+  a.L = c.L;
+  a.P = c.P;
+  a.Lp = code_slots(c.L);
+  a.tau = c.tau;
+  a.n_wtiles = (a.Lp + kTT - 1) / kTT;
+  a.n_tab_ctas = tables ? (c.B * c.H_q + kTQ - 1) / kTQ * a.n_wtiles : 0;
+  const int n_app = (a.n_keys + kAK - 1) / kAK * a.n_wtiles;
+  const int grid = a.n_tab_ctas + n_app;
+  if (grid == 0) return SOCKET_OK;
+  const size_t sm = prologue_smem_bytes();
+#define SK_PRO(N)                                                                              \
+  case N:                                                                                      \
+    cudaFuncSetAttribute(prologue_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    prologue_kernel<N><<<grid, kPT, sm, st>>>(a);                                              \
+    break;
+  switch (tables ? NH : 1) { SK_PRO(1) SK_PRO(2) SK_PRO(4) SK_PRO(8) }
+#undef SK_PRO
+  return check_launch("prologue_kernel");
 }
 
 size_t decode_step_workspace_bytes(const socket_cfg& c, int k) {
@@ -87,25 +95,23 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, const void*
   socket_status s = launch_decode_pdl(c, q, K, V, idx, cnt, k, out, lse, dws, dws_bytes, st, false,
                                       &tickets, &n_units);   // query only (tickets_out != null)
   if (s != SOCKET_OK) return s;
-  // ---- prologue ---------------------------------------------------------------
-  const int tchunks = (Lp + kTabPerCta - 1) / kTabPerCta;
-  const int n_table_ctas = c.B * H_sel * tchunks;
-  const int n_keys = c.B * c.H_kv;
-  const int n_append_ctas = do_append ? n_keys * tchunks : 0;
-  const dim3 grid(n_table_ctas + n_append_ctas);
-#define SK_PRO(N)                                                                                   \
-  case N: {                                                                                         \
-    const size_t sm = tables_smem_bytes(N);                                                         \
-    cudaFuncSetAttribute(step_prologue_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    step_prologue_kernel<N><<<grid, kTabThreads, sm, st>>>(                                         \
-        (const uint16_t*)q, (const uint16_t*)W, lut, (const uint16_t*)K, (const uint16_t*)V, codes, \
-        vnorm, seq_lens, tickets, n_units, c.H_q, H_sel, c.H_kv, c.N_max, c.L, c.P, Lp, c.tau,     \
-        n_table_ctas, tchunks);                                                                     \
-    break;                                                                                          \
-  }
-  switch (NH) { SK_PRO(1) SK_PRO(2) SK_PRO(4) SK_PRO(8) }
-#undef SK_PRO
-  s = check_launch("step_prologue_kernel");
+  // ---- prologue: tables || append ---------------------------------------------
+  ProArgs pa = {};
+  pa.q = (const uint16_t*)q;
+  pa.W = (const uint16_t*)W;
+  pa.lut = lut;
+  pa.K = (const uint16_t*)K;
+  pa.V = (const uint16_t*)V;
+  pa.codes = codes;
+  pa.vnorm = vnorm;
+  pa.seq_lens = seq_lens;
+  pa.tickets = tickets;
+  pa.n_tickets = n_units;
+  pa.n_keys = do_append ? c.B * c.H_kv : 0;
+  pa.n_begin = 0;
+  pa.n_count = 1;
+  pa.append_last = 1;
+  s = launch_prologue(c, pa, true, st);
   if (s != SOCKET_OK) return s;
   // ---- score, top-k, decode (PDL chain) ----------------------------------------
   s = launch_score_pdl(c, lut, codes, vnorm, seq_lens, mask, scores, st, true);

@@ -24,8 +24,6 @@ static __device__ unsigned long long g_pro_trace[8192 * 12];   // per translatio
   } while (0)
 #endif
 
-constexpr int kTabThreads = 256;  // one thread per (table, hyperplane row) of a 32-table chunk
-constexpr int kTabPerCta = 32;    // tables per CTA
 constexpr int kMaxHeads = 8;      // heads per selection row
 
 // Byte offset of (row-local key j, slot s) inside one (b, kv-head) code region.
@@ -39,252 +37,352 @@ __device__ __forceinline__ int slot_table(int s, int j, int Lp) {
   return (s & ~M) | ((s + j) & M);
 }
 
-// bf16 bits -> fp64, exactly (bf16 -> fp32 is a shift; fp32 -> fp64 is exact)
+// bf16 bits -> fp64 / fp32, exactly
 __device__ __forceinline__ double bf16_to_f64(uint32_t h) {
   return (double)__uint_as_float(h << 16);
 }
 
-// Shared memory of one tables CTA (dynamic; tables_smem_bytes(NH) bytes):
-//   qd   [kD][NH]  fp64 query heads (phase 1)      } union
-//   half [NH][2][16][kTabPerCta] fp32 (phase 3-4)  }
-//   fx   [NH][8][2][kTabPerCta]  fp64 sigma factors (table fastest: conflict-free reads)
-__host__ __device__ constexpr size_t tables_smem_bytes(int NH) {
-  return (size_t)NH * kTabPerCta * 16 * 8 +
-         ((size_t)NH * kD * 8 > (size_t)NH * 2 * 16 * kTabPerCta * 4
-              ? (size_t)NH * kD * 8
-              : (size_t)NH * 2 * 16 * kTabPerCta * 4);
+// ============================================================================
+// Projection prologue of a decode step: Alg. 2 tables and Alg. 1 on the new
+// keys, both as small tiled GEMMs (one 256-thread CTA per tile):
+//
+//   tables tile  = 16 query vectors x 8 tables (8P W rows), fp64:
+//     x[m][w] = sum_t q_m[t] W_w[t], t ascending (bf16 x bf16 products are
+//     exact in fp64, so this is the double dot product); staged in shared
+//     memory as fp64 (each element converted once per tile), 2 x 2 register
+//     micro-tile per thread.  Epilogue: u = tanh(x)/sqrt(d) (Alg. 2 l.217),
+//     the sigma factors sigma(+-2u/tau) in accurate fp32, half tables
+//     lo(r & 15) = prod_{i<4} f_i, hi(r >> 4) = prod_{i>=4} f_i in fp64
+//     (rounded once), T(r) = sum_h lo_h hi_h in fp32 (h ascending), written as
+//     the score kernel's LUT image and/or the plain [L][R] tables.
+//   append tile  = 32 keys x 8 tables, fp32: x = sum_t W[t] k[t] with fmaf,
+//     t ascending (the SIMT prefill's arithmetic, so both give identical
+//     codes); bit = x >= 0 (R-3), row i -> bit i (R-4), written to slot
+//     s = (l & ~M) | ((l - j) & M) of key j; the first table tile also writes
+//     ||v_j|| (vnorm_kernel's summation order).
+// ============================================================================
+constexpr int kPT = 256;   // threads per tile CTA
+constexpr int kTQ = 16;    // query vectors per tables tile
+constexpr int kTT = 8;     // tables per tile
+constexpr int kAK = 32;    // keys per append tile
+constexpr int kQS = 24;    // row stride (doubles) of the staged q tile [t][m]  (= 16 words mod 32:
+constexpr int kWS = 72;    // row stride (doubles) of the staged W tile [t][w]   conflict-free MMA fragments)
+constexpr int kKS = 36;    // row stride (floats) of the staged key tile   [t][m]
+constexpr int kAWS = 68;   // row stride (floats) of the staged W tile     [t][w]
+constexpr int kFXS = 9;    // padded table stride of the factor array
+
+__host__ __device__ constexpr size_t prologue_smem_bytes() {
+  return (size_t)kD * (kQS + kWS) * 8;    // >= append staging and the epilogue arrays
 }
 
-// One CTA = (b, selection row) x kTabPerCta tables [l0, l0 + 32), NH query heads.
-//  1. thread (tl, i) = (tid >> 3, tid & 7) owns W row (l0 + tl, i) and computes
-//     x_h = sum_t W[t] q_h[t] for every head h in fp64 (bf16 x bf16 products
-//     are exact in fp64; CH interleaved partial sums hide the DFMA latency, so
-//     x is the double dot product up to a few fp64 roundings);
-//  2. u = tanh(x)/sqrt(d) (Alg. 2 l.217) and the two sigma factors
-//     sigma(+-2u/tau) with the accurate fp32 functions (<= 2 ulp each);
-//  3. half tables lo(r & 15) = prod_{i<4} f_i, hi(r >> 4) = prod_{i>=4} f_i in
-//     fp64, rounded once to fp32;
-//  4. T(r) = sum_h lo_h * hi_h (fp32 fma, h ascending); consecutive threads
-//     write consecutive table columns of one LUT row (and/or the plain tables).
+struct ProArgs {
+  const uint16_t* q;
+  const uint16_t* W;
+  float* plain;           // [B][H_sel][L][R] or null
+  float* lut;             // LUT images [B*H_sel][panels][256][64] or null
+  const uint16_t* K;
+  const uint16_t* V;      // null: no norms
+  uint8_t* codes;
+  float* vnorm;
+  const int32_t* seq_lens;
+  int* tickets;           // zeroed by block 0 (decode tickets), or null
+  int n_tickets;
+  int B, H_q, H_sel, H_kv, N_max, L, P, Lp;
+  float tau;
+  int n_wtiles;           // ceil(Lp / kTT)
+  int n_tab_ctas;         // ceil(B*H_q / kTQ) * n_wtiles (0: no tables)
+  int n_keys, n_begin, n_count, append_last;   // append: key kk -> (bh, j)
+};
+
+// 8 bf16 (one uint4) -> 8 fp64 with integer ops (exact for zero and normal
+// numbers: sign | (exponent + 896) << 52 | mantissa << 45); any subnormal / inf /
+// nan in the group goes through the exact fp32 path instead.
+__device__ __forceinline__ void bf16x8_to_f64(const uint4 v, double* out, int stride) {
+  const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+  bool special = false;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t mag = ((e & 1) ? (w4[e >> 1] >> 16) : w4[e >> 1]) & 0x7FFFu;
+    special |= mag != 0u && (mag < 0x80u || mag >= 0x7F80u);
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t h = ((e & 1) ? (w4[e >> 1] >> 16) : w4[e >> 1]) & 0xFFFFu;
+    const uint32_t mag = h & 0x7FFFu;
+    double d;
+    if (special) {
+      d = (double)__uint_as_float(h << 16);
+    } else {
+      const uint32_t hi = ((h & 0x8000u) << 16) | (mag ? (mag << 13) + 0x38000000u : 0u);
+      d = __hiloint2double((int)hi, 0);
+    }
+    out[e * stride] = d;
+  }
+}
+
+// D(8x8) += A(8x4, row) B(4x8, col) in fp64 on the tensor cores (DMMA).
+// Fragments: a = A[lane >> 2][lane & 3], b = B[lane & 3][lane >> 2],
+// d{0,1} = D[lane >> 2][2 (lane & 3) + {0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 template <int NH>
-__device__ __forceinline__ void tables_cta(const uint16_t* __restrict__ q,
-                                           const uint16_t* __restrict__ W, float* __restrict__ plain,
-                                           float* __restrict__ lut, int H_q, int H_sel, int L, int P,
-                                           int Lp, float tau, int row, int l0, char* smem) {
-  double* fx = reinterpret_cast<double*>(smem);                                   // [NH][8][2][32]
-  double* qd = reinterpret_cast<double*>(smem + (size_t)NH * kTabPerCta * 16 * 8);  // [kD][NH]
-  float* half = reinterpret_cast<float*>(qd);                                     // [NH][2][16][32]
-  const int b = row / H_sel, r = row % H_sel;
-  const int h0 = (NH == 1) ? r : r * NH;     // first query head of the row
-  const int R = 1 << P;
-  const int tid = threadIdx.x;
+__device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, char* smem) {
+  double* qs = reinterpret_cast<double*>(smem);    // [kD][kQS]
+  double* ws = qs + kD * kQS;                      // [kD][kWS]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int P = a.P, L = a.L, R = 1 << P;
+  const int nqv = a.B * a.H_q;
+  const int qv0 = qt * kTQ;
+  const int l0 = wt * kTT;
+  const int nw = (L - l0 < kTT ? L - l0 : kTT) * P;   // valid W rows of the tile (<= 0: padding)
   PRO_STAMP(0);
   PRO_STAMP(1);
-  for (int e = tid; e < NH * kD; e += kTabThreads) {
-    const int h = e / kD, t = e % kD;
-    qd[t * NH + h] = bf16_to_f64(q[((size_t)b * H_q + h0 + h) * kD + t]);
+  {   // stage q (16 vectors) and W (64 rows): all loads first, then convert
+    uint4 vq, vw[4];
+    const int m = tid & 15, cq = tid >> 4;
+    vq = make_uint4(0, 0, 0, 0);
+    if (qv0 + m < nqv) vq = __ldg(reinterpret_cast<const uint4*>(a.q + (size_t)(qv0 + m) * kD) + cq);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = tid + k * kPT, w = e & 63, c = e >> 6;
+      vw[k] = make_uint4(0, 0, 0, 0);
+      if (w < nw) vw[k] = __ldg(reinterpret_cast<const uint4*>(a.W + (size_t)(l0 * P + w) * kD) + c);
+    }
+    bf16x8_to_f64(vq, qs + (cq * 8) * kQS + m, kQS);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = tid + k * kPT, w = e & 63, c = e >> 6;
+      bf16x8_to_f64(vw[k], ws + (c * 8) * kWS + w, kWS);
+    }
   }
   __syncthreads();
   PRO_STAMP(2);
-  // 1. projections
-  const int tl = tid >> 3, i = tid & 7;
-  const int l = l0 + tl;
-  const bool active = l < L && i < P;
-  // CH independent partial sums per head (t = CH m + c goes to chain c), so
-  // the fp64 FMA latency is hidden; the chains are added pairwise at the end
-  constexpr int CH = NH >= 8 ? 2 : (NH >= 4 ? 4 : 8);
-  double acc[NH];
+  // X[m][w] = sum_t q_m[t] W_w[t]: warp w8 owns W rows 8 w8 .. 8 w8 + 7 for both
+  // 8-vector halves of the tile (two 8x8 fp64 accumulators), k-steps of 4
+  double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
   {
-    double part[NH][CH];
-#pragma unroll
-    for (int h = 0; h < NH; ++h)
-#pragma unroll
-      for (int c = 0; c < CH; ++c) part[h][c] = 0.0;
-    if (active) {
-      const uint4* wrow = reinterpret_cast<const uint4*>(W + ((size_t)l * P + i) * kD);
-#pragma unroll 1
-      for (int c = 0; c < kD / 32; ++c) {          // 4 batches of 32 elements
-        uint4 wv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) wv[u] = __ldg(wrow + c * 4 + u);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t wd[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int t = c * 32 + u * 8 + e;
-            const double w = bf16_to_f64((e & 1) ? (wd[e >> 1] >> 16) : (wd[e >> 1] & 0xFFFFu));
-            const double* qt = qd + t * NH;
-#pragma unroll
-            for (int h = 0; h < NH; ++h) part[h][e % CH] = fma(w, qt[h], part[h][e % CH]);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < NH; ++h) {
-#pragma unroll
-      for (int w = CH / 2; w >= 1; w >>= 1)
-#pragma unroll
-        for (int c = 0; c < w; ++c) part[h][c] += part[h][c + w];
-      acc[h] = part[h][0];
+    const int kr = lane & 3, col = lane >> 2;
+#pragma unroll 8
+    for (int k0 = 0; k0 < kD; k0 += 4) {
+      const double* qrow = qs + (k0 + kr) * kQS;
+      const double b = ws[(k0 + kr) * kWS + warp * 8 + col];
+      dmma_8x8x4(c00, c01, qrow[col], b);
+      dmma_8x8x4(c10, c11, qrow[8 + col], b);
     }
   }
   PRO_STAMP(3);
-  // 2. sigma factors (c_{r,i} = +1 iff bit i of r is set, reading R-5)
-  if (active) {
+  __syncthreads();   // staging dead: the epilogue arrays reuse it
+  double* fx = reinterpret_cast<double*>(smem);                         // [m][bit][s][kFXS]
+  float* half = reinterpret_cast<float*>(fx + kTQ * 8 * 2 * kFXS);     // [m][hi][ent][kTT]
+  {
+    const double xv[2][2] = {{c00, c01}, {c10, c11}};
     const float inv_sqrt_d = 0.08838834764831845f;   // 1/sqrt(128), correctly rounded
 #pragma unroll
-    for (int h = 0; h < NH; ++h) {
-      const float uu = tanhf((float)acc[h]) * inv_sqrt_d;   // Alg. 2 l.217
-      const float a = 2.0f * uu / tau;                       // logit gap of bit i
-      const float fp = 1.0f / (1.0f + expf(-a));             // c_{r,i} = +1 (bit set)
-      const float fm = 1.0f / (1.0f + expf(a));              // c_{r,i} = -1
-      fx[((h * 8 + i) * 2 + 1) * kTabPerCta + tl] = (double)fp;
-      fx[((h * 8 + i) * 2 + 0) * kTabPerCta + tl] = (double)fm;
-    }
+    for (int hm = 0; hm < 2; ++hm)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int m = hm * 8 + (lane >> 2), w = warp * 8 + 2 * (lane & 3) + i;
+        if (w < nw) {
+          const int tl = w / P, bit = w - tl * P;
+          const float uu = tanhf((float)xv[hm][i]) * inv_sqrt_d;   // Alg. 2 l.217
+          const float av = 2.0f * uu / a.tau;                       // logit gap of bit i
+          const float fp = 1.0f / (1.0f + expf(-av));               // c_{r,i} = +1 (bit set, R-5)
+          const float fm = 1.0f / (1.0f + expf(av));                // c_{r,i} = -1
+          fx[((m * 8 + bit) * 2 + 1) * kFXS + tl] = (double)fp;
+          fx[((m * 8 + bit) * 2 + 0) * kFXS + tl] = (double)fm;
+        }
+      }
   }
-  __syncthreads();   // qd dead from here: `half` reuses it
+  __syncthreads();
   PRO_STAMP(4);
-  // 3. half tables (bits 0..3 and 4..P-1; a missing bit contributes 1): one
-  //    thread per (head, table, half) builds its 16 entries as the product
-  //    ((f0 f1) f2) f3 by doubling (4 + 8 + 16 fp64 multiplies).
-  for (int task = tid; task < NH * 2 * kTabPerCta; task += kTabThreads) {
-    const int t2 = task % kTabPerCta, hi = (task / kTabPerCta) & 1, h = task / (2 * kTabPerCta);
+  {   // half tables: one (vector, table, half) per thread, 16 entries ((f0 f1) f2) f3
+    const int tl = tid & 7, hi = (tid >> 3) & 1, m = tid >> 4;
     double f[4][2];
 #pragma unroll
     for (int bit = 0; bit < 4; ++bit) {
       const int ib = hi * 4 + bit;
-      f[bit][0] = ib < P ? fx[((h * 8 + ib) * 2 + 0) * kTabPerCta + t2] : 1.0;
-      f[bit][1] = ib < P ? fx[((h * 8 + ib) * 2 + 1) * kTabPerCta + t2] : 1.0;
+      f[bit][0] = ib < P ? fx[((m * 8 + ib) * 2 + 0) * kFXS + tl] : 1.0;
+      f[bit][1] = ib < P ? fx[((m * 8 + ib) * 2 + 1) * kFXS + tl] : 1.0;
     }
     double p01[4], p012[8];
 #pragma unroll
     for (int e = 0; e < 4; ++e) p01[e] = f[0][e & 1] * f[1][e >> 1];
 #pragma unroll
     for (int e = 0; e < 8; ++e) p012[e] = p01[e & 3] * f[2][e >> 2];
-    float* hrow = half + (size_t)((h * 2 + hi) * 16) * kTabPerCta + t2;
+    float* hrow = half + ((m * 2 + hi) * 16) * kTT + tl;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) hrow[e * kTabPerCta] = (float)(p012[e & 7] * f[3][e >> 3]);
+    for (int e = 0; e < 16; ++e) hrow[e * kTT] = (float)(p012[e & 7] * f[3][e >> 3]);
   }
   __syncthreads();
   PRO_STAMP(5);
-  // 4. entries T(rr) = sum_h lo_h(rr & 15) hi_h(rr >> 4) (fp32 fma, h ascending):
-  //    thread (t2 = tid & 31, g = tid >> 5) writes rows rr = 16 rh + rl for
-  //    rh in {g, g + 8}; a warp stores 32 consecutive LUT columns per row.
-  const int panels = Lp <= 64 ? 1 : (Lp + 63) / 64;
-  float* lrow = lut ? lut + (size_t)row * panels * (256 * 64) : nullptr;
-  {
-    const int t2 = tid & 31, g = tid >> 5;
-    const int ll = l0 + t2;
-    if (ll < Lp) {
-      const bool lvalid = ll < L;
-      float hv[2][NH];
+  // LUT entries T(rr) = sum_h lo_h(rr & 15) hi_h(rr >> 4): task = (selection row,
+  // LUT row rr, 4-table group), one float4 store of 4 consecutive columns
+  constexpr int kRows = kTQ / NH;
+  const int panels = a.Lp <= 64 ? 1 : (a.Lp + 63) / 64;
+  for (int task = tid; task < kRows * 256 * 2; task += kPT) {
+    const int g4 = task & 1, rr = (task >> 1) & 255, srow = task >> 9;
+    const int row = qv0 / NH + srow;
+    const int lb = l0 + 4 * g4;
+    if (qv0 + srow * NH >= nqv || lb >= a.Lp) continue;
+    float4 T = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (rr < R) {
 #pragma unroll
-      for (int m = 0; m < 2; ++m)
+      for (int h = 0; h < NH; ++h) {
+        const int m = srow * NH + h;
+        const float4 lo = *reinterpret_cast<const float4*>(half + ((m * 2 + 0) * 16 + (rr & 15)) * kTT + 4 * g4);
+        const float4 hv = *reinterpret_cast<const float4*>(half + ((m * 2 + 1) * 16 + (rr >> 4)) * kTT + 4 * g4);
+        T.x = fmaf(lo.x, hv.x, T.x);
+        T.y = fmaf(lo.y, hv.y, T.y);
+        T.z = fmaf(lo.z, hv.z, T.z);
+        T.w = fmaf(lo.w, hv.w, T.w);
+      }
+      // tables >= L are padding: 0
+      if (lb + 0 >= L) T.x = 0.f;
+      if (lb + 1 >= L) T.y = 0.f;
+      if (lb + 2 >= L) T.z = 0.f;
+      if (lb + 3 >= L) T.w = 0.f;
+      if (a.plain) {
+        const float tv[4] = {T.x, T.y, T.z, T.w};
 #pragma unroll
-        for (int h = 0; h < NH; ++h) hv[m][h] = half[((h * 2 + 1) * 16 + g + 8 * m) * kTabPerCta + t2];
-#pragma unroll 4
-      for (int rl = 0; rl < 16; ++rl) {
-        float lo[NH];
+        for (int u = 0; u < 4; ++u)
+          if (lb + u < L) a.plain[((size_t)row * L + lb + u) * R + rr] = tv[u];
+      }
+    }
+    if (a.lut) {
+      float* lrow = a.lut + (size_t)row * panels * (256 * 64);
+      if (a.Lp >= 32) {
+        *reinterpret_cast<float4*>(lrow + (size_t)(lb >> 6) * (256 * 64) + rr * 64 + (lb & 63)) = T;
+      } else {
+        const float tv[4] = {T.x, T.y, T.z, T.w};
 #pragma unroll
-        for (int h = 0; h < NH; ++h) lo[h] = half[((h * 2 + 0) * 16 + rl) * kTabPerCta + t2];
-#pragma unroll
-        for (int m = 0; m < 2; ++m) {
-          const int rr = (g + 8 * m) * 16 + rl;
-          float T = 0.f;
-          if (lvalid && rr < R) {
-#pragma unroll
-            for (int h = 0; h < NH; ++h) T = fmaf(lo[h], hv[m][h], T);
-            if (plain) plain[((size_t)row * L + ll) * R + rr] = T;
-          }
-          if (lrow) {
-            if (Lp >= 32) {
-              lrow[(size_t)(ll >> 6) * (256 * 64) + rr * 64 + (ll & 63)] = T;
-            } else {
-              for (int cc = ll; cc < 32; cc += Lp) lrow[rr * 64 + cc] = T;
-            }
-          }
-        }
+        for (int u = 0; u < 4; ++u)
+          if (lb + u < a.Lp)
+            for (int cc = lb + u; cc < 32; cc += a.Lp) lrow[rr * 64 + cc] = tv[u];
       }
     }
   }
   PRO_STAMP(6);
 }
 
-// Append path (Alg. 1 on a few new keys; the decode step's per-step hash).
-// One CTA = (key, 32-table chunk); thread (tl, i) = (tid >> 3, tid & 7) owns
-// W row (l0 + tl, i): x = sum_t W[t] k[t] in fp32 with fmaf, t ascending --
-// the same arithmetic as the SIMT prefill kernel, so both give identical
-// codes.  The 8 rows of a table sit in 8 consecutive lanes, so one ballot
-// yields 4 code bytes per warp; slot s = (l & ~M) | ((l - j) & M) of key j
-// (inverse of slot_table).  Warp 0 of chunk 0 also writes ||v_j|| with
-// exactly vnorm_kernel's summation order.  With append_last, key j is
-// seq_lens[b] - 1 of each (b, kv head) (skipped for empty sequences).
-// `ks` is 128 floats of shared memory.
-__device__ __forceinline__ void append_cta(
-    const uint16_t* __restrict__ K, const uint16_t* __restrict__ W, uint8_t* __restrict__ codes,
-    const uint16_t* __restrict__ V, float* __restrict__ vnorm, int N_max, int L, int P, int Lp,
-    int n_begin, int n_count, int append_last, const int32_t* __restrict__ seq_lens, int H_kv,
-    int key, int l0, float* ks) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int bh = key / n_count;
-  int j = n_begin + key % n_count;
-  if (append_last) {                      // decode step: the newest key j = seq_lens[b] - 1
-    const int n = seq_lens[bh / H_kv];
-    if (n <= 0) return;                   // uniform over the CTA
-    j = n - 1;
-  }
+__device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, char* smem) {
+  float* ks = reinterpret_cast<float*>(smem);      // [kD][kKS]
+  float* ws = ks + kD * kKS;                       // [kD][kAWS]
+  uint8_t* bits = reinterpret_cast<uint8_t*>(ws + kD * kAWS);   // [kAK][64]
+  int* kj = reinterpret_cast<int*>(bits + kAK * 64);            // [kAK] j (-1: no key)
+  int* kbh = kj + kAK;                                           // [kAK] bh
+  const int tid = threadIdx.x;
+  const int P = a.P, L = a.L;
+  const int l0 = wt * kTT;
+  const int nw = (L - l0 < kTT ? L - l0 : kTT) * P;
   PRO_STAMP(0);
   PRO_STAMP(1);
-  const uint16_t* krow = K + ((size_t)bh * N_max + j) * kD;
-  if (tid < kD / 2) {
-    const uint32_t u = reinterpret_cast<const uint32_t*>(krow)[tid];
-    ks[2 * tid] = bf16lo(u);
-    ks[2 * tid + 1] = bf16hi(u);
+  if (tid < kAK) {
+    const int kk = at * kAK + tid;
+    int j = -1, bh = 0;
+    if (kk < a.n_keys) {
+      bh = kk / a.n_count;
+      j = a.n_begin + kk % a.n_count;
+      if (a.append_last) {               // decode step: the newest key j = seq_lens[b] - 1
+        const int n = a.seq_lens[bh / a.H_kv];
+        j = n > 0 ? n - 1 : -1;
+      }
+    }
+    kj[tid] = j;
+    kbh[tid] = bh;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {   // stage keys: 32 rows x 16 uint4
+    const int e = tid + k * kPT, m = e & 31, c = e >> 5;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (kj[m] >= 0) v = __ldg(reinterpret_cast<const uint4*>(a.K + ((size_t)kbh[m] * a.N_max + kj[m]) * kD) + c);
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e2 = 0; e2 < 8; ++e2)
+      ks[(c * 8 + e2) * kKS + m] = (e2 & 1) ? bf16hi(w4[e2 >> 1]) : bf16lo(w4[e2 >> 1]);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {   // stage W: 64 rows x 16 uint4
+    const int e = tid + k * kPT, w = e & 63, c = e >> 6;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (w < nw) v = __ldg(reinterpret_cast<const uint4*>(a.W + (size_t)(l0 * P + w) * kD) + c);
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e2 = 0; e2 < 8; ++e2)
+      ws[(c * 8 + e2) * kAWS + w] = (e2 & 1) ? bf16hi(w4[e2 >> 1]) : bf16lo(w4[e2 >> 1]);
   }
   __syncthreads();
   PRO_STAMP(2);
-  const int tl = tid >> 3, i = tid & 7;
-  const int l = l0 + tl;
-  bool bit = false;
-  if (l < L && i < P) {
-    const uint4* wrow = reinterpret_cast<const uint4*>(W + ((size_t)l * P + i) * kD);
-    float x = 0.f;
-#pragma unroll 1
-    for (int c = 0; c < kD / 32; ++c) {
-      uint4 wv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) wv[u] = __ldg(wrow + c * 4 + u);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t wd[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float w = (e & 1) ? bf16hi(wd[e >> 1]) : bf16lo(wd[e >> 1]);
-          x = fmaf(w, ks[c * 32 + u * 8 + e], x);
-        }
-      }
-    }
-    bit = x >= 0.f;                        // sign(0) = +1 (R-3)
+  // keys 2kp, 2kp+1 x W rows 4wq .. 4wq+3
+  const int kp = tid & 15, wq = tid >> 4;
+  float x[2][4] = {};
+#pragma unroll 8
+  for (int t = 0; t < kD; ++t) {
+    const float2 kv = *reinterpret_cast<const float2*>(ks + t * kKS + 2 * kp);
+    const float4 wv = *reinterpret_cast<const float4*>(ws + t * kAWS + 4 * wq);
+    x[0][0] = fmaf(wv.x, kv.x, x[0][0]); x[0][1] = fmaf(wv.y, kv.x, x[0][1]);
+    x[0][2] = fmaf(wv.z, kv.x, x[0][2]); x[0][3] = fmaf(wv.w, kv.x, x[0][3]);
+    x[1][0] = fmaf(wv.x, kv.y, x[1][0]); x[1][1] = fmaf(wv.y, kv.y, x[1][1]);
+    x[1][2] = fmaf(wv.z, kv.y, x[1][2]); x[1][3] = fmaf(wv.w, kv.y, x[1][3]);
   }
   PRO_STAMP(3);
-  const unsigned bal = __ballot_sync(0xffffffffu, bit);
-  if (i == 0 && l < Lp) {
-    const uint32_t code = (bal >> (lane & 24)) & 0xFFu;   // row i -> bit i (R-4)
-    const int M = (Lp < 32 ? Lp : 32) - 1;
-    const int s = (l & ~M) | ((l - j) & M);
-    codes[(size_t)bh * N_max * Lp + code_off(j, s, Lp)] = (uint8_t)code;
-  }
-  if (V && l0 == 0 && tid < 32) {
-    const uint2 u = *reinterpret_cast<const uint2*>(V + ((size_t)bh * N_max + j) * kD + lane * 4);
-    float a = bf16lo(u.x), b = bf16hi(u.x), c = bf16lo(u.y), e = bf16hi(u.y);
-    float sq = fmaf(a, a, fmaf(b, b, fmaf(c, c, e * e)));
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    if (lane == 0) vnorm[(size_t)bh * N_max + j] = sqrtf(sq);
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int w = 4 * wq + j;
+      bits[(2 * kp + i) * 64 + w] = (w < nw && x[i][j] >= 0.f) ? 1 : 0;   // sign(0) = +1 (R-3)
+    }
+  __syncthreads();
+  {   // code byte of (key m, table tl): row i -> bit i (R-4)
+    const int m = tid >> 3, tl = tid & 7;
+    const int l = l0 + tl, j = kj[m];
+    if (j >= 0 && l < a.Lp) {
+      uint32_t code = 0;
+      for (int i = 0; i < P; ++i) code |= (uint32_t)bits[m * 64 + tl * P + i] << i;
+      const int Lp = a.Lp;
+      const int M = (Lp < 32 ? Lp : 32) - 1;
+      const int s = (l & ~M) | ((l - j) & M);
+      a.codes[(size_t)kbh[m] * a.N_max * Lp + code_off(j, s, Lp)] = (uint8_t)code;
+    }
+  }
+  if (a.V && wt == 0) {   // ||v_j||: warp w handles keys 4w .. 4w+3
+    const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int m = warp * 4 + r, j = kj[m];
+      if (j < 0) continue;
+      const uint2 u = *reinterpret_cast<const uint2*>(a.V + ((size_t)kbh[m] * a.N_max + j) * kD + lane * 4);
+      float va = bf16lo(u.x), vb = bf16hi(u.x), vc = bf16lo(u.y), vd = bf16hi(u.y);
+      float sq = fmaf(va, va, fmaf(vb, vb, fmaf(vc, vc, vd * vd)));
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      if (lane == 0) a.vnorm[(size_t)kbh[m] * a.N_max + j] = sqrtf(sq);
+    }
   }
   PRO_STAMP(6);
+}
+
+// Host: fill the shape fields of a ProArgs from cfg (tables: B*H_q query
+// vectors when lut/plain set; append: n_keys keys) and launch prologue_kernel
+// (defined in step.cu).
+socket_status launch_prologue(const socket_cfg& c, ProArgs a, bool tables, cudaStream_t st);
+
+template <int NH>
+__global__ void __launch_bounds__(kPT, 2) prologue_kernel(ProArgs a) {
+  extern __shared__ __align__(16) char psm[];
+  if (blockIdx.x == 0 && a.tickets)
+    for (int i = threadIdx.x; i < a.n_tickets; i += blockDim.x) a.tickets[i] = 0;
+  if ((int)blockIdx.x < a.n_tab_ctas) {
+    tables_tile<NH>(a, blockIdx.x / a.n_wtiles, blockIdx.x % a.n_wtiles, psm);
+  } else {
+    const int t = (int)blockIdx.x - a.n_tab_ctas;
+    append_tile(a, t / a.n_wtiles, t % a.n_wtiles, psm);
+  }
 }
 
 }  // namespace sk

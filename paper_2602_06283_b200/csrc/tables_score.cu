@@ -16,37 +16,14 @@
 namespace sk {
 
 
-template <int NH>
-__global__ void __launch_bounds__(kTabThreads)
-query_tables_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ W,
-                    float* __restrict__ plain, float* __restrict__ lut, int H_q, int H_sel,
-                    int L, int P, int Lp, float tau) {
-  extern __shared__ __align__(16) char tsm[];
-  tables_cta<NH>(q, W, plain, lut, H_q, H_sel, L, P, Lp, tau, blockIdx.x, blockIdx.y * kTabPerCta, tsm);
-}
-
 socket_status launch_query_tables(const socket_cfg& c, const void* q, const void* W,
                                   float* plain, float* lut, cudaStream_t st) {
-  const int H_sel = num_sel_rows(c);
-  const int NH = c.group_mode == SOCKET_GROUP_PER_QHEAD ? 1 : c.H_q / c.H_kv;
-  if (NH > kMaxHeads) return fail(SOCKET_EUNSUPPORTED, "more than 8 query heads per KV head");
-  const int Lp = code_slots(c.L);
-  dim3 grid(c.B * H_sel, (Lp + kTabPerCta - 1) / kTabPerCta);
-  switch (NH) {
-#define SK_QT(N)                                                                                 \
-  case N: {                                                                                      \
-    const size_t sm = tables_smem_bytes(N);                                                      \
-    cudaFuncSetAttribute(query_tables_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    query_tables_kernel<N><<<grid, kTabThreads, sm, st>>>((const uint16_t*)q, (const uint16_t*)W, \
-                                                          plain, lut, c.H_q, H_sel, c.L, c.P, Lp, c.tau); \
-    break;                                                                                       \
-  }
-    SK_QT(1) SK_QT(2) SK_QT(4) SK_QT(8)
-#undef SK_QT
-    default:
-      return fail(SOCKET_EUNSUPPORTED, "query tables: heads per selection row must be 1, 2, 4 or 8");
-  }
-  return check_launch("query_tables_kernel");
+  ProArgs a = {};
+  a.q = (const uint16_t*)q;
+  a.W = (const uint16_t*)W;
+  a.plain = plain;
+  a.lut = lut;
+  return launch_prologue(c, a, true, st);
 }
 
 // ----------------------------------------------------------------------------

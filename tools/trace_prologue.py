@@ -22,8 +22,8 @@ import torch  # noqa: E402
 
 from trace_topk import build_trace  # noqa: E402
 
-TAB = ["entry", "q load", "projection", "sigma", "half tables", "LUT write"]
-APP = ["entry", "k load", "projection", "(none)", "(none)", "code+norm"]
+TAB = ["entry", "staging", "projection", "sigma", "half tables", "LUT write"]
+APP = ["entry", "staging", "projection", "(none)", "(none)", "code+norm"]
 
 
 def main():
@@ -50,7 +50,7 @@ def main():
     buf = (ctypes.c_ulonglong * (8192 * 12))()
     assert L.socket_debug_prologue_trace(buf, 8192 * 12) == 0
     t = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 12).astype(np.int64)
-    n_tab = B * 8 * 2
+    n_tab = (B * 32 + 15) // 16 * 8
     for name, rows, ph in (("tables", t[:n_tab], TAB), ("append", t[n_tab:], APP)):
         rows = rows[rows[:, 0] != 0]
         if not len(rows):
