@@ -187,7 +187,8 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
   uint32_t nvalid = 0, nforced = 0, kmin = 0xFFFFFFFFu, kmax = 0u;
   if (a.mode == 0) {
     const float* src = a.scores + (size_t)row * a.N_max + base;   // 128-B aligned
-    constexpr int U = 4;                                          // float4 loads in flight
+    const bool forced_free = (a.sink <= 0 || base >= a.sink) && (a.window <= 0 || base + len <= n - a.window);
+    constexpr int U = 8;                                          // float4 loads in flight
     for (int i0 = tid * 4; i0 < len128; i0 += kTopkThreads * 4 * U) {
       float4 v[U];
 #pragma unroll
@@ -208,13 +209,24 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
         const float vs[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
         uint4 kk;
         uint32_t* kp = &kk.x;
+        if (forced_free) {           // no sink / window key in this slice: lean path
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t key = make_key(vs[e], base + i4 + e, n, a.sink, a.window, 0);
-          kp[e] = key;
-          nvalid += key != 0u;
-          nforced += key == 0xFFFFFFFFu;
-          if (key != 0u && key != 0xFFFFFFFFu) { kmin = min(kmin, key); kmax = max(kmax, key); }
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t key = vs[e] == -INFINITY ? 0u : f2key(vs[e]);
+            kp[e] = key;
+            nvalid += key != 0u;
+            kmin = min(kmin, key - 1u);      // invalid (0) wraps to the maximum
+            kmax = max(kmax, key);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t key = make_key(vs[e], base + i4 + e, n, a.sink, a.window, 0);
+            kp[e] = key;
+            nvalid += key != 0u;
+            nforced += key == 0xFFFFFFFFu;
+            if (key != 0u && key != 0xFFFFFFFFu) { kmin = min(kmin, key - 1u); kmax = max(kmax, key); }
+          }
         }
         *reinterpret_cast<uint4*>(keys + i4) = kk;
       }
@@ -225,9 +237,11 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
       if (i < len) key = make_key(load_elem(a, row, base + i), base + i, n, 0, 0, 1);
       keys[i] = key;
       nvalid += key != 0u;
-      if (key != 0u) { kmin = min(kmin, key); kmax = max(kmax, key); }
+      if (key != 0u) { kmin = min(kmin, key - 1u); kmax = max(kmax, key); }
     }
   }
+  kmin += 1u;   // back from key - 1 (no regular key: 0xFFFFFFFF + 1 = 0, fixed below)
+  if (kmin == 0u) kmin = 0xFFFFFFFFu;
   if (tid < 8) S.stat[tid] = (tid == 2) ? 0xFFFFFFFFu : 0u;   // kmin starts at +max
   if (tid < kTopkWarps) { S.wgt[tid] = 0; S.weq[tid] = 0; }
   if (tid < 2) S.acc[tid] = 0;
@@ -349,28 +363,28 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
     if (C <= (uint32_t)kCandCap) {
       // 3. candidate pass: keys of bin bstar -> S.cand (+ slice index); per warp the
       //    number of keys strictly above the bin (all of them are > T, forced included)
+      // a lane scans 4 consecutive keys per 128-key round (same rounds per warp
+      // as the emit pass, so the per-warp counts line up)
       uint32_t ab = 0;
       for (int r = r0; r < r1; ++r) {
+        const int i0 = r * 128 + lane * 4;
+        const uint4 kv = *reinterpret_cast<const uint4*>(keys + i0);
+        const uint32_t k4[4] = {kv.x, kv.y, kv.z, kv.w};
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          const int i = r * 128 + x * 32 + lane;
-          const uint32_t key = keys[i];
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t key = k4[e];
           const bool reg = key != 0u && key != 0xFFFFFFFFu;
           const uint32_t bin = (key - gmin) >> sh;
-          ab += __popc(__ballot_sync(kFull, key == 0xFFFFFFFFu || (reg && bin > bstar)));
-          const unsigned cm = __ballot_sync(kFull, reg && bin == bstar);
-          if (cm) {
-            uint32_t slot0 = 0;
-            if (lane == 0) slot0 = atomicAdd(&S.stat[4], (uint32_t)__popc(cm));
-            slot0 = __shfl_sync(kFull, slot0, 0);
-            if ((cm >> lane) & 1u) {
-              const uint32_t sl = slot0 + __popc(cm & lt);
-              S.cand[sl] = key;
-              S.cidx[sl] = (uint32_t)i;
-            }
+          ab += (key == 0xFFFFFFFFu || (reg && bin > bstar)) ? 1u : 0u;
+          if (reg && bin == bstar) {              // rare: ~C / len of the keys
+            const uint32_t sl = atomicAdd(&S.stat[4], 1u);
+            S.cand[sl] = key;
+            S.cidx[sl] = (uint32_t)(i0 + e);
           }
         }
       }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) ab += __shfl_xor_sync(kFull, ab, o);
       if (lane == 0) { S.wab[warp] = ab; atomicAdd(&S.stat[5], ab); }
       TK_TRACE(7);
       cluster.sync();
@@ -555,20 +569,46 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
     float* srow = a.sel_scores ? a.sel_scores + (size_t)row * a.k : nullptr;
     const int q = (int)quota;
     for (int r = r0; r < r1; ++r) {
+      // lane owns keys 4 lane .. 4 lane + 3 of the round (index order within the
+      // round = lane-major); ties at T (rare) take the per-32 ballot path below
+      const int i0 = r * 128 + lane * 4;
+      const uint4 kv = *reinterpret_cast<const uint4*>(keys + i0);
+      const uint32_t k4[4] = {kv.x, kv.y, kv.z, kv.w};
+      const bool anyeq = (k4[0] == T) | (k4[1] == T) | (k4[2] == T) | (k4[3] == T);
+      if (!__any_sync(kFull, anyeq && T != 0u)) {
+        unsigned gm[4];
+        int pre = 0, tot = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          gm[e] = __ballot_sync(kFull, k4[e] > T);
+          pre += __popc(gm[e] & lt);
+          tot += __popc(gm[e]);
+        }
+        int pos = gbase + pre + min(ebase, q);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (k4[e] > T) {
+            orow[pos] = base + i0 + e;
+            if (srow) srow[pos] = load_elem(a, row, base + i0 + e);
+            ++pos;
+          }
+        }
+        gbase += tot;
+        continue;
+      }
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
         const int i = r * 128 + x * 32 + lane;
         const uint32_t key = keys[i];
         const bool isgt = key > T, iseq = key != 0u && key == T;
-        const unsigned gm = __ballot_sync(kFull, isgt), em = __ballot_sync(kFull, iseq);
-        const int gr = gbase + __popc(gm & lt), er = ebase + __popc(em & lt);
-        const int j = base + i;
+        const unsigned gmx = __ballot_sync(kFull, isgt), em = __ballot_sync(kFull, iseq);
+        const int gr = gbase + __popc(gmx & lt), er = ebase + __popc(em & lt);
         if (isgt || (iseq && er < q)) {
-          const int pos = gr + min(er, q);
-          orow[pos] = j;
-          if (srow) srow[pos] = load_elem(a, row, j);
+          const int p = gr + min(er, q);
+          orow[p] = base + i;
+          if (srow) srow[p] = load_elem(a, row, base + i);
         }
-        gbase += __popc(gm);
+        gbase += __popc(gmx);
         ebase += __popc(em);
       }
     }
