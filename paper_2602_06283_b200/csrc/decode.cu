@@ -58,24 +58,25 @@ socket_status launch_decode_mma(const socket_cfg& c, const void* q, const void* 
                                 float* lse, float* part_out, cudaStream_t st, bool pdl);
 
 // Split geometry: rows per split is a multiple of `gran` (rows one CTA consumes
-// per round), at most `max_rps` (index staging), and the grid aims at
-// `target` CTAs in flight.
+// per round) and at most `max_rps` (index staging); the splits of a unit are
+// balanced (equal up to one granule), and the grid aims at `target` CTAs.
 static void pick_splits(int units, int max_rows, int gran, int max_rps, int target,
                         int& n_splits, int& rows_per_split) {
   int ns = (target + units - 1) / units;
   const int max_ns = (max_rows + 2 * gran - 1) / (2 * gran);   // >= 2 rounds per CTA
   if (ns > max_ns) ns = max_ns;
+  const int min_ns = (max_rows + max_rps - 1) / max_rps;        // index staging limit
+  if (ns < min_ns) ns = min_ns;
   if (ns < 1) ns = 1;
   int rps = (max_rows + ns - 1) / ns;
   rps = (rps + gran - 1) / gran * gran;
   if (rps < gran) rps = gran;
-  if (rps > max_rps) rps = max_rps;
   n_splits = (max_rows + rps - 1) / rps;
   if (n_splits < 1) n_splits = 1;
   rows_per_split = rps;
 }
 
-constexpr int kMmaGran = 64, kMmaMaxRps = 1024;
+constexpr int kMmaGran = 64, kMmaMaxRps = 2048;
 
 static void decode_geometry(const socket_cfg& c, int k, bool dense, int& units, int& NH,
                             int& n_splits, int& rps) {
@@ -84,7 +85,9 @@ static void decode_geometry(const socket_cfg& c, int k, bool dense, int& units, 
   units = c.B * H_sel;
   NH = per_q ? 1 : c.H_q / c.H_kv;
   const char* tune = getenv("SOCKET_DECODE_TARGET");   // tuning experiments only
-  const int target = tune ? atoi(tune) : kNumSMs;   // one CTA per SM (tools/tune_step.py)
+  // ~0.86 of one wave at 2 CTAs per SM: a single wave of balanced splits was the
+  // fastest geometry in tools/tune_step.py sweeps (B 4-16, 5x-10x, 32K)
+  const int target = tune ? atoi(tune) : 256;
   pick_splits(units, dense ? c.N_max : k, kMmaGran, kMmaMaxRps, target, n_splits, rps);
 }
 

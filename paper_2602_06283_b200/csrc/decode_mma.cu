@@ -22,7 +22,7 @@ constexpr int kMmaStages = 3;
 constexpr int kTileRows = 16;
 constexpr int kTileBytes = kTileRows * 2 * 256;                 // K and V rows of a tile
 constexpr int kMmaRing = kMmaWarps * kMmaStages * kTileBytes;   // 96 KB
-constexpr int kMmaMaxRows = 1024;                                // rows per split (idx staging)
+constexpr int kMmaMaxRows = 2048;                                // rows per split (idx staging)
 constexpr float kLog2eM = 1.4426950408889634f;
 
 struct MmaArgs {
