@@ -31,7 +31,7 @@ socket_status launch_query_tables(const socket_cfg& c, const void* q, const void
 // ----------------------------------------------------------------------------
 constexpr int kScoreThreads = 512;            // 16 warps, one CTA per SM (persistent)
 constexpr int kScoreWarps = kScoreThreads / 32;
-constexpr int kScoreStages = 3;               // per-warp cp.async ring depth (tiles)
+constexpr int kScoreStages = 4;               // per-warp cp.async ring depth (tiles)
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -187,16 +187,23 @@ score_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
         }
       }
       const float vn = *reinterpret_cast<const float*>(st + TS::CODE_BYTES + lane * 4);
-      float acc0 = 0.f, acc1 = 0.f;
+      // even slots accumulate in .x, odd slots in .y (one packed FADD2 per pair)
+      uint64_t acc = 0ull;
 #pragma unroll
-      for (int s2 = 0; s2 < LP; ++s2) {
-        const int sl = s2 & 31;
-        const uint32_t sel = (uint32_t)(4 + (sl & 1)) | ((uint32_t)(s2 & 3) << 4) | 0x7600u;
-        const uint32_t addr = __byte_perm(w[s2 >> 2], pk[sl >> 1], sel);   // code*256 + 4 c
-        const float v = *reinterpret_cast<const float*>(smem + (size_t)(s2 >> 6) * (256 * 64 * 4) +
-                                                        ((s2 & 32) ? 128 : 0) + addr);
-        if (s2 & 1) acc1 += v; else acc0 += v;
+      for (int s2 = 0; s2 < LP; s2 += 2) {
+        float v[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int ss = s2 + u, sl = ss & 31;
+          const uint32_t sel = (uint32_t)(4 + (sl & 1)) | ((uint32_t)(ss & 3) << 4) | 0x7600u;
+          const uint32_t addr = __byte_perm(w[ss >> 2], pk[sl >> 1], sel);   // code*256 + 4 c
+          v[u] = *reinterpret_cast<const float*>(smem + (size_t)(ss >> 6) * (256 * 64 * 4) +
+                                                 ((ss & 32) ? 128 : 0) + addr);
+        }
+        const uint64_t pv = (uint64_t)__float_as_uint(v[0]) | ((uint64_t)__float_as_uint(v[1]) << 32);
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(pv));
       }
+      const float acc0 = __uint_as_float((uint32_t)acc), acc1 = __uint_as_float((uint32_t)(acc >> 32));
       const int ti = first + i * kScoreWarps;
       const int j = ti * 32 + lane;
       const bool ok = j < n && (!mrow || mrow[j]);
