@@ -67,6 +67,14 @@ typedef enum {
  *             H_sel = H_q selection rows (the paper's literal single-query form). */
 typedef enum { SOCKET_GROUP_KV_SHARED = 0, SOCKET_GROUP_PER_QHEAD = 1 } socket_group_mode;
 
+/* Which bucket weights the tables hold.
+ *  SOFT: Alg. 2 soft bucket probabilities p_tau(r | q) -- SOCKET, Eq. 4;
+ *  HARD: the indicator [r == b_q^(l)] of the query's own bucket (b_q by the key
+ *        rule of Alg. 1, sign(0) = +1) -- traditional LSH, Eq. 3, so that the
+ *        score is the collision count sum_l [b_j^(l) == b_q^(l)] (times ||v_j||,
+ *        or a caller-supplied all-ones vnorm for the plain Eq. 3 count). */
+typedef enum { SOCKET_SCORING_SOFT = 0, SOCKET_SCORING_HARD = 1 } socket_scoring;
+
 typedef struct {
   int32_t B;          /* batch                                                     */
   int32_t H_q;        /* query heads                                               */
@@ -78,6 +86,7 @@ typedef struct {
   float tau;          /* temperature > 0 (Alg. 2)                                  */
   float sm_scale;     /* softmax scale on q.k (reading R-2; usually 1/sqrt(d))     */
   int32_t group_mode; /* socket_group_mode                                         */
+  int32_t scoring;    /* socket_scoring; 0 = soft scores (SOCKET, Eq. 4)           */
 } socket_cfg;
 
 /* ------------------------------------------------------------------------ *

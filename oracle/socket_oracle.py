@@ -141,6 +141,26 @@ def selection_tables(q: np.ndarray, W: np.ndarray, tau: float, H_kv: int,
     return p.reshape(B, H_kv, G, *p.shape[2:]).sum(axis=2)  # [B, H_kv, L, R]
 
 
+def selection_tables_hard(q: np.ndarray, W: np.ndarray, H_kv: int,
+                          group_mode: int) -> np.ndarray:
+    """Hard-LSH tables (Eq. 3): T[b][row][l][r] = [r == b_q^(l)],
+    summed over the group's query heads in KV_SHARED mode (reading R-14), so
+    that sum_l T[row, l, b_j^(l)] is the collision count of Eq. 3 (summed over
+    the group).  b_q^(l) is the query's own bucket by the key rule of Alg. 1
+    (hash_query).  q [B, H_q, d]."""
+    B, H_q, d = q.shape
+    L, P, _ = W.shape
+    G = H_q // H_kv
+    T = np.zeros((B, H_q, L, 1 << P), dtype=np.float64)
+    for b in range(B):
+        for h in range(H_q):
+            bq = hash_query(q[b, h], W)                     # [L]
+            T[b, h, np.arange(L), bq] = 1.0
+    if group_mode == GROUP_PER_QHEAD:
+        return T
+    return T.reshape(B, H_kv, G, L, 1 << P).sum(axis=2)
+
+
 # ---------------------------------------------------------------------------
 # Eq. 4 / Alg. 3 / Alg. 4  soft collision scores               P:183-188, P:238-244, P:1485-1506
 # ---------------------------------------------------------------------------

@@ -31,7 +31,7 @@ class SocketCfg(ctypes.Structure):
         ("B", ctypes.c_int32), ("H_q", ctypes.c_int32), ("H_kv", ctypes.c_int32),
         ("d", ctypes.c_int32), ("N_max", ctypes.c_int32), ("L", ctypes.c_int32),
         ("P", ctypes.c_int32), ("tau", ctypes.c_float), ("sm_scale", ctypes.c_float),
-        ("group_mode", ctypes.c_int32),
+        ("group_mode", ctypes.c_int32), ("scoring", ctypes.c_int32),
     ]
 
 

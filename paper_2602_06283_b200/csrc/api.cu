@@ -38,6 +38,8 @@ static socket_status validate(const socket_cfg* c) {
   if (!std::isfinite(c->sm_scale)) return fail(SOCKET_EINVAL, "sm_scale must be finite");
   if (c->group_mode != SOCKET_GROUP_KV_SHARED && c->group_mode != SOCKET_GROUP_PER_QHEAD)
     return fail(SOCKET_EINVAL, "unknown group_mode");
+  if (c->scoring != SOCKET_SCORING_SOFT && c->scoring != SOCKET_SCORING_HARD)
+    return fail(SOCKET_EINVAL, "unknown scoring");
   return SOCKET_OK;
 }
 

@@ -50,6 +50,7 @@ socket_status launch_prologue(const socket_cfg& c, ProArgs a, bool tables, cudaS
   a.P = c.P;
   a.Lp = code_slots(c.L);
   a.tau = c.tau;
+  a.hard = c.scoring == SOCKET_SCORING_HARD;
   a.n_wtiles = (a.Lp + kTT - 1) / kTT;
   a.n_tab_ctas = tables ? (c.B * c.H_q + kTQ - 1) / kTQ * a.n_wtiles : 0;
   const int n_app = (a.n_keys + kAK - 1) / kAK * a.n_wtiles;

@@ -89,6 +89,7 @@ struct ProArgs {
   int n_tickets;
   int B, H_q, H_sel, H_kv, N_max, L, P, Lp;
   float tau;
+  int hard;               // SOCKET_SCORING_HARD: indicator factors [bit == (x >= 0)]
   int n_wtiles;           // ceil(Lp / kTT)
   int n_tab_ctas;         // ceil(B*H_q / kTQ) * n_wtiles (0: no tables)
   int n_keys, n_begin, n_count, append_last;   // append: key kk -> (bh, j)
@@ -188,12 +189,18 @@ __device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, ch
         const int m = hm * 8 + (lane >> 2), w = warp * 8 + 2 * (lane & 3) + i;
         if (w < nw) {
           const int tl = w / P, bit = w - tl * P;
-          const float uu = tanhf((float)xv[hm][i]) * inv_sqrt_d;   // Alg. 2 l.217
-          const float av = 2.0f * uu / a.tau;                       // logit gap of bit i
-          const float fp = 1.0f / (1.0f + expf(-av));               // c_{r,i} = +1 (bit set, R-5)
-          const float fm = 1.0f / (1.0f + expf(av));                // c_{r,i} = -1
-          fx[((m * 8 + bit) * 2 + 1) * kFXS + tl] = (double)fp;
-          fx[((m * 8 + bit) * 2 + 0) * kFXS + tl] = (double)fm;
+          double fp, fm;
+          if (a.hard) {            // Eq. 3: the product over bits is the indicator of b_q
+            fp = xv[hm][i] >= 0.0 ? 1.0 : 0.0;                      // sign(0) = +1 (R-3)
+            fm = 1.0 - fp;
+          } else {
+            const float uu = tanhf((float)xv[hm][i]) * inv_sqrt_d;  // Alg. 2 l.217
+            const float av = 2.0f * uu / a.tau;                      // logit gap of bit i
+            fp = (double)(1.0f / (1.0f + expf(-av)));                // c_{r,i} = +1 (bit set, R-5)
+            fm = (double)(1.0f / (1.0f + expf(av)));                 // c_{r,i} = -1
+          }
+          fx[((m * 8 + bit) * 2 + 1) * kFXS + tl] = fp;
+          fx[((m * 8 + bit) * 2 + 0) * kFXS + tl] = fm;
         }
       }
   }

@@ -33,11 +33,12 @@ class Config:
     sm_scale: float | None = None   # default 1/sqrt(d) (reading R-2)
     group_mode: int = KV_SHARED
     d: int = 128
+    scoring: int = 0       # SOCKET_SCORING_SOFT (Eq. 4); 1 = hard LSH collision counts (Eq. 3)
 
     def c(self) -> SocketCfg:
         s = self.sm_scale if self.sm_scale is not None else 1.0 / math.sqrt(self.d)
         return SocketCfg(self.B, self.H_q, self.H_kv, self.d, self.N_max, self.L, self.P,
-                         float(self.tau), float(s), int(self.group_mode))
+                         float(self.tau), float(s), int(self.group_mode), int(self.scoring))
 
     @property
     def H_sel(self) -> int:

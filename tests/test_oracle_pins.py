@@ -392,3 +392,52 @@ def test_golden_table6_defaults_are_the_build_defaults():
     c = Config(B=1, H_q=1, H_kv=1, N_max=32)
     row = g["rows"][0]
     assert (c.P, c.L) == (row["P"], row["L"]) and row["tau"][0] <= c.tau <= row["tau"][1]
+
+
+# ---------------------------------------------------------------------------
+# Hard-LSH tables (Eq. 3) and the Fig. 2 ranking metrics
+# ---------------------------------------------------------------------------
+def test_hard_tables_give_eq3_collision_counts():
+    """sum_l T_hard[l, b_j] is Eq. 3's collision count; tables are one-hot per
+    head (KV_SHARED: sums to G); tau -> 0 soft tables tend to them."""
+    r = rng(21)
+    B, H_q, H_kv, d, L, P, N = 2, 4, 2, 64, 12, 6, 300
+    W = r.standard_normal((L, P, d))
+    q = r.standard_normal((B, H_q, d))
+    K = r.standard_normal((N, d))
+    codes, _ = O.hash_keys(K, W)
+    Tp = O.selection_tables_hard(q, W, H_kv, O.GROUP_PER_QHEAD)
+    assert np.array_equal(Tp.sum(axis=-1), np.ones((B, H_q, L)))
+    for b in range(B):
+        for h in range(H_q):
+            assert np.array_equal(O.soft_scores(Tp[b, h], codes), O.hard_scores(O.hash_query(q[b, h], W), codes))
+    Tg = O.selection_tables_hard(q, W, H_kv, O.GROUP_KV_SHARED)
+    assert np.array_equal(Tg.sum(axis=-1), np.full((B, H_kv, L), H_q // H_kv))
+    assert np.array_equal(Tg[:, 1], Tp[:, 2] + Tp[:, 3])
+    # a key equal to the query collides in every table
+    K[7] = q[0, 0]
+    codes, _ = O.hash_keys(K, W)
+    assert O.soft_scores(Tp[0, 0], codes)[7] == L
+    # tau -> 0: soft tables -> one-hot at the hard bucket (on tables with a clear margin)
+    x = W @ q[0, 0]
+    keep = np.min(np.abs(np.tanh(x)), axis=1) > 0.05
+    Ts = O.selection_tables(q[:1, :1], W[keep], 1e-4, 1, O.GROUP_PER_QHEAD)[0, 0]
+    Th = O.selection_tables_hard(q[:1, :1], W[keep], 1, O.GROUP_PER_QHEAD)[0, 0]
+    assert np.max(np.abs(Ts - Th)) < 1e-6
+
+
+def test_ranking_metrics_closed_forms():
+    """P:825-847 definitions on hand-checkable cases."""
+    from oracle import ranking as RK
+    assert RK.precision([1, 2, 3, 4], [3, 4, 5, 6]) == 0.5
+    assert RK.jaccard([1, 2, 3, 4], [3, 4, 5, 6]) == 2 / 6
+    assert RK.jaccard([1, 2], [1, 2]) == 1.0 and RK.jaccard([1], [2]) == 0.0
+    # DCG of relevances (1, 0, 1): (2^1-1)/log2(2) + 0 + (2^1-1)/log2(4) = 1.5
+    assert abs(RK.dcg([1, 0, 1]) - 1.5) < 1e-15
+    rel = np.array([0.0, 1.0, 0.5, 0.25])
+    assert abs(RK.ndcg([1, 2, 3], rel) - 1.0) < 1e-15            # ideal order
+    worse = RK.dcg(rel[[3, 2, 1]]) / RK.dcg([1.0, 0.5, 0.25])
+    assert abs(RK.ndcg([3, 2, 1], rel) - worse) < 1e-15 and worse < 1.0
+    assert np.array_equal(RK.ranked_selection([0.1, 0.9, 0.5, 0.9], [0, 1, 2, 3]), [1, 3, 2, 0])
+    g = RK.graded_relevance([2.0, -1.0, 0.5])
+    assert np.allclose(g, [1.0, 0.0, 0.5])
