@@ -236,6 +236,21 @@ socket_status socket_sparse_decode(const socket_cfg* cfg, const void* q, const v
 socket_status socket_lse_combine(const socket_cfg* cfg, const float* partials, int32_t G,
                                  void* out, float* lse, void* stream);
 
+/* Value-aware sampling decode, Eq. 6: for every query row (b, h)
+ * (requires PER_QHEAD, so that `scores` holds that head's own s_j), with the
+ * masked value scores s_j = ||v_j|| w_hat_j of socket_score (-inf = invalid):
+ *   p_j = s_j / sum_i s_i                    (= a~_j ||v_j|| / sum_i a~_i ||v_i||)
+ *   J_m = min{ j < seq_lens[b] : sum_{i<=j} s_i > u_m sum_i s_i }   (inverse CDF)
+ *   out = (1/M) sum_m (a~_J / p_J) v_J = (sum s / sum w_hat) / M * sum_m v_J / ||v_J||
+ * where a~_j = w_hat_j / sum_i w_hat_i and w_hat_j = s_j / ||v_j|| (0 if ||v_j|| = 0,
+ * DESIGN.md R-24).  uniforms [B][H_q][M] fp32 in [0, 1) are the caller's draws;
+ * samples [B][H_q][M] (nullable) receives J_m in the order of the uniforms
+ * (-1 for a row without mass, whose output is 0).  out [B][H_q][d] bf16.
+ * 1 <= M <= 8192.  No workspace. */
+socket_status socket_sample_decode(const socket_cfg* cfg, const float* scores, const float* vnorm,
+                                   const void* V, const int32_t* seq_lens, const float* uniforms,
+                                   int32_t M, int32_t* samples, void* out, void* stream);
+
 /* Eq. 1 (with sm_scale): dense flash-decode over every key
  * j < seq_lens[b] of the kv head of each query head; the k = n baseline. */
 socket_status socket_dense_decode(const socket_cfg* cfg, const void* q, const void* K,

@@ -252,6 +252,40 @@ def dense_attention(q, K, V, n: int, sm_scale: float, mask=None):
     return sparse_attention(q, K, V, np.nonzero(valid)[0], sm_scale)
 
 
+def sampling_estimator(s: np.ndarray, vnorm: np.ndarray, V: np.ndarray, n: int,
+                       u: np.ndarray):
+    """Eq. 6 sampling-based estimator, literally.
+
+    s [N] masked value scores s_j = ||v_j|| w_hat_j (Alg. 4; -inf invalid),
+    vnorm [N], V [N, d], n = sequence length, u [M] uniforms in [0, 1).
+      w_hat_j = s_j / ||v_j||  (0 where ||v_j|| = 0 or j invalid; reading R-24)
+      a~_j = w_hat_j / sum_i w_hat_i
+      p_j  = a~_j ||v_j|| / sum_i a~_i ||v_i||
+      J_m  = min{ j : sum_{i<=j} p_i > u_m }                  (inverse CDF, J_m ~ p)
+      T    = (1/M) sum_m (a~_{J_m} / p_{J_m}) v_{J_m}          (Eq. 6, P:340-346)
+    Returns (J [M] int64, T [d]); a row without mass gives J = -1 and T = 0.
+    The inverse CDF is evaluated on the unnormalised cumulative sums
+    (sum_{i<=j} s_i > u_m sum_i s_i), the same event in exact arithmetic.
+    """
+    N = s.shape[0]
+    valid = (np.arange(N) < n) & np.isfinite(s) & (s > 0)
+    sv = np.where(valid, s, 0.0)
+    vn = np.asarray(vnorm, dtype=np.float64)
+    w_hat = np.where(valid & (vn > 0), sv / np.where(vn > 0, vn, 1.0), 0.0)
+    M = u.shape[0]
+    if sv.sum() <= 0 or w_hat.sum() <= 0:
+        return np.full(M, -1, dtype=np.int64), np.zeros(V.shape[1])
+    a = w_hat / w_hat.sum()
+    p = a * vn / np.sum(a * vn)
+    C = np.cumsum(sv)                                   # sum_{i<=j} s_i, j ascending
+    J = np.searchsorted(C, u * C[-1], side="right")     # first j with C_j > u C_n
+    J = np.minimum(J, N - 1)
+    T = np.zeros(V.shape[1])
+    for m in range(M):
+        T += (a[J[m]] / p[J[m]]) * V[J[m]]
+    return J.astype(np.int64), T / M
+
+
 def lse_combine(parts):
     """Merge split softmax states: parts = [(y_s, lse_s)] over disjoint subsets.
 

@@ -270,6 +270,19 @@ socket_status socket_dense_decode(const socket_cfg* cfg, const void* q, const vo
                        ws_bytes, S(stream));
 }
 
+socket_status socket_sample_decode(const socket_cfg* cfg, const float* scores, const float* vnorm,
+                                   const void* V, const int32_t* seq_lens, const float* uniforms,
+                                   int32_t M, int32_t* samples, void* out, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(scores);
+  SK_NONNULL(vnorm);
+  SK_NONNULL(V);
+  SK_NONNULL(seq_lens);
+  SK_NONNULL(uniforms);
+  SK_NONNULL(out);
+  return launch_sample_decode(*cfg, scores, vnorm, V, seq_lens, uniforms, M, samples, out, S(stream));
+}
+
 socket_status socket_lse_combine(const socket_cfg* cfg, const float* partials, int32_t G,
                                  void* out, float* lse, void* stream) {
   SK_CHECK(validate(cfg));

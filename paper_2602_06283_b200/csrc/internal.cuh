@@ -67,6 +67,9 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, const void*
                                  const int32_t* seq_lens, const uint8_t* mask, int do_append, int k,
                                  int sink, int window, float* scores, int32_t* idx, int32_t* cnt,
                                  void* out, float* lse, void* ws, size_t ws_bytes, cudaStream_t st);
+socket_status launch_sample_decode(const socket_cfg& c, const float* scores, const float* vnorm,
+                                   const void* V, const int32_t* seq_lens, const float* uniforms,
+                                   int M, int32_t* samples, void* out, cudaStream_t st);
 socket_status launch_lse_combine(const socket_cfg& c, const float* partials, int G,
                                  void* out, float* lse, cudaStream_t st);
 

@@ -224,6 +224,25 @@ def sparse_decode(cfg: Config, q, K, V, idx, cnt, k: int, out=None, lse=None, pa
     return out, lse
 
 
+def sample_decode(cfg: Config, scores, vnorm, V, seq_lens, uniforms, samples=None, out=None,
+                  want_samples: bool = True):
+    """Eq. 6 value-aware sampling estimator (PER_QHEAD rows): M = uniforms.shape[-1]
+    draws by inverse CDF of p_j = s_j / sum s; out bf16 [B][H_q][d], samples
+    int32 [B][H_q][M] (J_m in the order of the uniforms)."""
+    _need(scores, torch.float32, (cfg.B, cfg.H_q, cfg.N_max), "scores")
+    M = int(uniforms.shape[-1])
+    _need(uniforms, torch.float32, (cfg.B, cfg.H_q, M), "uniforms")
+    dev = scores.device
+    if out is None:
+        out = torch.empty((cfg.B, cfg.H_q, cfg.d), dtype=torch.bfloat16, device=dev)
+    if want_samples and samples is None:
+        samples = torch.empty((cfg.B, cfg.H_q, M), dtype=torch.int32, device=dev)
+    c = cfg.c()
+    check(lib().socket_sample_decode(ctypes.byref(c), _p(scores), _p(vnorm), _p(V), _p(seq_lens),
+                                     _p(uniforms), M, _p(samples), _p(out), _stream(scores)))
+    return out, samples
+
+
 def dense_decode(cfg: Config, q, K, V, seq_lens, out=None, lse=None, ws=None):
     """Eq. 1 dense flash-decode over j < seq_lens[b] (the k = n baseline)."""
     dev = q.device

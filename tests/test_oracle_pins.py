@@ -441,3 +441,42 @@ def test_ranking_metrics_closed_forms():
     assert np.array_equal(RK.ranked_selection([0.1, 0.9, 0.5, 0.9], [0, 1, 2, 3]), [1, 3, 2, 0])
     g = RK.graded_relevance([2.0, -1.0, 0.5])
     assert np.allclose(g, [1.0, 0.0, 0.5])
+
+
+# ---------------------------------------------------------------------------
+# Eq. 6 sampling estimator
+# ---------------------------------------------------------------------------
+def test_sampling_estimator_inverse_cdf_by_hand():
+    """Tiny case worked by hand: s = (1, 2, 1) -> C = (1, 3, 4); u = (0.1, 0.3,
+    0.8) -> targets (0.4, 1.2, 3.2) -> J = (0, 1, 2); a key past n or with -inf
+    score is never drawn."""
+    s = np.array([1.0, 2.0, 1.0, 5.0, -np.inf])
+    vn = np.array([1.0, 2.0, 4.0, 1.0, 1.0])
+    V = np.eye(5, 3)
+    J, T = O.sampling_estimator(s, vn, V, 3, np.array([0.1, 0.3, 0.8]))
+    assert list(J) == [0, 1, 2]
+    # a~ = w_hat / sum w_hat with w_hat = (1, 1, 0.25); p = s / sum s = (1, 2, 1) / 4
+    a = np.array([1.0, 1.0, 0.25]) / 2.25
+    p = np.array([0.25, 0.5, 0.25])
+    ref = (a[0] / p[0] * V[0] + a[1] / p[1] * V[1] + a[2] / p[2] * V[2]) / 3
+    assert np.allclose(T, ref, atol=1e-15)
+    Jn, Tn = O.sampling_estimator(np.full(4, -np.inf), np.ones(4), np.ones((4, 2)), 4, np.array([0.5]))
+    assert list(Jn) == [-1] and np.all(Tn == 0)
+
+
+def test_sampling_estimator_is_unbiased():
+    """E[T] = sum_j a~_j v_j = y_{tau,L}(q): stratified draws
+    u_m = (m + 1/2)/M converge at O(1/M); iid draws average to it within 5 sigma."""
+    r = rng(31)
+    N, d = 40, 8
+    s = r.uniform(0.1, 2.0, N)
+    vn = r.uniform(0.5, 3.0, N)
+    V = r.standard_normal((N, d))
+    w_hat = s / vn
+    y = (w_hat / w_hat.sum()) @ V
+    M = 1 << 16
+    _, T = O.sampling_estimator(s, vn, V, N, (np.arange(M) + 0.5) / M)
+    assert np.max(np.abs(T - y)) < 2e-3
+    runs = np.stack([O.sampling_estimator(s, vn, V, N, r.uniform(size=256))[1] for _ in range(400)])
+    se = runs.std(axis=0, ddof=1) / np.sqrt(runs.shape[0])
+    assert np.all(np.abs(runs.mean(axis=0) - y) < 5 * se + 1e-12)
