@@ -33,7 +33,6 @@ static socket_status validate(const socket_cfg* c) {
   if (c->L < 1) return fail(SOCKET_EINVAL, "L must be >= 1");
   if (c->L > 128) return fail(SOCKET_EUNSUPPORTED, "L > 128 not implemented");
   if (c->P < 1 || c->P > 16) return fail(SOCKET_EINVAL, "P must be in [1, 16]");
-  if (c->P > 8) return fail(SOCKET_EUNSUPPORTED, "P > 8 (u16 codes) not implemented");
   if (!(c->tau > 0.f) || !std::isfinite(c->tau)) return fail(SOCKET_EINVAL, "tau must be > 0");
   if (!std::isfinite(c->sm_scale)) return fail(SOCKET_EINVAL, "sm_scale must be finite");
   if (c->group_mode != SOCKET_GROUP_KV_SHARED && c->group_mode != SOCKET_GROUP_PER_QHEAD)
@@ -69,14 +68,14 @@ int32_t socket_code_slots(int32_t L) { return code_slots(L); }
 
 size_t socket_codes_bytes(const socket_cfg* c) {
   if (!c) return 0;
-  return (size_t)c->B * c->H_kv * c->N_max * code_slots(c->L);
+  return (size_t)c->B * c->H_kv * c->N_max * code_slots(c->L) * code_elem_bytes(c->P);
 }
 
 size_t socket_workspace_bytes(const socket_cfg* c, int32_t op, int32_t k) {
   if (validate(c) != SOCKET_OK) return 0;
   switch (op) {
     case SOCKET_OP_SCORE:
-      return align16((size_t)c->B * num_sel_rows(*c) * lut_bytes_per_row(c->L));
+      return align16((size_t)c->B * num_sel_rows(*c) * lut_row_bytes(*c));
     case SOCKET_OP_SPARSE_DECODE:
       return align16(decode_workspace_bytes(*c, k > 0 ? k : 1, false));
     case SOCKET_OP_DENSE_DECODE:

@@ -17,12 +17,13 @@ namespace sk {
 // ----------------------------------------------------------------------------
 constexpr int kHashThreads = 256;
 
+template <typename CT>   // code element: uint8_t (P <= 8) or uint16_t (P > 8)
 __global__ void __launch_bounds__(kHashThreads)
 hash_keys_simt_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict__ W,
-                      uint8_t* __restrict__ codes, int H_kv, int N_max, int L, int P, int Lp,
+                      CT* __restrict__ codes, int H_kv, int N_max, int L, int P, int Lp,
                       int n_begin, int n_end) {
   __shared__ float kt[kD][33];            // K tile transposed: kt[t][key]
-  __shared__ uint8_t cs[32][128 + 4];     // codes of the tile: cs[key][table]  (L <= 128)
+  __shared__ CT cs[32][128 + 4];          // codes of the tile: cs[key][table]  (L <= 128)
   const int bh = blockIdx.y;
   const int tile = (n_begin >> 5) + blockIdx.x;
   const int j0 = tile * 32;
@@ -42,32 +43,31 @@ hash_keys_simt_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict
       for (int t = 0; t < kD; ++t) x = fmaf(__uint_as_float((uint32_t)w[t] << 16), kt[t][lane], x);
       code |= (x >= 0.f ? 1u : 0u) << i;   // sign(0) = +1 (R-3); row i -> bit i (R-4)
     }
-    cs[lane][l] = (uint8_t)code;
+    cs[lane][l] = (CT)code;
   }
   __syncthreads();
-  // write: thread = (key, chunk); CB contiguous bytes per (key, chunk)
+  // write: thread = (key, chunk); CB contiguous code elements per (key, chunk)
   const int CB = Lp < 16 ? Lp : 16;
   const int nch = Lp / CB;
-  uint8_t* cb = codes + (size_t)bh * N_max * Lp;
+  CT* cb = codes + (size_t)bh * N_max * Lp;
   for (int i = threadIdx.x; i < 32 * nch; i += kHashThreads) {
     const int key = i & 31, ch = i >> 5;
     const int j = j0 + key;
     if (j < n_begin || j >= n_end) continue;
-    uint8_t buf[16];
+    __align__(16) CT buf[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
       if (e < CB) {
         const int s = ch * CB + e;
         const int t = slot_table(s, j, Lp);
-        buf[e] = t < L ? cs[key][t] : 0;
+        buf[e] = t < L ? cs[key][t] : (CT)0;
       }
     }
-    uint8_t* dst = cb + code_off(j, ch * CB, Lp);
-    if (CB == 16) {
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(buf);
-    } else {
-      *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(buf);
-    }
+    CT* dst = cb + code_off(j, ch * CB, Lp);
+    const int nbytes = CB * (int)sizeof(CT);   // 8, 16 or 32
+    for (int o = 0; o < nbytes; o += 8)
+      *reinterpret_cast<uint2*>(reinterpret_cast<char*>(dst) + o) =
+          *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(buf) + o);
   }
 }
 
@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(256) vnorm_kernel(const uint16_t* __restrict__
 }
 
 // plain [bh][L][N_max] <-> tiled layout; one thread per (bh, j, slot)
-__global__ void pack_codes_kernel(const uint8_t* __restrict__ plain, uint8_t* __restrict__ codes,
+template <typename CT>
+__global__ void pack_codes_kernel(const CT* __restrict__ plain, CT* __restrict__ codes,
                                   int N_max, int L, int Lp, long long total, bool unpack) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
@@ -137,11 +138,11 @@ __global__ void pack_codes_kernel(const uint8_t* __restrict__ plain, uint8_t* __
   const int j = (int)(r % N_max);
   const long long bh = r / N_max;
   const int t = slot_table(s, j, Lp);
-  uint8_t* cdst = codes + bh * (long long)N_max * Lp + code_off(j, s, Lp);
+  CT* cdst = codes + bh * (long long)N_max * Lp + code_off(j, s, Lp);
   if (!unpack) {
-    *cdst = t < L ? plain[(bh * L + t) * N_max + j] : 0;
+    *cdst = t < L ? plain[(bh * L + t) * N_max + j] : (CT)0;
   } else if (t < L) {
-    const_cast<uint8_t*>(plain)[(bh * L + t) * N_max + j] = *cdst;
+    const_cast<CT*>(plain)[(bh * L + t) * N_max + j] = *cdst;
   }
 }
 
@@ -150,9 +151,14 @@ socket_status launch_hash_keys_simt(const socket_cfg& c, const void* K, const vo
   const int Lp = code_slots(c.L);
   const int t0 = n_begin >> 5, t1 = (n_begin + n_count - 1) >> 5;
   dim3 grid(t1 - t0 + 1, c.B * c.H_kv);
-  hash_keys_simt_kernel<<<grid, kHashThreads, 0, st>>>(
-      (const uint16_t*)K, (const uint16_t*)W, codes, c.H_kv, c.N_max, c.L, c.P, Lp, n_begin,
-      n_begin + n_count);
+  if (c.P > 8)
+    hash_keys_simt_kernel<uint16_t><<<grid, kHashThreads, 0, st>>>(
+        (const uint16_t*)K, (const uint16_t*)W, reinterpret_cast<uint16_t*>(codes), c.H_kv, c.N_max,
+        c.L, c.P, Lp, n_begin, n_begin + n_count);
+  else
+    hash_keys_simt_kernel<uint8_t><<<grid, kHashThreads, 0, st>>>(
+        (const uint16_t*)K, (const uint16_t*)W, codes, c.H_kv, c.N_max, c.L, c.P, Lp, n_begin,
+        n_begin + n_count);
   return check_launch("hash_keys_simt_kernel");
 }
 
@@ -202,8 +208,14 @@ socket_status launch_pack_codes(const socket_cfg& c, const uint8_t* plain, uint8
   const long long total = (long long)c.B * c.H_kv * c.N_max * Lp;
   if (total == 0) return SOCKET_OK;
   const int threads = 256;
-  pack_codes_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0, st>>>(
-      plain, codes, c.N_max, c.L, Lp, total, unpack);
+  const unsigned blocks = (unsigned)((total + threads - 1) / threads);
+  if (c.P > 8)
+    pack_codes_kernel<uint16_t><<<blocks, threads, 0, st>>>(
+        reinterpret_cast<const uint16_t*>(plain), reinterpret_cast<uint16_t*>(codes), c.N_max, c.L,
+        Lp, total, unpack);
+  else
+    pack_codes_kernel<uint8_t><<<blocks, threads, 0, st>>>(plain, codes, c.N_max, c.L, Lp, total,
+                                                            unpack);
   return check_launch("pack_codes_kernel");
 }
 

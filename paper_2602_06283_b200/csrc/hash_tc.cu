@@ -490,6 +490,7 @@ socket_status launch_hash_keys_tc(const socket_cfg& c, const void* K, const void
                                   uint8_t* codes, int n_begin, int n_count, cudaStream_t st,
                                   bool* used) {
   *used = false;
+  if (c.P > 8) return SOCKET_OK;   // wide codes: CUDA-core path
   const int Lp = code_slots(c.L);
   const int NC = Lp * 8;
   if (NC > 512 || n_count < kTcM) return SOCKET_OK;    // CUDA-core path

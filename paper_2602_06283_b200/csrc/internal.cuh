@@ -36,6 +36,22 @@ inline int num_sel_rows(const socket_cfg& c) {
 inline size_t lut_bytes_per_row(int L) {
   return (size_t)lut_panels(code_slots(L)) * kLutRows * kLutPanelCols * sizeof(float);
 }
+// P > 8 ("wide" codes, NEXT-2): one uint16 per (key, table); the score kernel's
+// LUT holds per query head the two factor half-tables A(lo), B(hi) of the
+// exact product form p(r) = A(r mod 2^Pl) B(r >> Pl), Pl = P / 2.
+inline int code_elem_bytes(int P) { return P > 8 ? 2 : 1; }
+inline int wide_lo_bits(int P) { return P / 2; }
+inline int wide_entries(int P) { return 1 << (P - P / 2); }   // rows per half-table image
+inline int heads_per_row(const socket_cfg& c) {
+  return c.group_mode == SOCKET_GROUP_PER_QHEAD ? 1 : c.H_q / c.H_kv;
+}
+// LUT image bytes of one selection row for cfg (P <= 8: the [256][64] table
+// panels; P > 8: [NH][2][2^(P - P/2)][64] half-table panels)
+inline size_t lut_row_bytes(const socket_cfg& c) {
+  if (c.P <= 8) return lut_bytes_per_row(c.L);
+  return (size_t)heads_per_row(c) * 2 * wide_entries(c.P) * kLutPanelCols * sizeof(float);
+}
+constexpr size_t kWideLutMax = 160 * 1024;   // shared-memory budget of the wide score kernel
 
 // ----------------------------------------------------------------------------
 // launchers (defined in the kernel .cu files)

@@ -51,7 +51,8 @@ socket_status launch_prologue(const socket_cfg& c, ProArgs a, bool tables, cudaS
   a.Lp = code_slots(c.L);
   a.tau = c.tau;
   a.hard = c.scoring == SOCKET_SCORING_HARD;
-  a.n_wtiles = (a.Lp + kTT - 1) / kTT;
+  a.tpt = c.P > 8 ? 64 / c.P : kTT;
+  a.n_wtiles = (a.Lp + a.tpt - 1) / a.tpt;
   a.n_tab_ctas = tables ? (c.B * c.H_q + kTQ - 1) / kTQ * a.n_wtiles : 0;
   const int n_app = (a.n_keys + kAK - 1) / kAK * a.n_wtiles;
   const int grid = a.n_tab_ctas + n_app;
@@ -68,7 +69,7 @@ socket_status launch_prologue(const socket_cfg& c, ProArgs a, bool tables, cudaS
 }
 
 size_t decode_step_workspace_bytes(const socket_cfg& c, int k) {
-  const size_t lut = ((size_t)c.B * num_sel_rows(c) * lut_bytes_per_row(c.L) + 255) & ~(size_t)255;
+  const size_t lut = ((size_t)c.B * num_sel_rows(c) * lut_row_bytes(c) + 255) & ~(size_t)255;
   return lut + decode_workspace_bytes(c, k, false);
 }
 
@@ -80,11 +81,12 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, const void*
                                  cudaStream_t st) {
   const int Lp = code_slots(c.L);
   if (Lp > 64) return fail(SOCKET_EUNSUPPORTED, "decode step: L > 64 not supported");
+  if (c.P > 8) return fail(SOCKET_EUNSUPPORTED, "decode step: P > 8 runs stage by stage");
   const int H_sel = num_sel_rows(c);
   const int NH = c.group_mode == SOCKET_GROUP_PER_QHEAD ? 1 : c.H_q / c.H_kv;
   if (NH != 1 && NH != 2 && NH != 4 && NH != 8)
     return fail(SOCKET_EUNSUPPORTED, "decode step: heads per selection row must be 1, 2, 4 or 8");
-  const size_t lut_bytes = ((size_t)c.B * H_sel * lut_bytes_per_row(c.L) + 255) & ~(size_t)255;
+  const size_t lut_bytes = ((size_t)c.B * H_sel * lut_row_bytes(c) + 255) & ~(size_t)255;
   if (ws_bytes < decode_step_workspace_bytes(c, k))
     return fail(SOCKET_EWORKSPACE, "decode step: workspace too small");
   float* lut = static_cast<float*>(ws);

@@ -90,7 +90,8 @@ struct ProArgs {
   int B, H_q, H_sel, H_kv, N_max, L, P, Lp;
   float tau;
   int hard;               // SOCKET_SCORING_HARD: indicator factors [bit == (x >= 0)]
-  int n_wtiles;           // ceil(Lp / kTT)
+  int tpt;                // tables per tile: 8 for P <= 8, 64 / P for wide codes
+  int n_wtiles;           // ceil(Lp / tpt)
   int n_tab_ctas;         // ceil(B*H_q / kTQ) * n_wtiles (0: no tables)
   int n_keys, n_begin, n_count, append_last;   // append: key kk -> (bh, j)
 };
@@ -130,6 +131,56 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// Wide codes (P > 8): the tables are not materialized (2^P entries per table);
+// the score kernel's LUT image holds, per query head h and table l, the two
+// factor half-tables of the exact product form (factorization):
+//   A_h(e) = prod_{i < Pl} f_i(bit i of e),   B_h(e) = prod_{Pl <= i < P} f_i(bit i - Pl of e)
+// (fp64 products in bit order, rounded once), so p_h(r) = A_h(r mod 2^Pl) B_h(r >> Pl)
+// and T(r) = sum_h A_h B_h.  Image of a selection row: [h][half][E = 2^(P-Pl)][64 cols].
+// The plain tables (socket_query_tables) are expanded from the same halves.
+template <int NH>
+__device__ __forceinline__ void wide_tables_epilogue(const ProArgs& a, const double* fx, int qv0,
+                                                     int l0, int nqv) {
+  const int P = a.P, L = a.L, Pl = P / 2, E = 1 << (P - Pl), R = 1 << P;
+  const int tid = threadIdx.x;
+  const size_t row_floats = (size_t)NH * 2 * E * 64;
+  auto half_entry = [&](int m, int tl, int hi, int e) -> float {
+    const int b0 = hi ? Pl : 0, nb = hi ? P - Pl : Pl;
+    double p = 1.0;
+    for (int i = 0; i < nb; ++i) p *= fx[((m * 16 + b0 + i) * 2 + ((e >> i) & 1)) * kFXS + tl];
+    return (float)p;
+  };
+  if (a.lut) {   // one (vector, table, half) per task
+    for (int task = tid; task < kTQ * a.tpt * 2; task += kPT) {
+      const int hi = task & 1, tl = (task >> 1) % a.tpt, m = (task >> 1) / a.tpt;
+      const int l = l0 + tl;
+      if (qv0 + m >= nqv || l >= a.Lp) continue;
+      const int nent = 1 << (hi ? P - Pl : Pl);
+      float* img = a.lut + (size_t)((qv0 + m) / NH) * row_floats + (size_t)(((m % NH) * 2 + hi) * E) * 64;
+      for (int e = 0; e < nent; ++e) {
+        const float v = l < L ? half_entry(m, tl, hi, e) : 0.f;
+        if (a.Lp >= 32) img[e * 64 + l] = v;
+        else for (int cc = l; cc < 32; cc += a.Lp) img[e * 64 + cc] = v;
+      }
+    }
+  }
+  if (a.plain) {   // T(r) = sum_h A_h(r mod 2^Pl) B_h(r >> Pl), fp32 fma, h ascending
+    constexpr int kRows = kTQ / NH;
+    const long long n_ent = (long long)kRows * a.tpt * R;
+    for (long long e = tid; e < n_ent; e += kPT) {
+      const int r = (int)(e % R), tl = (int)((e / R) % a.tpt), srow = (int)(e / R / a.tpt);
+      const int l = l0 + tl;
+      if (qv0 + srow * NH >= nqv || l >= L) continue;
+      float T = 0.f;
+      for (int h = 0; h < NH; ++h) {
+        const int m = srow * NH + h;
+        T = fmaf(half_entry(m, tl, 0, r & ((1 << Pl) - 1)), half_entry(m, tl, 1, r >> Pl), T);
+      }
+      a.plain[((size_t)(qv0 / NH + srow) * L + l) * R + r] = T;
+    }
+  }
+}
+
 template <int NH>
 __device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, char* smem) {
   double* qs = reinterpret_cast<double*>(smem);    // [kD][kQS]
@@ -138,8 +189,8 @@ __device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, ch
   const int P = a.P, L = a.L, R = 1 << P;
   const int nqv = a.B * a.H_q;
   const int qv0 = qt * kTQ;
-  const int l0 = wt * kTT;
-  const int nw = (L - l0 < kTT ? L - l0 : kTT) * P;   // valid W rows of the tile (<= 0: padding)
+  const int l0 = wt * a.tpt;
+  const int nw = (L - l0 < a.tpt ? L - l0 : a.tpt) * P;   // valid W rows of the tile (<= 0: padding)
   PRO_STAMP(0);
   PRO_STAMP(1);
   {   // stage q (16 vectors) and W (64 rows): all loads first, then convert
@@ -177,8 +228,8 @@ __device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, ch
   }
   PRO_STAMP(3);
   __syncthreads();   // staging dead: the epilogue arrays reuse it
-  double* fx = reinterpret_cast<double*>(smem);                         // [m][bit][s][kFXS]
-  float* half = reinterpret_cast<float*>(fx + kTQ * 8 * 2 * kFXS);     // [m][hi][ent][kTT]
+  double* fx = reinterpret_cast<double*>(smem);                         // [m][bit < 16][s][kFXS]
+  float* half = reinterpret_cast<float*>(fx + kTQ * 16 * 2 * kFXS);    // [m][hi][ent][kTT]
   {
     const double xv[2][2] = {{c00, c01}, {c10, c11}};
     const float inv_sqrt_d = 0.08838834764831845f;   // 1/sqrt(128), correctly rounded
@@ -199,12 +250,17 @@ __device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, ch
             fp = (double)(1.0f / (1.0f + expf(-av)));                // c_{r,i} = +1 (bit set, R-5)
             fm = (double)(1.0f / (1.0f + expf(av)));                 // c_{r,i} = -1
           }
-          fx[((m * 8 + bit) * 2 + 1) * kFXS + tl] = fp;
-          fx[((m * 8 + bit) * 2 + 0) * kFXS + tl] = fm;
+          fx[((m * 16 + bit) * 2 + 1) * kFXS + tl] = fp;
+          fx[((m * 16 + bit) * 2 + 0) * kFXS + tl] = fm;
         }
       }
   }
   __syncthreads();
+  if (P > 8) {   // wide codes (NEXT-2): per-head factor half-tables, no group sum
+    wide_tables_epilogue<NH>(a, fx, qv0, l0, nqv);
+    PRO_STAMP(6);
+    return;
+  }
   PRO_STAMP(4);
   {   // half tables: one (vector, table, half) per thread, 16 entries ((f0 f1) f2) f3
     const int tl = tid & 7, hi = (tid >> 3) & 1, m = tid >> 4;
@@ -212,8 +268,8 @@ __device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, ch
 #pragma unroll
     for (int bit = 0; bit < 4; ++bit) {
       const int ib = hi * 4 + bit;
-      f[bit][0] = ib < P ? fx[((m * 8 + ib) * 2 + 0) * kFXS + tl] : 1.0;
-      f[bit][1] = ib < P ? fx[((m * 8 + ib) * 2 + 1) * kFXS + tl] : 1.0;
+      f[bit][0] = ib < P ? fx[((m * 16 + ib) * 2 + 0) * kFXS + tl] : 1.0;
+      f[bit][1] = ib < P ? fx[((m * 16 + ib) * 2 + 1) * kFXS + tl] : 1.0;
     }
     double p01[4], p012[8];
 #pragma unroll
@@ -283,8 +339,8 @@ __device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, ch
   int* kbh = kj + kAK;                                           // [kAK] bh
   const int tid = threadIdx.x;
   const int P = a.P, L = a.L;
-  const int l0 = wt * kTT;
-  const int nw = (L - l0 < kTT ? L - l0 : kTT) * P;
+  const int l0 = wt * a.tpt;
+  const int nw = (L - l0 < a.tpt ? L - l0 : a.tpt) * P;
   PRO_STAMP(0);
   PRO_STAMP(1);
   if (tid < kAK) {
@@ -348,13 +404,15 @@ __device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, ch
   {   // code byte of (key m, table tl): row i -> bit i (R-4)
     const int m = tid >> 3, tl = tid & 7;
     const int l = l0 + tl, j = kj[m];
-    if (j >= 0 && l < a.Lp) {
+    if (j >= 0 && tl < a.tpt && l < a.Lp) {
       uint32_t code = 0;
       for (int i = 0; i < P; ++i) code |= (uint32_t)bits[m * 64 + tl * P + i] << i;
       const int Lp = a.Lp;
       const int M = (Lp < 32 ? Lp : 32) - 1;
       const int s = (l & ~M) | ((l - j) & M);
-      a.codes[(size_t)kbh[m] * a.N_max * Lp + code_off(j, s, Lp)] = (uint8_t)code;
+      const size_t o = (size_t)kbh[m] * a.N_max * Lp + code_off(j, s, Lp);
+      if (P > 8) reinterpret_cast<uint16_t*>(a.codes)[o] = (uint16_t)code;
+      else a.codes[o] = (uint8_t)code;
     }
   }
   if (a.V && wt == 0) {   // ||v_j||: warp w handles keys 4w .. 4w+3

@@ -219,9 +219,107 @@ score_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
   }
 }
 
+// ----------------------------------------------------------------------------
+// wide-code score kernel (P > 8, NEXT-2): codes are uint16, the LUT image holds
+// per head the factor half-tables A_h (low Pl bits) and B_h (high P - Pl bits);
+//   w_hat(j) = sum_s sum_h A_h[l(s)](lo) * B_h[l(s)](hi)   (fp32 fma, s then h ascending)
+// One CTA = (selection row, 256-tile chunk); lane = key, same bank-rotated
+// column c(s, lane) = (s & 32) | ((s + lane) & 31) as the byte-code kernel.
+// ----------------------------------------------------------------------------
+constexpr int kWideThreads = 512;
+constexpr int kWideTilesPerCta = 256;
+
+template <int NH>
+__global__ void __launch_bounds__(kWideThreads, 1)
+score_wide_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ codes,
+                  const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
+                  const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
+                  int G_sel, int N_max, int Lp, int P, int E, int row_floats) {
+  extern __shared__ __align__(16) float wlut[];
+  const int row = blockIdx.y;
+  const int b = row / H_sel, r = row % H_sel, g = r / G_sel;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const float4* src = reinterpret_cast<const float4*>(lut_g + (size_t)row * row_floats);
+  for (int i = threadIdx.x; i < row_floats / 4; i += kWideThreads)
+    reinterpret_cast<float4*>(wlut)[i] = src[i];
+  __syncthreads();
+  const int n = seq_lens[b];
+  const int Pl = P / 2;
+  const uint32_t lomask = (1u << Pl) - 1u;
+  const int CB = Lp < 16 ? Lp : 16;
+  const int tiles = N_max >> 5;
+  const int t0 = blockIdx.x * kWideTilesPerCta;
+  const int t1 = min(t0 + kWideTilesPerCta, tiles);
+  const uint16_t* crow = codes + ((size_t)b * H_kv + g) * N_max * Lp;
+  const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
+  const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
+  float* srow = scores + (size_t)row * N_max;
+  for (int ti = t0 + warp; ti < t1; ti += kWideThreads / 32) {
+    const int j = ti * 32 + lane;
+    if (ti * 32 >= n) {                       // whole tile past seq_len
+      srow[j] = -INFINITY;
+      continue;
+    }
+    float acc = 0.f;
+    for (int ch = 0; ch < Lp / CB; ++ch) {
+      const uint16_t* cp = crow + code_off(j, ch * CB, Lp);
+      uint4 w[2];
+      w[0] = ldg_nc_v4(cp);
+      w[1] = CB == 16 ? ldg_nc_v4(cp + 8) : make_uint4(0, 0, 0, 0);
+      const uint32_t* wd = reinterpret_cast<const uint32_t*>(w);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        if (e >= CB) break;
+        const int sidx = ch * CB + e;
+        const uint32_t code = (e & 1) ? (wd[e >> 1] >> 16) : (wd[e >> 1] & 0xFFFFu);
+        const int col = (sidx & 32) | ((sidx + lane) & 31);
+        const int lo = (int)(code & lomask), hi = (int)(code >> Pl);
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+          acc = fmaf(wlut[((h * 2) * E + lo) * 64 + col], wlut[((h * 2 + 1) * E + hi) * 64 + col], acc);
+      }
+    }
+    const bool ok = j < n && (!mrow || mrow[j]);
+    srow[j] = ok ? vrow[j] * acc : -INFINITY;
+  }
+}
+
+static socket_status launch_score_wide(const socket_cfg& c, const float* lut, const uint8_t* codes,
+                                       const float* vnorm, const int32_t* seq_lens,
+                                       const uint8_t* mask, float* scores, cudaStream_t st) {
+  const int Lp = code_slots(c.L);
+  if (Lp > 64) return fail(SOCKET_EUNSUPPORTED, "score: P > 8 with more than 64 tables");
+  const size_t bytes = lut_row_bytes(c);
+  if (bytes > kWideLutMax)
+    return fail(SOCKET_EUNSUPPORTED, "score: P > 8 half-tables of this group size exceed shared memory");
+  const int NH = heads_per_row(c);
+  const int H_sel = num_sel_rows(c);
+  const int G_sel = c.group_mode == SOCKET_GROUP_PER_QHEAD ? c.H_q / c.H_kv : 1;
+  const dim3 grid((c.N_max / 32 + kWideTilesPerCta - 1) / kWideTilesPerCta, c.B * H_sel);
+  if (grid.x == 0 || grid.y == 0) return SOCKET_OK;
+  const int E = wide_entries(c.P);
+  const int row_floats = (int)(bytes / sizeof(float));
+#define SK_WIDE(N)                                                                             \
+  case N:                                                                                      \
+    cudaFuncSetAttribute(score_wide_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); \
+    score_wide_kernel<N><<<grid, kWideThreads, bytes, st>>>(                                   \
+        lut, reinterpret_cast<const uint16_t*>(codes), vnorm, seq_lens, mask, scores, H_sel, c.H_kv, \
+        G_sel, c.N_max, Lp, c.P, E, row_floats);                                               \
+    break;
+  switch (NH) {
+    SK_WIDE(1) SK_WIDE(2) SK_WIDE(4) SK_WIDE(8)
+    default:
+      return fail(SOCKET_EUNSUPPORTED, "score: heads per selection row must be 1, 2, 4 or 8");
+  }
+#undef SK_WIDE
+  return check_launch("score_wide_kernel");
+}
+
 socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint8_t* codes,
                                const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
                                float* scores, cudaStream_t st, bool pdl) {
+  if (c.P > 8) return launch_score_wide(c, lut, codes, vnorm, seq_lens, mask, scores, st);
   const int Lp = code_slots(c.L);
   const int H_sel = num_sel_rows(c);
   const int G_sel = c.group_mode == SOCKET_GROUP_PER_QHEAD ? c.H_q / c.H_kv : 1;

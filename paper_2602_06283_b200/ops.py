@@ -105,8 +105,14 @@ def hash_keys(cfg: Config, K, W, codes, V=None, vnorm=None, n_begin: int = 0, n_
     return codes
 
 
+def plain_code_dtype(cfg: Config):
+    """Element type of plain [B][H_kv][L][N_max] codes: uint8 for P <= 8, 16-bit
+    (int16 holding the uint16 bit pattern) for P > 8."""
+    return torch.uint8 if cfg.P <= 8 else torch.int16
+
+
 def pack_codes(cfg: Config, plain):
-    _need(plain, torch.uint8, (cfg.B, cfg.H_kv, cfg.L, cfg.N_max), "plain codes")
+    _need(plain, plain_code_dtype(cfg), (cfg.B, cfg.H_kv, cfg.L, cfg.N_max), "plain codes")
     codes = alloc_codes(cfg, plain.device)
     c = cfg.c()
     check(lib().socket_pack_codes(ctypes.byref(c), _p(plain), _p(codes), _stream(plain)))
@@ -115,7 +121,8 @@ def pack_codes(cfg: Config, plain):
 
 def unpack_codes(cfg: Config, codes):
     _need(codes, torch.uint8, (codes_bytes(cfg),), "codes")
-    plain = torch.zeros((cfg.B, cfg.H_kv, cfg.L, cfg.N_max), dtype=torch.uint8, device=codes.device)
+    plain = torch.zeros((cfg.B, cfg.H_kv, cfg.L, cfg.N_max), dtype=plain_code_dtype(cfg),
+                        device=codes.device)
     c = cfg.c()
     check(lib().socket_unpack_codes(ctypes.byref(c), _p(codes), _p(plain), _stream(codes)))
     return plain

@@ -55,7 +55,7 @@ def _cfg(**kw):
 
 
 @pytest.mark.parametrize("bad,status", [
-    (dict(L=0), 1), (dict(P=0), 1), (dict(P=17), 1), (dict(P=10), 2), (dict(tau=0.0), 1),
+    (dict(L=0), 1), (dict(P=0), 1), (dict(P=17), 1), (dict(tau=0.0), 1),
     (dict(tau=-1.0), 1), (dict(d=64), 2), (dict(d=0), 1), (dict(H_q=6, H_kv=4), 1),
     (dict(N_max=100), 1), (dict(group_mode=7), 1), (dict(L=200), 2), (dict(scoring=2), 1),
 ])
