@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--tau", type=float, default=0.5)
     ap.add_argument("--mode", default="kv_shared", choices=["kv_shared", "per_qhead"])
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-rows", action="store_true", help="skip the NEXT-row measurements")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
@@ -353,6 +354,11 @@ def run_ours(a):
     if not a.no_dense:
         dense = dense_baselines(a, cfg, q, K, V, lens, flush, stream)
 
+    # ---- (3b) the SURVEY section 8(f) rows on the same cache ------------------------
+    rows = {}
+    if not a.no_rows and world == 1:
+        rows = next_rows(a, cfg, dec, q, K, V, W, lens, k, flush, stream, dev, hbm)
+
     # ---- (4) end to end through the public API with host buffers -----------------
     e2e = end_to_end(a, cfg, dec, q, K, V, lens, N, flush, stream, dev)
     e2e_ms = max_over_ranks(e2e["ms"])
@@ -379,11 +385,74 @@ def run_ours(a):
         line["dense"] = {"best": best[0], "tokens_per_s": round(B * world / (best[1]["ms"] * 1e-3), 1),
                          "ms_per_step": best[1]["ms"], "all": dense,
                          "speedup_sparse_vs_dense": round(best[1]["ms"] / step_ms, 3)}
+    if rows:
+        line["next_rows"] = rows
     if cpu:
         line["cpu_baseline"] = {k2: cpu[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def next_rows(a, cfg, dec, q, K, V, W, lens, k, flush, stream, dev, hbm):
+    """SURVEY 8(f) rows on the bench cache, each timed like the headline (L2
+    flushed before every step, CUDA events on the launching stream):
+      hard_lsh  (f3): the fused step with Eq. 3 hard-LSH tables (scoring = 1);
+      wide_codes(f2): the RULER setting L = 60, P = 10 (600 bits/token, uint16
+                      codes), stage by stage; its score kernel's HBM rate;
+      sampling  (f4): Eq. 6 sampling decode over PER_QHEAD rows, M = k draws."""
+    import dataclasses
+
+    import torch
+
+    import datagen
+    from paper_2602_06283_b200 import PER_QHEAD, SocketDecoder, ops
+    from paper_2602_06283_b200 import _lib
+    B, N = cfg.B, cfg.N_max
+    out = {}
+    # f3 -------------------------------------------------------------------------
+    cfg_h = dataclasses.replace(cfg, scoring=1)
+    dh = SocketDecoder(cfg_h, W, K, V, k=k)
+    dh.codes, dh.vnorm = dec.codes, dec.vnorm            # same index, hard tables
+    dh.capture(q, lens, append=True)
+    ms = _time(dh.replay, flush, stream, a.warmup, a.steps)
+    out["hard_lsh"] = {"ms_per_step": round(ms, 5), "tokens_per_s": round(B / (ms * 1e-3), 1),
+                       "config": "same workload, scoring = hard (Eq. 3 collision counts x ||v||)"}
+    del dh
+    # f2 -------------------------------------------------------------------------
+    Lw, Pw = 60, 10
+    cfg_w = dataclasses.replace(cfg, L=Lw, P=Pw)
+    Ww = torch.from_numpy(datagen.make_projections(4343, Lw, Pw, 128).view("int16")).to(dev).view(torch.bfloat16)
+    dw = SocketDecoder(cfg_w, Ww, K, V, k=k)
+    dw.prefill()
+    ms = _time(lambda: dw.step(q, lens, append=True), flush, stream, a.warmup, a.steps)
+    lut = ops.workspace(cfg_w, _lib.OP_SCORE, 1, dev)
+    ops.build_lut(cfg_w, q, Ww, lut)
+    sms = _time(lambda: ops.score_lut(cfg_w, lut, dw.codes, dw.vnorm, lens, out=dw.scores),
+                flush, stream, a.warmup, a.steps)
+    sb = B * cfg.H_kv * N * (Lw * 2 + 4) + B * cfg_w.H_sel * N * 4
+    out["wide_codes"] = {"ms_per_step": round(ms, 5), "tokens_per_s": round(B / (ms * 1e-3), 1),
+                         "score_ms": round(sms, 5), "score_GB/s": round(sb / (sms * 1e-3) / 1e9, 1),
+                         "score_frac": round(sb / (sms * 1e-3) / 1e9 / hbm, 4),
+                         "config": "L=60, P=10 (uint16 codes, 600 bits/token), stage by stage"}
+    del dw, lut
+    torch.cuda.empty_cache()
+    # f4 -------------------------------------------------------------------------
+    cfg_s = dataclasses.replace(cfg, group_mode=PER_QHEAD)
+    sc = ops.score(cfg_s, q, W, dec.codes, dec.vnorm, lens)
+    g = torch.Generator(device=dev).manual_seed(99)
+    u = torch.rand((B, cfg.H_q, k), generator=g, device=dev)
+    smp = torch.empty((B, cfg.H_q, k), dtype=torch.int32, device=dev)
+    o = torch.empty((B, cfg.H_q, 128), dtype=torch.bfloat16, device=dev)
+    ms = _time(lambda: ops.sample_decode(cfg_s, sc, dec.vnorm, V, lens, u, samples=smp, out=o),
+               flush, stream, a.warmup, a.steps)
+    ab = B * cfg.H_q * (N * 8 + k * (4 + 4 + 256 + 4) + 256)
+    out["sampling"] = {"ms": round(ms, 5), "GB/s": round(ab / (ms * 1e-3) / 1e9, 1),
+                       "frac": round(ab / (ms * 1e-3) / 1e9 / hbm, 4), "M": k,
+                       "config": "Eq. 6 over PER_QHEAD rows (B x 32), M = k draws; "
+                                 "bytes = scores + norms per row + per draw (u, J, v row, norm)"}
+    del sc
+    return out
 
 
 def _time(fn, flush, stream, warmup, steps):
@@ -442,8 +511,8 @@ def dense_baselines(a, cfg, q, K, V, lens, flush, stream):
         indptr = torch.arange(0, cfg.B + 1, dtype=torch.int32, device=q.device) * npg
         indices = torch.arange(cfg.B * npg, dtype=torch.int32, device=q.device)
         last = torch.full((cfg.B,), page, dtype=torch.int32, device=q.device)
-        w.plan(indptr, indices, last, cfg.H_q, cfg.H_kv, 128, page, data_type=torch.bfloat16,
-               sm_scale=cfg.scale)
+        w.plan(indptr, indices, last, cfg.H_q, cfg.H_kv, 128, page, q_data_type=torch.bfloat16,
+               kv_data_type=torch.bfloat16, sm_scale=cfg.scale)
         f = lambda: w.run(q, kv)
         res["flashinfer"] = {"ms": round(_time(f, flush, stream, a.warmup, a.steps), 5)}
         del kv
