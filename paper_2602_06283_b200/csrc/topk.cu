@@ -701,7 +701,12 @@ static socket_status launch_topk_common(TopkArgs a, int n_max_row, cudaStream_t 
   int cs = 1;
   const char* tune = getenv("SOCKET_TOPK_MIN_CTAS");   // tuning experiments only
   const int min_ctas = tune ? atoi(tune) : kNumSMs;
-  while (cs < 16 && ((size_t)(n_max_row + cs - 1) / cs > kMaxSlice || a.rows * cs < min_ctas))
+  // grow the cluster while a slice is too big for shared memory, or while the grid
+  // is below min_ctas and the slices stay >= 4096 keys (smaller slices cost more
+  // in cluster synchronization than they save; tools/tune_step.py, B = 1-16)
+  constexpr int kMinSlice = 4096;
+  while (cs < 16 && ((size_t)(n_max_row + cs - 1) / cs > kMaxSlice ||
+                     (a.rows * cs < min_ctas && (n_max_row + 2 * cs - 1) / (2 * cs) >= kMinSlice)))
     cs *= 2;
   int per = (n_max_row + cs - 1) / cs;
   per = (per + 127) & ~127;
