@@ -25,6 +25,12 @@ extern "C" int socket_debug_prologue_trace(unsigned long long* host, int n) {
 }
 #endif
 
+bool fused_step_applies(const socket_cfg& c);
+socket_status launch_fused_step(const socket_cfg& c, const void* q, const void* K, const void* V,
+                                const void* W, uint8_t* codes, float* vnorm, const int32_t* seq_lens,
+                                const uint8_t* mask, int do_append, int k, int sink, int window,
+                                float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
+                                cudaStream_t st);
 socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint8_t* codes,
                                const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
                                float* scores, cudaStream_t st, bool pdl);
@@ -89,6 +95,10 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, const void*
   const size_t lut_bytes = ((size_t)c.B * H_sel * lut_row_bytes(c) + 255) & ~(size_t)255;
   if (ws_bytes < decode_step_workspace_bytes(c, k))
     return fail(SOCKET_EWORKSPACE, "decode step: workspace too small");
+  // small batch (one cluster per selection row fits one wave): one fused launch
+  if (fused_step_applies(c))
+    return launch_fused_step(c, q, K, V, W, codes, vnorm, seq_lens, mask, do_append, k, sink, window,
+                             scores, idx, cnt, out, lse, st);
   float* lut = static_cast<float*>(ws);
   void* dws = static_cast<char*>(ws) + lut_bytes;
   const size_t dws_bytes = ws_bytes - lut_bytes;

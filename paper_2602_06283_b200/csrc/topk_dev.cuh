@@ -1,0 +1,629 @@
+// Device side of the exact cluster top-k (Alg. 3 l.244, PAPER.md; sink/window
+// P:686), shared by topk_cluster_kernel (topk.cu) and the fused small-batch
+// decode step (fused.cu).  Not part of the ABI.
+#pragma once
+#include <cooperative_groups.h>
+#include <cstdlib>
+
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sk {
+
+constexpr int kTopkThreads = 512;
+constexpr int kTopkWarps = kTopkThreads / 32;
+constexpr int kBins = 2048;
+constexpr int kCandCap = 2048;
+
+#ifdef SK_TRACE
+// phase stamps (clock64 of thread 0 of every CTA), read by tools/trace_topk.py
+static __device__ unsigned long long g_topk_trace[4096 * 16];   // per translation unit
+#define TK_TRACE(i)                                                                          \
+  do {                                                                                       \
+    if (threadIdx.x == 0) {                                                                  \
+      const int cta = blockIdx.y * gridDim.x + blockIdx.x;                                   \
+      if (cta < 4096) g_topk_trace[cta * 16 + (i)] = clock64();                              \
+    }                                                                                        \
+  } while (0)
+#else
+#define TK_TRACE(i) \
+  do {              \
+  } while (0)
+#endif
+
+struct TopkArgs {
+  // mode 0: scores [rows][N_max], n = seq_lens[b]
+  // mode 1: resolve; candidates cand_scores [G][rows][k]; n = G*k
+  int mode;
+  const float* scores;
+  const int32_t* seq_lens;
+  const float* cand_scores;
+  const int32_t* cand_idx;
+  int rows, H_sel, N_max, k, sink, window, G, rank;
+  int per;                 // slice length per CTA (multiple of 32)
+  int32_t* idx;
+  int32_t* cnt;
+  float* sel_scores;
+};
+
+__device__ __forceinline__ float load_elem(const TopkArgs& a, int row, int e) {
+  if (a.mode == 0) return a.scores[(size_t)row * a.N_max + e];
+  const int s = e / a.k, i = e % a.k;
+  return a.cand_scores[((size_t)s * a.rows + row) * a.k + i];
+}
+
+__device__ __forceinline__ uint32_t make_key(float s, int e, int n, int sink, int window, int mode) {
+  if (s == -INFINITY) return 0u;
+  if (mode == 0 && (e < sink || e >= n - window)) return 0xFFFFFFFFu;
+  return f2key(s);
+}
+
+// exclusive scan over the warps of one value per warp
+__device__ __forceinline__ int block_excl_scan_warps(int v, int* sh, int warp, int lane, int& total) {
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  int pre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kTopkWarps; ++w) {
+    const int x = sh[w];
+    pre += (w < warp) ? x : 0;
+    tot += x;
+  }
+  total = tot;
+  return pre;
+}
+
+struct __align__(16) TopkShared {
+  uint32_t hist[kBins];          // local histogram (radix fallback: two 256-bin buffers)
+  uint32_t cand[kCandCap];       // local candidates: keys of the target bin
+  uint32_t cidx[kCandCap];       // their slice-local indices
+  uint32_t gcand[kCandCap];      // candidates gathered from the cluster, rank-major
+  uint32_t rhist[256];           // local radix histogram for candidate resolve
+  int scan[kTopkWarps];
+  int scan2[kTopkWarps];
+  uint32_t wab[kTopkWarps];      // per warp: keys strictly above the target bin (forced included)
+  uint32_t wgt[kTopkWarps];      // per warp: local candidates > T
+  uint32_t weq[kTopkWarps];      // per warp: local candidates == T
+  uint32_t roff[17];             // gathered-candidate offset of every rank
+  uint32_t rab[16];              // above-bin count of every rank
+  uint32_t glob[4];              // cluster totals: nvalid, nforced, kmin, kmax
+  uint32_t coarse[64];           // local histogram folded into 64 coarse bins (read remotely)
+  uint32_t acc[2];               // lower ranks' candidates > T / == T
+  alignas(16) uint32_t stat[8];  // nvalid, nforced, kmin, kmax, ncand, above, gt, eq (read remotely)
+  uint32_t dec[4];
+};
+
+// Local exact select over a small candidate array: the `need`-th largest key
+// (1-based) and how many candidates are strictly greater.
+__device__ __forceinline__ void local_select(const uint32_t* c, int C, uint32_t need, TopkShared& S, int tid,
+                             int warp, int lane, uint32_t& T, uint32_t& above) {
+  uint32_t prefix = 0, k_rem = need;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    const uint32_t hmask = pass == 0 ? 0u : (0xFFFFFFFFu << (shift + 8));
+    for (int i = tid; i < 256; i += kTopkThreads) S.rhist[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < ((C + 31) & ~31); i += kTopkThreads) {
+      const bool m = i < C && (c[i] & hmask) == (prefix & hmask);
+      const uint32_t bin = m ? ((c[i] >> shift) & 255u) : 256u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+      if (m && lane == __ffs(peers) - 1) atomicAdd(&S.rhist[bin], (uint32_t)__popc(peers));
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t c8[8], tot = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { c8[q] = S.rhist[255 - (lane * 8 + q)]; tot += c8[q]; }
+      uint32_t inc = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const uint32_t excl = inc - tot;
+      const unsigned hb = __ballot_sync(0xffffffffu, excl < k_rem && inc >= k_rem);
+      if (lane == __ffs(hb) - 1) {
+        uint32_t run = excl;
+        for (int q = 0; q < 8; ++q) {
+          if (run + c8[q] >= k_rem) { S.dec[0] = 255 - (lane * 8 + q); S.dec[1] = k_rem - run; break; }
+          run += c8[q];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= S.dec[0] << shift;
+    k_rem = S.dec[1];
+  }
+  T = prefix;
+  above = need - k_rem;
+}
+
+// Everything after the slice load: cluster statistics, the exact threshold T
+// and tie quota, and the stable emit of idx / cnt (see the file header of
+// topk.cu).  keys[] holds this CTA's slice (base, len) as monotone u32 keys
+// (len rounded up to 128 with 0 = invalid), and (nvalid, nforced, kmin, kmax)
+// are this thread's statistics of its loaded keys (kmin over regular keys,
+// 0xFFFFFFFF if none).  If sel_local != NULL, the CTA's selected keys (global
+// indices, ascending) are also written to sel_local[0 .. *sel_cnt), i.e. the
+// CTA's contiguous share idx[row][*sel_lo .. *sel_lo + *sel_cnt).
+__device__ __forceinline__ void topk_core(const TopkArgs& a, uint32_t* keys, TopkShared& S, int row,
+                                       int n, int base, int len, uint32_t nvalid, uint32_t nforced,
+                                       uint32_t kmin, uint32_t kmax, int32_t* sel_local,
+                                       int* sel_lo, int* sel_cnt) {
+  constexpr unsigned kFull = 0xffffffffu;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int csize = (int)cluster.num_blocks();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int len32 = (len + 31) & ~31;
+  const int len128 = (len + 127) & ~127;
+  const int nr = len128 >> 7;
+  const int rpw = max(1, (nr + kTopkWarps - 1) / kTopkWarps);
+  const int r0 = warp * rpw, r1 = min(nr, r0 + rpw);
+  (void)len32;
+  if (tid < 8) S.stat[tid] = (tid == 2) ? 0xFFFFFFFFu : 0u;   // kmin starts at +max
+  if (tid < kTopkWarps) { S.wgt[tid] = 0; S.weq[tid] = 0; }
+  if (tid < 2) S.acc[tid] = 0;
+  for (int i = tid; i < kBins; i += kTopkThreads) S.hist[i] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    nvalid += __shfl_xor_sync(kFull, nvalid, o);
+    nforced += __shfl_xor_sync(kFull, nforced, o);
+    kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
+  }
+  if (lane == 0) {
+    atomicAdd(&S.stat[0], nvalid);
+    atomicAdd(&S.stat[1], nforced);
+    atomicMin(&S.stat[2], kmin);
+    atomicMax(&S.stat[3], kmax);
+  }
+  TK_TRACE(2);
+  cluster.sync();
+  // ---- 1. cluster totals: lane r of warp 0 reads rank r's statistics ----------
+  if (warp == 0) {
+    uint32_t v0 = 0, v1 = 0, v2 = 0xFFFFFFFFu, v3 = 0;
+    if (lane < csize) {
+      const uint4 rs = *reinterpret_cast<const uint4*>(cluster.map_shared_rank(S.stat, lane));
+      v0 = rs.x; v1 = rs.y; v2 = rs.z; v3 = rs.w;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      v0 += __shfl_xor_sync(kFull, v0, o);
+      v1 += __shfl_xor_sync(kFull, v1, o);
+      v2 = min(v2, __shfl_xor_sync(kFull, v2, o));
+      v3 = max(v3, __shfl_xor_sync(kFull, v3, o));
+    }
+    if (lane == 0) { S.glob[0] = v0; S.glob[1] = v1; S.glob[2] = v2; S.glob[3] = v3; }
+  }
+  __syncthreads();
+  const uint32_t tvalid = S.glob[0], tforced = S.glob[1], gmin = S.glob[2], gmax = S.glob[3];
+  const uint32_t k_eff = min((uint32_t)a.k, tvalid);
+  TK_TRACE(3);
+
+  // ---- find T and quota --------------------------------------------------------
+  uint32_t T = 0, quota = 0;            // select keys > T, plus `quota` keys == T
+  bool done = false;
+  if (k_eff == tvalid) {
+    done = true;                         // everything valid is selected
+  } else if (k_eff <= tforced) {
+    T = 0xFFFFFFFFu;                     // only forced keys (they all tie at the max key)
+    quota = k_eff;
+    done = true;
+  }
+  const uint32_t need = k_eff - tforced;  // rank among regular keys (>= 1 when !done)
+  bool fallback = false, counted = false;
+  if (!done) {
+    // 2. adaptive histogram over [gmin, gmax]
+    // bin = (key - gmin) >> sh with the smallest sh that maps [gmin, gmax] into
+    // kBins bins: monotone and exact (no division)
+    const uint32_t span = gmax - gmin;
+    const int sh = span < (uint32_t)kBins ? 0 : (32 - __clz(span)) - 11;
+    for (int i = tid * 4; i < len128; i += kTopkThreads * 4) {
+      const uint4 kv = *reinterpret_cast<const uint4*>(keys + i);
+      const uint32_t k4[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (k4[e] != 0u && k4[e] != 0xFFFFFFFFu) atomicAdd(&S.hist[(k4[e] - gmin) >> sh], 1u);
+    }
+    // coarse histogram: 64 bins of 32 fine bins each (thread t folds bins 4t..4t+3,
+    // 8 lanes per coarse bin)
+    __syncthreads();
+    {
+      const uint4 h = *reinterpret_cast<const uint4*>(&S.hist[tid * 4]);
+      uint32_t cs4 = h.x + h.y + h.z + h.w;
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) cs4 += __shfl_xor_sync(kFull, cs4, o);
+      if ((lane & 7) == 0) S.coarse[tid >> 3] = cs4;
+    }
+    TK_TRACE(4);
+    cluster.sync();
+    TK_TRACE(5);
+    // cluster sums, coarse then fine (DSMEM: csize x (64 + 32) words per CTA), each
+    // followed by a descending suffix scan that locates the bin of rank `need`
+    if (warp == 0) {
+      uint32_t c0 = 0, c1 = 0;                 // coarse bins 63 - 2 lane, 62 - 2 lane
+      for (int r = 0; r < csize; ++r) {
+        const uint32_t* rc = cluster.map_shared_rank(S.coarse, r);
+        c0 += rc[63 - 2 * lane];
+        c1 += rc[62 - 2 * lane];
+      }
+      const uint32_t tot = c0 + c1;
+      uint32_t inc = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const uint32_t excl = inc - tot;         // keys in coarse bins above mine
+      const unsigned hit = __ballot_sync(kFull, excl < need && inc >= need);
+      const int hl = __ffs(hit) - 1;
+      const uint32_t ex_h = __shfl_sync(kFull, excl, hl), c0_h = __shfl_sync(kFull, c0, hl);
+      const bool first = ex_h + c0_h >= need;
+      const int cb = first ? 63 - 2 * hl : 62 - 2 * hl;
+      const uint32_t need_c = need - (first ? ex_h : ex_h + c0_h);   // rank inside coarse bin cb
+      // fine bins of cb: lane l holds bin cb*32 + 31 - l (descending)
+      const int fb = cb * 32 + 31 - lane;
+      uint32_t f = 0;
+      for (int r = 0; r < csize; ++r) f += cluster.map_shared_rank(S.hist, r)[fb];
+      uint32_t finc = f;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, finc, o);
+        if (lane >= o) finc += y;
+      }
+      const uint32_t fex = finc - f;
+      if (fex < need_c && finc >= need_c) { S.dec[0] = (uint32_t)fb; S.dec[1] = need_c - fex; S.dec[2] = f; }
+    }
+    __syncthreads();
+    const uint32_t bstar = S.dec[0], need2 = S.dec[1], C = S.dec[2];
+    TK_TRACE(6);
+    if (C <= (uint32_t)kCandCap) {
+      // 3. candidate pass: keys of bin bstar -> S.cand (+ slice index); per warp the
+      //    number of keys strictly above the bin (all of them are > T, forced included)
+      // a lane scans 4 consecutive keys per 128-key round (same rounds per warp
+      // as the emit pass, so the per-warp counts line up)
+      uint32_t ab = 0;
+      for (int r = r0; r < r1; ++r) {
+        const int i0 = r * 128 + lane * 4;
+        const uint4 kv = *reinterpret_cast<const uint4*>(keys + i0);
+        const uint32_t k4[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t key = k4[e];
+          const bool reg = key != 0u && key != 0xFFFFFFFFu;
+          const uint32_t bin = (key - gmin) >> sh;
+          ab += (key == 0xFFFFFFFFu || (reg && bin > bstar)) ? 1u : 0u;
+          if (reg && bin == bstar) {              // rare: ~C / len of the keys
+            const uint32_t sl = atomicAdd(&S.stat[4], 1u);
+            S.cand[sl] = key;
+            S.cidx[sl] = (uint32_t)(i0 + e);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) ab += __shfl_xor_sync(kFull, ab, o);
+      if (lane == 0) { S.wab[warp] = ab; atomicAdd(&S.stat[5], ab); }
+      TK_TRACE(7);
+      cluster.sync();
+      TK_TRACE(8);
+      // gather every rank's candidates (rank-major) and above-bin counts
+      if (warp == 0) {
+        uint32_t nc = 0, rab = 0;
+        if (lane < csize) {
+          const uint32_t* rs = cluster.map_shared_rank(S.stat, lane);
+          nc = rs[4];
+          rab = rs[5];
+        }
+        uint32_t inc = nc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (lane < csize) { S.roff[lane + 1] = inc; S.rab[lane] = rab; }
+        if (lane == 0) S.roff[0] = 0;
+      }
+      __syncthreads();
+      for (int i = tid; i < (int)C; i += kTopkThreads) {
+        int r = 0;
+        while (r + 1 < csize && S.roff[r + 1] <= (uint32_t)i) ++r;
+        S.gcand[i] = cluster.map_shared_rank(S.cand, r)[i - (int)S.roff[r]];
+      }
+      __syncthreads();
+      // T = the need2-th largest candidate, above = candidates > T
+      uint32_t above;
+      if (C <= 1024u) {
+        // rank counting: candidate i is T iff #greater < need2 <= #greater + #equal
+        for (int i = tid; i < (int)C; i += kTopkThreads) {
+          const uint32_t me = S.gcand[i];
+          uint32_t gt = 0, eq = 0;
+          int j = 0;
+          for (; j + 4 <= (int)C; j += 4) {
+            const uint4 v = *reinterpret_cast<const uint4*>(&S.gcand[j]);
+            gt += (v.x > me) + (v.y > me) + (v.z > me) + (v.w > me);
+            eq += (v.x == me) + (v.y == me) + (v.z == me) + (v.w == me);
+          }
+          for (; j < (int)C; ++j) { gt += S.gcand[j] > me; eq += S.gcand[j] == me; }
+          if (gt < need2 && gt + eq >= need2) { S.dec[0] = me; S.dec[1] = gt; }   // ties write equal values
+        }
+        __syncthreads();
+        T = S.dec[0];
+        above = S.dec[1];
+      } else {
+        local_select(S.gcand, (int)C, need2, S, tid, warp, lane, T, above);
+      }
+      quota = need2 - above;
+      TK_TRACE(9);
+      // keys > T / == T before this CTA and per warp, from the candidate lists alone
+      uint32_t gtb = 0, eqb = 0;
+      for (int i = tid; i < (int)S.roff[crank]; i += kTopkThreads) {
+        const uint32_t cv = S.gcand[i];
+        gtb += cv > T;
+        eqb += cv == T;
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        gtb += __shfl_xor_sync(kFull, gtb, o);
+        eqb += __shfl_xor_sync(kFull, eqb, o);
+      }
+      if (lane == 0 && (gtb | eqb)) { atomicAdd(&S.acc[0], gtb); atomicAdd(&S.acc[1], eqb); }
+      const int nloc = (int)S.stat[4];
+      for (int i = tid; i < nloc; i += kTopkThreads) {
+        const uint32_t cv = S.cand[i];
+        const int w = (int)(S.cidx[i] >> 7) / rpw;
+        if (cv > T) atomicAdd(&S.wgt[w], 1u);
+        else if (cv == T) atomicAdd(&S.weq[w], 1u);
+      }
+      __syncthreads();
+      counted = true;
+    } else {
+      fallback = true;
+    }
+  }
+  if (fallback) {
+    // 4-pass MSB radix select over the cluster (8-bit digits), regular keys only
+    uint32_t prefix = 0, k_rem = need;
+    uint32_t* h2 = S.hist;                  // two 256-bin buffers: hist[0..255], hist[256..511]
+    cluster.sync();                          // everyone finished reading the 2048-bin histograms
+    for (int i = tid; i < 512; i += kTopkThreads) h2[i] = 0;
+    __syncthreads();
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass;
+      uint32_t* hb = h2 + (pass & 1) * 256;
+      const uint32_t hmask = pass == 0 ? 0u : (0xFFFFFFFFu << (shift + 8));
+      for (int i = tid; i < len32; i += kTopkThreads) {
+        const uint32_t key = keys[i];
+        const bool m = key != 0u && key != 0xFFFFFFFFu && (key & hmask) == (prefix & hmask);
+        const uint32_t bin = m ? ((key >> shift) & 255u) : 256u;
+        const uint32_t peers = __match_any_sync(kFull, bin);
+        if (m && lane == __ffs(peers) - 1) atomicAdd(&hb[bin], (uint32_t)__popc(peers));
+      }
+      cluster.sync();
+      if (warp == 0) {
+        uint32_t c8[8], tot = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int bin = 255 - (lane * 8 + q);
+          uint32_t s = 0;
+          for (int c = 0; c < csize; ++c) s += *cluster.map_shared_rank(&hb[bin], c);
+          c8[q] = s;
+          tot += s;
+        }
+        uint32_t inc = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, inc, o);
+          if (lane >= o) inc += y;
+        }
+        const uint32_t excl = inc - tot;
+        const unsigned hbits = __ballot_sync(kFull, excl < k_rem && inc >= k_rem);
+        if (lane == __ffs(hbits) - 1) {
+          uint32_t run = excl;
+          for (int q = 0; q < 8; ++q) {
+            if (run + c8[q] >= k_rem) { S.dec[0] = 255 - (lane * 8 + q); S.dec[1] = k_rem - run; break; }
+            run += c8[q];
+          }
+        }
+      }
+      // clear the other buffer (its last remote readers finished before this sync)
+      for (int i = tid; i < 256; i += kTopkThreads) h2[((pass + 1) & 1) * 256 + i] = 0;
+      __syncthreads();
+      prefix |= S.dec[0] << shift;
+      k_rem = S.dec[1];
+    }
+    T = prefix;
+    quota = k_rem;
+  }
+
+  // ---- stable compaction ------------------------------------------------------
+  // Output position of a selected key = gt_rank + min(eq_rank, quota), where
+  // gt_rank / eq_rank count keys > T / == T at smaller indices (row-global).
+  int em_all = 0;
+  TK_TRACE(10);
+  if (a.mode == 0) {
+    int gbase, ebase;   // row-global ranks of this warp's first key
+    uint32_t cta_gb = 0, cta_eb = 0, cta_gt = 0, cta_eq = 0;   // this CTA's share (sel_local)
+    if (counted) {
+      uint32_t gb = S.acc[0], eb = S.acc[1];
+      for (int r = 0; r < crank; ++r) gb += S.rab[r];
+      uint32_t gw = 0, ew = 0;
+      for (int w = 0; w < warp; ++w) { gw += S.wab[w] + S.wgt[w]; ew += S.weq[w]; }
+      gbase = (int)(gb + gw);
+      ebase = (int)(eb + ew);
+      cta_gb = gb;
+      cta_eb = eb;
+      for (int w = 0; w < kTopkWarps; ++w) { cta_gt += S.wab[w] + S.wgt[w]; cta_eq += S.weq[w]; }
+    } else {
+      // everything / only forced keys selected, or the radix fallback: count pass
+      uint32_t g = 0, e = 0;
+      for (int r = r0; r < r1; ++r) {
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const uint32_t key = keys[r * 128 + x * 32 + lane];
+          g += __popc(__ballot_sync(kFull, key > T));
+          e += __popc(__ballot_sync(kFull, key != 0u && key == T));
+        }
+      }
+      if (lane == 0) { S.scan[warp] = (int)g; S.scan2[warp] = (int)e; }
+      __syncthreads();
+      uint32_t gw = 0, ew = 0, gtot = 0, etot = 0;
+#pragma unroll
+      for (int w = 0; w < kTopkWarps; ++w) {
+        const uint32_t xg = (uint32_t)S.scan[w], xe = (uint32_t)S.scan2[w];
+        gw += w < warp ? xg : 0u; ew += w < warp ? xe : 0u;
+        gtot += xg; etot += xe;
+      }
+      if (tid == 0) { S.stat[6] = gtot; S.stat[7] = etot; }
+      cluster.sync();
+      uint32_t gb = 0, eb = 0;
+      for (int r = 0; r < crank; ++r) {
+        const uint32_t* rs = cluster.map_shared_rank(S.stat, r);
+        gb += rs[6];
+        eb += rs[7];
+      }
+      gbase = (int)(gb + gw);
+      ebase = (int)(eb + ew);
+      cta_gb = gb;
+      cta_eb = eb;
+      cta_gt = gtot;
+      cta_eq = etot;
+    }
+    TK_TRACE(11);
+    const int sel0 = (int)cta_gb + min((int)cta_eb, (int)quota);
+    if (sel_lo) {
+      *sel_lo = sel0;
+      *sel_cnt = (int)(cta_gb + cta_gt) + min((int)(cta_eb + cta_eq), (int)quota) - sel0;
+    }
+    em_all = (int)k_eff;
+    int32_t* orow = a.idx + (size_t)row * a.k;
+    float* srow = a.sel_scores ? a.sel_scores + (size_t)row * a.k : nullptr;
+    const int q = (int)quota;
+    for (int r = r0; r < r1; ++r) {
+      // lane owns keys 4 lane .. 4 lane + 3 of the round (index order within the
+      // round = lane-major); ties at T (rare) take the per-32 ballot path below
+      const int i0 = r * 128 + lane * 4;
+      const uint4 kv = *reinterpret_cast<const uint4*>(keys + i0);
+      const uint32_t k4[4] = {kv.x, kv.y, kv.z, kv.w};
+      const bool anyeq = (k4[0] == T) | (k4[1] == T) | (k4[2] == T) | (k4[3] == T);
+      if (!__any_sync(kFull, anyeq && T != 0u)) {
+        unsigned gm[4];
+        int pre = 0, tot = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          gm[e] = __ballot_sync(kFull, k4[e] > T);
+          pre += __popc(gm[e] & lt);
+          tot += __popc(gm[e]);
+        }
+        int pos = gbase + pre + min(ebase, q);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (k4[e] > T) {
+            orow[pos] = base + i0 + e;
+            if (srow) srow[pos] = load_elem(a, row, base + i0 + e);
+            if (sel_local) sel_local[pos - sel0] = base + i0 + e;
+            ++pos;
+          }
+        }
+        gbase += tot;
+        continue;
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int i = r * 128 + x * 32 + lane;
+        const uint32_t key = keys[i];
+        const bool isgt = key > T, iseq = key != 0u && key == T;
+        const unsigned gmx = __ballot_sync(kFull, isgt), em = __ballot_sync(kFull, iseq);
+        const int gr = gbase + __popc(gmx & lt), er = ebase + __popc(em & lt);
+        if (isgt || (iseq && er < q)) {
+          const int p = gr + min(er, q);
+          orow[p] = base + i;
+          if (srow) srow[p] = load_elem(a, row, base + i);
+          if (sel_local) sel_local[p - sel0] = base + i;
+        }
+        gbase += __popc(gmx);
+        ebase += __popc(em);
+      }
+    }
+  } else {
+    const int groups = len32 >> 5;
+    const int gpw = (groups + kTopkWarps - 1) / kTopkWarps;
+    const int g0 = warp * gpw;
+    const int g1 = min(groups, g0 + gpw);
+    int eq_w = 0;
+    for (int gi = g0; gi < g1; ++gi) {
+      const uint32_t key = keys[gi * 32 + lane];
+      eq_w += __popc(__ballot_sync(0xffffffffu, key != 0u && key == T));
+    }
+    int eq_tot;
+    const int eq_pre = block_excl_scan_warps(eq_w, S.scan, warp, lane, eq_tot);
+    if (tid == 0) S.stat[6] = (uint32_t)eq_tot;
+    cluster.sync();
+    int eq_before = 0;
+    for (int c = 0; c < crank; ++c) eq_before += (int)*cluster.map_shared_rank(&S.stat[6], c);
+    const int emit_lo = a.rank * a.k;
+    const int emit_hi = (a.rank + 1) * a.k;
+    int em_w = 0;
+    {
+      int eq_run = eq_before + eq_pre;
+      for (int gi = g0; gi < g1; ++gi) {
+        const int i = gi * 32 + lane;
+        const uint32_t key = keys[i];
+        const bool valid = key != 0u;
+        const unsigned eb = __ballot_sync(0xffffffffu, valid && key == T);
+        const int my_eq = eq_run + __popc(eb & ((1u << lane) - 1u));
+        const int e = base + i;
+        const bool sel = valid && (key > T || (key == T && (uint32_t)my_eq < quota)) &&
+                         e >= emit_lo && e < emit_hi;
+        em_w += __popc(__ballot_sync(0xffffffffu, sel));
+        eq_run += __popc(eb);
+      }
+    }
+    int em_tot;
+    const int em_pre = block_excl_scan_warps(em_w, S.scan, warp, lane, em_tot);
+    if (tid == 0) S.stat[7] = (uint32_t)em_tot;
+    cluster.sync();
+    int em_before = 0;
+    for (int c = 0; c < csize; ++c) {
+      const int x = (int)*cluster.map_shared_rank(&S.stat[7], c);
+      em_all += x;
+      em_before += c < crank ? x : 0;
+    }
+    int eq_run = eq_before + eq_pre;
+    int pos = em_before + em_pre;
+    int32_t* orow = a.idx + (size_t)row * a.k;
+    for (int gi = g0; gi < g1; ++gi) {
+      const int i = gi * 32 + lane;
+      const uint32_t key = keys[i];
+      const bool valid = key != 0u;
+      const unsigned eb = __ballot_sync(0xffffffffu, valid && key == T);
+      const int my_eq = eq_run + __popc(eb & ((1u << lane) - 1u));
+      const int e = base + i;
+      const bool sel = valid && (key > T || (key == T && (uint32_t)my_eq < quota)) &&
+                       e >= emit_lo && e < emit_hi;
+      const unsigned sb = __ballot_sync(0xffffffffu, sel);
+      if (sel) orow[pos + __popc(sb & ((1u << lane) - 1u))] =
+          a.cand_idx[((size_t)a.rank * a.rows + row) * a.k + (e - emit_lo)];
+      pos += __popc(sb);
+      eq_run += __popc(eb);
+    }
+  }
+  TK_TRACE(12);
+  if (crank == 0) {
+    int32_t* orow = a.idx + (size_t)row * a.k;
+    for (int p = em_all + tid; p < a.k; p += kTopkThreads) {
+      orow[p] = -1;
+      if (a.sel_scores) a.sel_scores[(size_t)row * a.k + p] = -INFINITY;
+    }
+    if (tid == 0) a.cnt[row] = em_all;
+  }
+  TK_TRACE(13);
+  cluster.sync();   // keep shared memory alive until every CTA finished remote reads
+  TK_TRACE(14);
+}
+
+}  // namespace sk

@@ -430,8 +430,10 @@ def test_full_size_c2_sampled(B, k):
 
 
 def test_decode_step_fused_matches_unfused():
-    """socket_decode_step (fused prologue + PDL chain) is bit-identical to the
-    stage-by-stage calls."""
+    """socket_decode_step (small batch: the one-launch cluster kernel) gives the
+    stage-by-stage calls' codes, norms, scores and selection bit for bit; the
+    attention is split per cluster CTA instead of per decode split, so out and
+    lse agree to fp32 / bf16 rounding."""
     cfg, c, W, d = make(2, 8, 2, 4096, 60, 8, seed=41)
     a = SocketDecoder(cfg, d["W"], d["K"].clone(), d["V"].clone(), k=409)
     b = SocketDecoder(cfg, d["W"], d["K"].clone(), d["V"].clone(), k=409)
@@ -442,12 +444,17 @@ def test_decode_step_fused_matches_unfused():
     assert torch.equal(a.codes, b.codes) and torch.equal(a.vnorm, b.vnorm)
     assert torch.equal(a.scores, b.scores)
     assert torch.equal(a.idx, b.idx) and torch.equal(a.cnt, b.cnt)
-    assert torch.equal(oa, ob) and torch.equal(la, lb)
+    assert (oa.float() - ob.float()).abs().max().item() <= 2e-3
+    assert ((la - lb).abs() <= 1e-4 + 2e-5 * lb.abs()).all()
 
 
-def test_decode_step_ragged_sink_window_mask_vs_oracle():
-    """Fused step with ragged lengths (the append hashes key seq_lens[b]-1 of each
-    sequence), sink/window forcing and a key mask, against the oracle."""
+@pytest.mark.parametrize("one_launch", [True, False])
+def test_decode_step_ragged_sink_window_mask_vs_oracle(one_launch, monkeypatch):
+    """socket_decode_step with ragged lengths (the append hashes key seq_lens[b]-1
+    of each sequence), sink/window forcing and a key mask, against the oracle --
+    through the one-launch cluster kernel and through the PDL-chained kernels."""
+    if not one_launch:
+        monkeypatch.setenv("SOCKET_NO_FUSED", "1")
     lens = [3000, 4096, 1]
     cfg, c, W, d = make(3, 8, 2, 4096, 16, 8, seed=43, seq_lens=lens)
     k, sink, window = 300, 4, 16
