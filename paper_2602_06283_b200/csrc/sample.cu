@@ -38,6 +38,21 @@ struct SampleArgs {
   int H_q, H_kv, N_max, M, Mp2;
 };
 
+// 4 consecutive floats at p[j..j+3] (j % 4 == 0, 16-B aligned); lanes >= j1 read as 0
+__device__ __forceinline__ float4 ld4_masked(const float* p, int j, int j1) {
+  if (j + 4 <= j1) return __ldg(reinterpret_cast<const float4*>(p + j));
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j < j1) v.x = p[j];
+  if (j + 1 < j1) v.y = p[j + 1];
+  if (j + 2 < j1) v.z = p[j + 2];
+  return v;
+}
+__device__ __forceinline__ float pick8(const float4& a, const float4& b, int i) {
+  const float4 v = i < 4 ? a : b;
+  const int k = i & 3;
+  return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+
 __device__ __forceinline__ bool pair_less(float a, int ia, float b, int ib) {
   return a < b || (a == b && ia < ib);
 }
@@ -85,17 +100,23 @@ __global__ void __launch_bounds__(kSmpThreads, 1) sample_decode_kernel(SampleArg
   }
 
   // ---- 2. segment sums and the block scan ----------------------------------------
-  const int S = (n + kSmpThreads - 1) / kSmpThreads;
+  // segments are multiples of 4 keys so they can be read as float4 (j0 16-B aligned)
+  const int S = (((n + kSmpThreads - 1) / kSmpThreads) + 3) & ~3;
   const int j0 = min(tid * S, n), j1 = min(j0 + S, n);
   float seg_s = 0.f, seg_w = 0.f;
   int jpos = -1;
-  for (int j = j0; j < j1; ++j) {
-    const float s = srow[j];
-    if (s > 0.f) {                           // -inf (invalid) and 0 carry no mass
-      seg_s += s;
-      const float vn = vrow[j];
-      seg_w += vn > 0.f ? s / vn : 0.f;      // w_hat_j = s_j / ||v_j||  (reading R-24)
-      jpos = j;
+#pragma unroll 4
+  for (int j = j0; j < j1; j += 4) {
+    const float4 sv = ld4_masked(srow, j, j1);
+    const float4 vv = ld4_masked(vrow, j, j1);
+    const float ss[4] = {sv.x, sv.y, sv.z, sv.w}, vs[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (ss[e] > 0.f) {                     // -inf (invalid), 0 and padding carry no mass
+        seg_s += ss[e];
+        seg_w += vs[e] > 0.f ? ss[e] / vs[e] : 0.f;   // w_hat_j = s_j / ||v_j||  (R-24)
+        jpos = j + e;
+      }
     }
   }
   if (jpos >= 0) atomicMax(&s_jlast, jpos);
@@ -150,10 +171,21 @@ __global__ void __launch_bounds__(kSmpThreads, 1) sample_decode_kernel(SampleArg
     const int m0 = s_lo[tid], m1 = s_lo[tid + 1];
     float c = off;            // cumulative mass of the segment's keys before j
     int j = j0, jl = -1;
+    // the segment is read 8 keys at a time (two float4), the next 8 prefetched
+    int cj = j0;
+    float4 a0 = ld4_masked(srow, cj, j1), a1 = ld4_masked(srow, cj + 4, j1);
+    float4 b0 = ld4_masked(srow, cj + 8, j1), b1 = ld4_masked(srow, cj + 12, j1);
     for (int m = m0; m < m1; ++m) {
       const float x = su[m] * C;
       while (j < j1) {
-        const float s = srow[j];
+        if (j >= cj + 8) {
+          cj += 8;
+          a0 = b0;
+          a1 = b1;
+          b0 = ld4_masked(srow, cj + 8, j1);
+          b1 = ld4_masked(srow, cj + 12, j1);
+        }
+        const float s = pick8(a0, a1, j - cj);
         if (s > 0.f) {
           jl = j;
           if (c + s > x) break;  // J = j; key j stays unconsumed for the next target
@@ -178,14 +210,26 @@ __global__ void __launch_bounds__(kSmpThreads, 1) sample_decode_kernel(SampleArg
     const int per = (M + kSmpWarps - 1) / kSmpWarps;
     const int mb = min(warp * per, M), me = min(mb + per, M);
     const uint16_t* vbase = a.V + ((size_t)b * a.H_kv + g) * a.N_max * kD + lane * 4;
-    for (int m = mb; m < me; ++m) {
-      const int J = sj[m];
-      const uint2 u = *reinterpret_cast<const uint2*>(vbase + (size_t)J * kD);
-      const float f = 1.0f / vrow[J];
-      acc[0] = fmaf(bf16lo(u.x), f, acc[0]);
-      acc[1] = fmaf(bf16hi(u.x), f, acc[1]);
-      acc[2] = fmaf(bf16lo(u.y), f, acc[2]);
-      acc[3] = fmaf(bf16hi(u.y), f, acc[3]);
+    constexpr int U = 8;                     // rows in flight per warp
+    for (int m0 = mb; m0 < me; m0 += U) {
+      uint2 u[U];
+      float vn[U];
+#pragma unroll
+      for (int x = 0; x < U; ++x) {
+        const int m = m0 + x;
+        const int J = m < me ? sj[m] : sj[mb];
+        u[x] = ldg_nc_v2(vbase + (size_t)J * kD);
+        vn[x] = __ldg(vrow + J);
+      }
+#pragma unroll
+      for (int x = 0; x < U; ++x) {          // accumulate in draw order
+        if (m0 + x >= me) break;
+        const float f = 1.0f / vn[x];
+        acc[0] = fmaf(bf16lo(u[x].x), f, acc[0]);
+        acc[1] = fmaf(bf16hi(u[x].x), f, acc[1]);
+        acc[2] = fmaf(bf16lo(u[x].y), f, acc[2]);
+        acc[3] = fmaf(bf16hi(u[x].y), f, acc[3]);
+      }
     }
   }
 #pragma unroll
