@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsocket_b200.so")
+LIB_PATH = os.environ.get("SOCKET_LIB_VARIANT") or os.path.join(HERE, "libsocket_b200.so")   # variant: experiments only (tools/variant_build.py)
 
 SOCKET_OK, SOCKET_EINVAL, SOCKET_EUNSUPPORTED, SOCKET_ECUDA, SOCKET_EWORKSPACE = range(5)
 GROUP_KV_SHARED, GROUP_PER_QHEAD = 0, 1

@@ -18,7 +18,10 @@ namespace sk {
 
 constexpr int kMmaWarps = 4;
 constexpr int kMmaThreads = kMmaWarps * 32;
-constexpr int kMmaStages = 3;
+#ifndef SK_DECODE_STAGES
+#define SK_DECODE_STAGES 3
+#endif
+constexpr int kMmaStages = SK_DECODE_STAGES;   // cp.async ring depth (tiles per warp)
 constexpr int kMmaRing = kMmaWarps * kMmaStages * kTileBytes;   // 96 KB
 constexpr int kMmaMaxRows = 2048;                                // rows per split (idx staging)
 
