@@ -522,25 +522,17 @@ def dense_baselines(a, cfg, q, K, V, lens, flush, stream):
 
 
 def end_to_end(a, cfg, dec, q, K, V, lens, N, flush, stream, dev):
-    """Public API with host buffers: H2D of q and of the new token's K/V rows from
-    pinned memory, the step, D2H of the output -- all inside the timed region."""
-    import torch
-    B = cfg.B
-    q_h = q.cpu().pin_memory()
-    k_new = K[:, :, N - 1].cpu().pin_memory()
-    v_new = V[:, :, N - 1].cpu().pin_memory()
-    out_h = torch.empty((B, cfg.H_q, 128), dtype=torch.bfloat16).pin_memory()
-    q_d = torch.empty_like(q)
-
-    def step():
-        q_d.copy_(q_h, non_blocking=True)
-        K[:, :, N - 1].copy_(k_new, non_blocking=True)
-        V[:, :, N - 1].copy_(v_new, non_blocking=True)
-        out, _ = dec.step(q_d, lens, append=True)
-        out_h.copy_(out, non_blocking=True)
-
-    ms = _time(step, flush, stream, a.warmup, a.steps)
-    h2d = q_h.numel() * 2 + k_new.numel() * 2 + v_new.numel() * 2
+    """Public API with host buffers (SocketDecoder.bind_host / host_step): one
+    H2D copy of q and the new token's K/V rows from pinned memory, the step
+    (which stores the new rows into the cache and hashes them) and the D2H copy
+    of the output, all inside the timed region, replayed as one CUDA graph."""
+    k_row, v_row = K[:, :, N - 1].cpu(), V[:, :, N - 1].cpu()   # before bind_host's warm-up step
+    q_h, k_h, v_h, out_h = dec.bind_host(lens)
+    q_h.copy_(q.cpu())
+    k_h.copy_(k_row)
+    v_h.copy_(v_row)
+    ms = _time(dec.host_step, flush, stream, a.warmup, a.steps)
+    h2d = q_h.numel() * 2 + k_h.numel() * 2 + v_h.numel() * 2
     return {"ms": ms, "h2d": h2d, "d2h": out_h.numel() * 2}
 
 

@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SOCKET_ABI_VERSION 1
+#define SOCKET_ABI_VERSION 2
 
 typedef enum {
   SOCKET_OK = 0,
@@ -193,15 +193,21 @@ socket_status socket_score_lut(const socket_cfg* cfg, const void* lut, const uin
 /* One whole SOCKET decode step, as one call with internal fusion:
  *   if append_last != 0: Alg. 1 on the newest key j = seq_lens[b] - 1 of every
  *     (b, kv head) (codes + vnorm; the new key is a candidate, reading R-18),
- *     in the same launch as the Alg. 2 table build;
+ *     in the same launch as the Alg. 2 table build.  If k_new / v_new are
+ *     non-NULL ([B][H_kv][d] bf16, the new token's K and V rows), the step also
+ *     stores them into K / V at row j (the caller need not write the cache);
+ *     otherwise the caller has written row j already;
  *   then scores (Eq. 4 / Alg. 4, written to `scores`), TopK with sink/window
  *   (idx, cnt as socket_topk) and sparse attention (out, lse as
- *   socket_sparse_decode), chained with programmatic dependent launch.
- * Requires L <= 64.  ws: socket_workspace_bytes(cfg, SOCKET_OP_DECODE_STEP, k). */
-socket_status socket_decode_step(const socket_cfg* cfg, const void* q, const void* K,
-                                 const void* V, const void* W, uint8_t* codes, float* vnorm,
+ *   socket_sparse_decode).  Up to 8 selection rows (KV_SHARED, P <= 8) run as
+ *   one cluster launch; otherwise 4 launches chained with programmatic
+ *   dependent launch.  Requires L <= 64 and P <= 8.
+ *   ws: socket_workspace_bytes(cfg, SOCKET_OP_DECODE_STEP, k). */
+socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, void* V,
+                                 const void* W, uint8_t* codes, float* vnorm,
                                  const int32_t* seq_lens, const uint8_t* mask,
-                                 int32_t append_last, int32_t k, int32_t sink, int32_t window,
+                                 int32_t append_last, const void* k_new, const void* v_new,
+                                 int32_t k, int32_t sink, int32_t window,
                                  float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
                                  void* ws, size_t ws_bytes, void* stream);
 

@@ -72,8 +72,8 @@ def lib():
         "socket_topk_resolve": (i32, [cfgp, P, P, i32, i32, i32, P, P, P, ctypes.c_size_t, P]),
         "socket_build_lut": (i32, [cfgp, P, P, P, ctypes.c_size_t, P]),
         "socket_score_lut": (i32, [cfgp, P, P, P, P, P, P, P]),
-        "socket_decode_step": (i32, [cfgp, P, P, P, P, P, P, P, P, i32, i32, i32, i32, P, P, P, P,
-                                     P, P, ctypes.c_size_t, P]),
+        "socket_decode_step": (i32, [cfgp, P, P, P, P, P, P, P, P, i32, P, P, i32, i32, i32, P, P,
+                                     P, P, P, P, ctypes.c_size_t, P]),
         "socket_sample_decode": (i32, [cfgp, P, P, P, P, P, i32, P, P, P]),
         "socket_last_error": (ctypes.c_char_p, []),
         "socket_version": (i32, []),

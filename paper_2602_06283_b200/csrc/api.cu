@@ -172,10 +172,11 @@ socket_status socket_score_lut(const socket_cfg* cfg, const void* lut, const uin
                       S(stream));
 }
 
-socket_status socket_decode_step(const socket_cfg* cfg, const void* q, const void* K,
-                                 const void* V, const void* W, uint8_t* codes, float* vnorm,
+socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, void* V,
+                                 const void* W, uint8_t* codes, float* vnorm,
                                  const int32_t* seq_lens, const uint8_t* mask,
-                                 int32_t append_last, int32_t k, int32_t sink, int32_t window,
+                                 int32_t append_last, const void* k_new, const void* v_new,
+                                 int32_t k, int32_t sink, int32_t window,
                                  float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
                                  void* ws, size_t ws_bytes, void* stream) {
   SK_CHECK(validate(cfg));
@@ -191,13 +192,16 @@ socket_status socket_decode_step(const socket_cfg* cfg, const void* q, const voi
   SK_NONNULL(cnt);
   SK_NONNULL(out);
   SK_NONNULL(ws);
+  if ((k_new == nullptr) != (v_new == nullptr)) return fail(SOCKET_EINVAL, "k_new and v_new must both be set or both NULL");
+  if (k_new && !append_last) return fail(SOCKET_EINVAL, "k_new / v_new need append_last");
   if (k <= 0) return fail(SOCKET_EINVAL, "k must be >= 1");
   if (k > cfg->N_max) return fail(SOCKET_EINVAL, "k > N_max");
   if (sink < 0 || window < 0 || (long long)sink + window > k)
     return fail(SOCKET_EINVAL, "need 0 <= sink, window and sink + window <= k");
   if (cfg->B == 0 || cfg->N_max == 0) return SOCKET_OK;
-  return launch_decode_step(*cfg, q, K, V, W, codes, vnorm, seq_lens, mask, append_last != 0, k,
-                            sink, window, scores, idx, cnt, out, lse, ws, ws_bytes, S(stream));
+  return launch_decode_step(*cfg, q, K, V, W, codes, vnorm, seq_lens, mask, append_last != 0,
+                            k_new, v_new, k, sink, window, scores, idx, cnt, out, lse, ws, ws_bytes,
+                            S(stream));
 }
 
 socket_status socket_topk(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,

@@ -58,8 +58,10 @@ constexpr int kFQs = 8;     // staged q row stride (doubles): [t][h]
 
 struct FusedArgs {
   const uint16_t* q;
-  const uint16_t* K;
-  const uint16_t* V;
+  uint16_t* K;            // written at row seq_lens[b] - 1 when k_new is set
+  uint16_t* V;
+  const uint16_t* k_new;  // [B][H_kv][d] new rows, or null (already in the cache)
+  const uint16_t* v_new;
   const uint16_t* W;
   uint8_t* codes;
   float* vnorm;
@@ -132,7 +134,20 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
       }
     }
     const bool app = a.do_append && n > 0;
-    if (app && tid < kD) s_ks[tid] = bf16lo((uint32_t)a.K[(((size_t)b * a.H_kv + g) * a.N_max + n - 1) * kD + tid]);
+    if (app && tid < kD) {
+      const size_t crow = (((size_t)b * a.H_kv + g) * a.N_max + n - 1) * kD;
+      if (a.k_new) {   // the new rows come from k_new / v_new; CTA 0 stores them in the cache
+        const size_t nrow = ((size_t)b * a.H_kv + g) * kD;
+        const uint16_t kv = a.k_new[nrow + tid];
+        s_ks[tid] = bf16lo((uint32_t)kv);
+        if (c == 0) {
+          a.K[crow + tid] = kv;
+          a.V[crow + tid] = a.v_new[nrow + tid];
+        }
+      } else {
+        s_ks[tid] = bf16lo((uint32_t)a.K[crow + tid]);
+      }
+    }
     __syncthreads();
     FU_STAMP(1);
     // x[h][w] = q_h . W_w in fp64 on the tensor cores: warp w8 owns W rows 8 w8 .. + 7
@@ -210,7 +225,8 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
       a.codes[((size_t)b * a.H_kv + g) * a.N_max * LP + code_off(j, s, LP)] = (uint8_t)code;
     }
     if (app && c == 0 && warp == 0) {   // ||v_j|| of the newest key (vnorm_kernel's order)
-      const uint2 u = *reinterpret_cast<const uint2*>(a.V + (((size_t)b * a.H_kv + g) * a.N_max + n - 1) * kD + lane * 4);
+      const uint2 u = a.v_new ? *reinterpret_cast<const uint2*>(a.v_new + ((size_t)b * a.H_kv + g) * kD + lane * 4)
+                              : *reinterpret_cast<const uint2*>(a.V + (((size_t)b * a.H_kv + g) * a.N_max + n - 1) * kD + lane * 4);
       float va = bf16lo(u.x), vb = bf16hi(u.x), vc = bf16lo(u.y), vd = bf16hi(u.y);
       float sq = fmaf(va, va, fmaf(vb, vb, fmaf(vc, vc, vd * vd)));
 #pragma unroll
@@ -573,9 +589,10 @@ bool fused_step_applies(const socket_cfg& c) {
   return fused_geometry(c, CS, S);
 }
 
-socket_status launch_fused_step(const socket_cfg& c, const void* q, const void* K, const void* V,
+socket_status launch_fused_step(const socket_cfg& c, const void* q, void* K, void* V,
                                 const void* W, uint8_t* codes, float* vnorm, const int32_t* seq_lens,
-                                const uint8_t* mask, int do_append, int k, int sink, int window,
+                                const uint8_t* mask, int do_append, const void* k_new,
+                                const void* v_new, int k, int sink, int window,
                                 float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
                                 cudaStream_t st) {
   int CS, S;
@@ -583,8 +600,10 @@ socket_status launch_fused_step(const socket_cfg& c, const void* q, const void* 
   const int Lp = code_slots(c.L);
   FusedArgs a;
   a.q = (const uint16_t*)q;
-  a.K = (const uint16_t*)K;
-  a.V = (const uint16_t*)V;
+  a.K = (uint16_t*)K;
+  a.V = (uint16_t*)V;
+  a.k_new = (const uint16_t*)k_new;
+  a.v_new = (const uint16_t*)v_new;
   a.W = (const uint16_t*)W;
   a.codes = codes;
   a.vnorm = vnorm;

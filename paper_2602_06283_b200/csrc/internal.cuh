@@ -78,11 +78,12 @@ socket_status launch_decode(const socket_cfg& c, const void* q, const void* K, c
                             const int32_t* seq_lens, bool dense, void* out, float* lse,
                             float* partial, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t decode_step_workspace_bytes(const socket_cfg& c, int k);
-socket_status launch_decode_step(const socket_cfg& c, const void* q, const void* K, const void* V,
+socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, void* V,
                                  const void* W, uint8_t* codes, float* vnorm,
-                                 const int32_t* seq_lens, const uint8_t* mask, int do_append, int k,
-                                 int sink, int window, float* scores, int32_t* idx, int32_t* cnt,
-                                 void* out, float* lse, void* ws, size_t ws_bytes, cudaStream_t st);
+                                 const int32_t* seq_lens, const uint8_t* mask, int do_append,
+                                 const void* k_new, const void* v_new, int k, int sink, int window,
+                                 float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
+                                 void* ws, size_t ws_bytes, cudaStream_t st);
 socket_status launch_sample_decode(const socket_cfg& c, const float* scores, const float* vnorm,
                                    const void* V, const int32_t* seq_lens, const float* uniforms,
                                    int M, int32_t* samples, void* out, cudaStream_t st);

@@ -26,9 +26,10 @@ extern "C" int socket_debug_prologue_trace(unsigned long long* host, int n) {
 #endif
 
 bool fused_step_applies(const socket_cfg& c);
-socket_status launch_fused_step(const socket_cfg& c, const void* q, const void* K, const void* V,
+socket_status launch_fused_step(const socket_cfg& c, const void* q, void* K, void* V,
                                 const void* W, uint8_t* codes, float* vnorm, const int32_t* seq_lens,
-                                const uint8_t* mask, int do_append, int k, int sink, int window,
+                                const uint8_t* mask, int do_append, const void* k_new,
+                                const void* v_new, int k, int sink, int window,
                                 float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
                                 cudaStream_t st);
 socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint8_t* codes,
@@ -79,12 +80,12 @@ size_t decode_step_workspace_bytes(const socket_cfg& c, int k) {
   return lut + decode_workspace_bytes(c, k, false);
 }
 
-socket_status launch_decode_step(const socket_cfg& c, const void* q, const void* K, const void* V,
+socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, void* V,
                                  const void* W, uint8_t* codes, float* vnorm,
-                                 const int32_t* seq_lens, const uint8_t* mask, int do_append, int k,
-                                 int sink, int window, float* scores, int32_t* idx, int32_t* cnt,
-                                 void* out, float* lse, void* ws, size_t ws_bytes,
-                                 cudaStream_t st) {
+                                 const int32_t* seq_lens, const uint8_t* mask, int do_append,
+                                 const void* k_new, const void* v_new, int k, int sink, int window,
+                                 float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
+                                 void* ws, size_t ws_bytes, cudaStream_t st) {
   const int Lp = code_slots(c.L);
   if (Lp > 64) return fail(SOCKET_EUNSUPPORTED, "decode step: L > 64 not supported");
   if (c.P > 8) return fail(SOCKET_EUNSUPPORTED, "decode step: P > 8 runs stage by stage");
@@ -97,8 +98,8 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, const void*
     return fail(SOCKET_EWORKSPACE, "decode step: workspace too small");
   // small batch (one cluster per selection row fits one wave): one fused launch
   if (fused_step_applies(c))
-    return launch_fused_step(c, q, K, V, W, codes, vnorm, seq_lens, mask, do_append, k, sink, window,
-                             scores, idx, cnt, out, lse, st);
+    return launch_fused_step(c, q, K, V, W, codes, vnorm, seq_lens, mask, do_append, k_new, v_new, k,
+                             sink, window, scores, idx, cnt, out, lse, st);
   float* lut = static_cast<float*>(ws);
   void* dws = static_cast<char*>(ws) + lut_bytes;
   const size_t dws_bytes = ws_bytes - lut_bytes;
@@ -115,6 +116,10 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, const void*
   pa.lut = lut;
   pa.K = (const uint16_t*)K;
   pa.V = (const uint16_t*)V;
+  pa.k_new = (const uint16_t*)k_new;
+  pa.v_new = (const uint16_t*)v_new;
+  pa.K_w = (uint16_t*)K;
+  pa.V_w = (uint16_t*)V;
   pa.codes = codes;
   pa.vnorm = vnorm;
   pa.seq_lens = seq_lens;

@@ -82,6 +82,10 @@ struct ProArgs {
   float* lut;             // LUT images [B*H_sel][panels][256][64] or null
   const uint16_t* K;
   const uint16_t* V;      // null: no norms
+  const uint16_t* k_new;  // decode step: the new rows [B*H_kv][d] (append_last), or null --
+  const uint16_t* v_new;  //   then the tiles read them here and store them into K_w / V_w
+  uint16_t* K_w;
+  uint16_t* V_w;
   uint8_t* codes;
   float* vnorm;
   const int32_t* seq_lens;
@@ -362,7 +366,18 @@ __device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, ch
   for (int k = 0; k < 2; ++k) {   // stage keys: 32 rows x 16 uint4
     const int e = tid + k * kPT, m = e & 31, c = e >> 5;
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (kj[m] >= 0) v = __ldg(reinterpret_cast<const uint4*>(a.K + ((size_t)kbh[m] * a.N_max + kj[m]) * kD) + c);
+    if (kj[m] >= 0) {
+      if (a.k_new) {   // the new row comes from k_new; the first table tile also fills the cache
+        v = __ldg(reinterpret_cast<const uint4*>(a.k_new + (size_t)kbh[m] * kD) + c);
+        if (wt == 0) {
+          reinterpret_cast<uint4*>(a.K_w + ((size_t)kbh[m] * a.N_max + kj[m]) * kD)[c] = v;
+          reinterpret_cast<uint4*>(a.V_w + ((size_t)kbh[m] * a.N_max + kj[m]) * kD)[c] =
+              __ldg(reinterpret_cast<const uint4*>(a.v_new + (size_t)kbh[m] * kD) + c);
+        }
+      } else {
+        v = __ldg(reinterpret_cast<const uint4*>(a.K + ((size_t)kbh[m] * a.N_max + kj[m]) * kD) + c);
+      }
+    }
     const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int e2 = 0; e2 < 8; ++e2)
@@ -421,7 +436,8 @@ __device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, ch
     for (int r = 0; r < 4; ++r) {
       const int m = warp * 4 + r, j = kj[m];
       if (j < 0) continue;
-      const uint2 u = *reinterpret_cast<const uint2*>(a.V + ((size_t)kbh[m] * a.N_max + j) * kD + lane * 4);
+      const uint2 u = a.v_new ? *reinterpret_cast<const uint2*>(a.v_new + (size_t)kbh[m] * kD + lane * 4)
+                              : *reinterpret_cast<const uint2*>(a.V + ((size_t)kbh[m] * a.N_max + j) * kD + lane * 4);
       float va = bf16lo(u.x), vb = bf16hi(u.x), vc = bf16lo(u.y), vd = bf16hi(u.y);
       float sq = fmaf(va, va, fmaf(vb, vb, fmaf(vc, vc, vd * vd)));
 #pragma unroll

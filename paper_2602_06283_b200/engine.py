@@ -49,16 +49,23 @@ class SocketDecoder:
                       n_begin=0, n_count=n)
 
     # --- one decode step --------------------------------------------------------
-    def step(self, q: torch.Tensor, seq_lens: torch.Tensor, append: bool = False, mask=None):
+    def step(self, q: torch.Tensor, seq_lens: torch.Tensor, append: bool = False, mask=None,
+             k_new=None, v_new=None):
         """One decode step.  append=True first hashes the newest key of every
-        sequence (position seq_lens[b] - 1; the caller has written its K/V row).
-        Uses the fused socket_decode_step (one library call, 4 launches)."""
+        sequence (position seq_lens[b] - 1): its K/V rows are either already in
+        the cache, or passed as k_new / v_new ([B][H_kv][d]) and stored by the
+        step itself.  Uses socket_decode_step (one library call)."""
         if not self.fused:
+            if k_new is not None:
+                n = seq_lens.long() - 1
+                bi = torch.arange(self.cfg.B, device=self.device)
+                self.K[bi, :, n] = k_new
+                self.V[bi, :, n] = v_new
             return self.step_unfused(q, seq_lens, append, mask)
         ops.decode_step(self.cfg, q, self.K, self.V, self.W, self.codes, self.vnorm, seq_lens,
                         self.k, append=append, sink=self.sink, window=self.window, mask=mask,
                         scores=self.scores, idx=self.idx, cnt=self.cnt, out=self.out, lse=self.lse,
-                        ws=self.ws_step)
+                        ws=self.ws_step, k_new=k_new, v_new=v_new)
         return self.out, self.lse
 
     def step_unfused(self, q, seq_lens, append: bool = False, mask=None):
@@ -96,3 +103,48 @@ class SocketDecoder:
     def replay(self):
         self.graph.replay()
         return self.out, self.lse
+
+    # --- host I/O: pinned host inputs -> step -> pinned host output -------------
+    def bind_host(self, seq_lens: torch.Tensor):
+        """Allocate pinned host I/O buffers for host_step(): q [B][H_q][d] and the
+        new token's K and V rows [B][H_kv][d] packed in one pinned input buffer,
+        and a pinned output [B][H_q][d].  host_step() issues one H2D copy of the
+        inputs, the decode step as a CUDA graph (it stores the new rows into the
+        cache at seq_lens[b] - 1 and hashes them) and one D2H copy of the output.
+        (Memcpy nodes from pinned host memory inside the graph cost ~50 us of
+        launch latency per replay on this driver, so the copies stay outside.)
+        Returns the pinned views (q_in, k_in, v_in, out)."""
+        cfg, dev = self.cfg, self.device
+        nq = cfg.B * cfg.H_q * cfg.d
+        nk = cfg.B * cfg.H_kv * cfg.d
+        self._in_h = torch.empty(nq + 2 * nk, dtype=torch.bfloat16).pin_memory()
+        self._in_d = torch.empty(nq + 2 * nk, dtype=torch.bfloat16, device=dev)
+        out_h = torch.empty((cfg.B, cfg.H_q, cfg.d), dtype=torch.bfloat16).pin_memory()
+        views = lambda t: (t[:nq].view(cfg.B, cfg.H_q, cfg.d), t[nq:nq + nk].view(cfg.B, cfg.H_kv, cfg.d),
+                           t[nq + nk:].view(cfg.B, cfg.H_kv, cfg.d))
+        q_d, k_d, v_d = views(self._in_d)
+        self._in_h.zero_()
+        self._in_d.zero_()
+
+        def body():
+            self.step(q_d, seq_lens, append=True, k_new=k_d, v_new=v_d)
+
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            body()
+        torch.cuda.current_stream(dev).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            body()
+        self.graph_host = g
+        self._host = (*views(self._in_h), out_h)
+        return self._host
+
+    def host_step(self):
+        """One step from the pinned inputs of bind_host() to its pinned output
+        (asynchronous on the current stream)."""
+        self._in_d.copy_(self._in_h, non_blocking=True)
+        self.graph_host.replay()
+        self._host[3].copy_(self.out, non_blocking=True)
+        return self._host[3]

@@ -175,9 +175,13 @@ def score_lut(cfg: Config, lut, codes, vnorm, seq_lens, mask=None, out=None):
 
 def decode_step(cfg: Config, q, K, V, W, codes, vnorm, seq_lens, k: int, append: bool = True,
                 sink: int = 0, window: int = 0, mask=None, scores=None, idx=None, cnt=None,
-                out=None, lse=None, ws=None):
+                out=None, lse=None, ws=None, k_new=None, v_new=None):
     """One fused decode step (append-hash of key seq_lens[b]-1, tables, scores,
-    top-k, sparse decode) -- socket_decode_step."""
+    top-k, sparse decode) -- socket_decode_step.  With k_new / v_new
+    ([B][H_kv][d] bf16) the step also stores the new token's rows into K / V."""
+    if k_new is not None:
+        _need(k_new, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.d), "k_new")
+        _need(v_new, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.d), "v_new")
     dev = q.device
     if scores is None:
         scores = torch.empty((cfg.B, cfg.H_sel, cfg.N_max), dtype=torch.float32, device=dev)
@@ -193,7 +197,8 @@ def decode_step(cfg: Config, q, K, V, W, codes, vnorm, seq_lens, k: int, append:
         ws = workspace(cfg, _lib.OP_DECODE_STEP, k, dev)
     c = cfg.c()
     check(lib().socket_decode_step(ctypes.byref(c), _p(q), _p(K), _p(V), _p(W), _p(codes), _p(vnorm),
-                                   _p(seq_lens), _p(mask), int(bool(append)), k, sink, window,
+                                   _p(seq_lens), _p(mask), int(bool(append)), _p(k_new), _p(v_new),
+                                   k, sink, window,
                                    _p(scores), _p(idx), _p(cnt), _p(out), _p(lse), _p(ws),
                                    ws.numel(), _stream(q)))
     return out, lse

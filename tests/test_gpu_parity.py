@@ -485,3 +485,51 @@ def test_decode_step_ragged_sink_window_mask_vs_oracle(one_launch, monkeypatch):
             for h in range(r * 4, r * 4 + 4):
                 y, _ = O.sparse_attention(q[b, h], K[b, r], V[b, r], S, cfg.scale)
                 assert np.max(np.abs(out[b, h].float().cpu().numpy() - y)) <= 2e-3
+
+
+@pytest.mark.parametrize("one_launch", [True, False])
+def test_decode_step_with_new_rows(one_launch, monkeypatch):
+    """socket_decode_step(k_new, v_new) stores the new token's rows into the
+    cache at seq_lens[b] - 1 and gives exactly the result of writing them first."""
+    if not one_launch:
+        monkeypatch.setenv("SOCKET_NO_FUSED", "1")
+    lens = [2048, 1500]
+    cfg, c, W, d = make(2, 8, 2, 2048, 60, 8, seed=51, seq_lens=lens)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    k_new = torch.randn((2, 2, 128), generator=g, device=DEV).to(torch.bfloat16)
+    v_new = torch.randn((2, 2, 128), generator=g, device=DEV).to(torch.bfloat16)
+    Ka, Va = d["K"].clone(), d["V"].clone()
+    Kb, Vb = d["K"].clone(), d["V"].clone()
+    for b in range(2):
+        Kb[b, :, lens[b] - 1] = k_new[b]
+        Vb[b, :, lens[b] - 1] = v_new[b]
+    a = SocketDecoder(cfg, d["W"], Ka, Va, k=300)
+    bb = SocketDecoder(cfg, d["W"], Kb, Vb, k=300)
+    a.prefill()
+    bb.prefill()
+    oa, la = [t.clone() for t in a.step(d["q"], d["seq_lens"], append=True, k_new=k_new, v_new=v_new)]
+    ob, lb = [t.clone() for t in bb.step(d["q"], d["seq_lens"], append=True)]
+    assert torch.equal(Ka, Kb) and torch.equal(Va, Vb)
+    assert torch.equal(a.codes, bb.codes) and torch.equal(a.vnorm, bb.vnorm)
+    assert torch.equal(a.idx, bb.idx) and torch.equal(oa, ob) and torch.equal(la, lb)
+
+
+def test_host_step_graph_matches_device_step():
+    """bind_host / host_step (H2D inputs + step + D2H output in one CUDA graph)
+    gives the device step's output in pinned host memory."""
+    cfg, c, W, d = make(4, 8, 2, 2048, 60, 8, seed=53)
+    K2, V2 = d["K"].clone(), d["V"].clone()
+    a = SocketDecoder(cfg, d["W"], d["K"], d["V"], k=256)
+    a.prefill()
+    b = SocketDecoder(cfg, d["W"], K2, V2, k=256)
+    b.prefill()
+    n = 2048
+    k_row, v_row = K2[:, :, n - 1].cpu(), V2[:, :, n - 1].cpu()   # bind_host's warm-up rewrites a's
+    q_h, k_h, v_h, out_h = a.bind_host(d["seq_lens"])
+    q_h.copy_(d["q"].cpu())
+    k_h.copy_(k_row)
+    v_h.copy_(v_row)
+    a.host_step()
+    torch.cuda.synchronize()
+    ob, _ = b.step(d["q"], d["seq_lens"], append=True)
+    assert torch.equal(out_h, ob.cpu())
