@@ -445,7 +445,7 @@ def test_decode_step_fused_matches_unfused():
     assert torch.equal(a.scores, b.scores)
     assert torch.equal(a.idx, b.idx) and torch.equal(a.cnt, b.cnt)
     assert (oa.float() - ob.float()).abs().max().item() <= 2e-3
-    assert ((la - lb).abs() <= 1e-4 + 2e-5 * lb.abs()).all()
+    assert ((la - lb).abs() <= 1e-3).all()
 
 
 @pytest.mark.parametrize("one_launch", [True, False])
@@ -533,3 +533,37 @@ def test_host_step_graph_matches_device_step():
     torch.cuda.synchronize()
     ob, _ = b.step(d["q"], d["seq_lens"], append=True)
     assert torch.equal(out_h, ob.cpu())
+
+
+@pytest.mark.parametrize("B,H_q,H_kv,N,L,lens,scoring,sink,window", [
+    (1, 1, 1, 4096, 16, [4096], 0, 0, 0),          # configs[0], NH = 1, Lp = 16 (replicated LUT columns)
+    (1, 8, 1, 2048, 8, [1000], 0, 0, 0),           # NH = 8, Lp = 8
+    (2, 8, 2, 1024, 33, [1024, 0], 0, 2, 8),       # empty sequence, sink/window, Lp = 64
+    (1, 4, 2, 8192, 60, [8190], 1, 0, 0),          # hard-LSH tables, n not a multiple of 32
+    (4, 8, 2, 2048, 60, [2048, 1, 700, 2047], 0, 0, 4),
+])
+def test_one_launch_step_matches_chained(B, H_q, H_kv, N, L, lens, scoring, sink, window, monkeypatch):
+    """The one-launch cluster step and the PDL-chained kernels agree on every
+    output: codes, norms, scores and the selection bit for bit, attention to
+    fp32 / bf16 rounding."""
+    import dataclasses
+    cfg, c, W, d = make(B, H_q, H_kv, N, L, 8, seed=61 + L, seq_lens=lens)
+    cfg = dataclasses.replace(cfg, scoring=scoring)
+    k = max(sink + window, min(N // 8, 512))
+    res = []
+    for no_fused in (False, True):
+        if no_fused:
+            monkeypatch.setenv("SOCKET_NO_FUSED", "1")
+        dec = SocketDecoder(cfg, d["W"], d["K"].clone(), d["V"].clone(), k=k, sink=sink, window=window)
+        dec.prefill()
+        out, lse = dec.step(d["q"], d["seq_lens"], append=True)
+        res.append([t.clone() for t in (dec.codes, dec.vnorm, dec.scores, dec.idx, dec.cnt, out, lse)])
+    a, b = res
+    for x, y in zip(a[:5], b[:5]):
+        assert torch.equal(x, y)
+    assert (a[5].float() - b[5].float()).abs().max().item() <= 2e-3
+    fin = torch.isfinite(b[6])
+    assert torch.equal(torch.isfinite(a[6]), fin)
+    # the attention weights are rounded to bf16 per tile relative to the running
+    # max, which depends on the split: lse agrees within the 1e-3 bar of DESIGN 5
+    assert ((a[6][fin] - b[6][fin]).abs() <= 1e-3).all()
