@@ -399,7 +399,7 @@ def next_rows(a, cfg, dec, q, K, V, W, lens, k, flush, stream, dev, hbm):
     flushed before every step, CUDA events on the launching stream):
       hard_lsh  (f3): the fused step with Eq. 3 hard-LSH tables (scoring = 1);
       wide_codes(f2): the RULER setting L = 60, P = 10 (600 bits/token, uint16
-                      codes), stage by stage; its score kernel's HBM rate;
+                      codes), graph-replayed step; its score kernel's HBM rate;
       sampling  (f4): Eq. 6 sampling decode over PER_QHEAD rows, M = k draws."""
     import dataclasses
 
@@ -425,7 +425,8 @@ def next_rows(a, cfg, dec, q, K, V, W, lens, k, flush, stream, dev, hbm):
     Ww = torch.from_numpy(datagen.make_projections(4343, Lw, Pw, 128).view("int16")).to(dev).view(torch.bfloat16)
     dw = SocketDecoder(cfg_w, Ww, K, V, k=k)
     dw.prefill()
-    ms = _time(lambda: dw.step(q, lens, append=True), flush, stream, a.warmup, a.steps)
+    dw.capture(q, lens, append=True)
+    ms = _time(dw.replay, flush, stream, a.warmup, a.steps)
     lut = ops.workspace(cfg_w, _lib.OP_SCORE, 1, dev)
     ops.build_lut(cfg_w, q, Ww, lut)
     sms = _time(lambda: ops.score_lut(cfg_w, lut, dw.codes, dw.vnorm, lens, out=dw.scores),
@@ -434,7 +435,7 @@ def next_rows(a, cfg, dec, q, K, V, W, lens, k, flush, stream, dev, hbm):
     out["wide_codes"] = {"ms_per_step": round(ms, 5), "tokens_per_s": round(B / (ms * 1e-3), 1),
                          "score_ms": round(sms, 5), "score_GB/s": round(sb / (sms * 1e-3) / 1e9, 1),
                          "score_frac": round(sb / (sms * 1e-3) / 1e9 / hbm, 4),
-                         "config": "L=60, P=10 (uint16 codes, 600 bits/token), stage by stage"}
+                         "config": "L=60, P=10 (uint16 codes, 600 bits/token), graph-replayed step"}
     del dw, lut
     torch.cuda.empty_cache()
     # f4 -------------------------------------------------------------------------

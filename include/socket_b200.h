@@ -201,7 +201,7 @@ socket_status socket_score_lut(const socket_cfg* cfg, const void* lut, const uin
  *   (idx, cnt as socket_topk) and sparse attention (out, lse as
  *   socket_sparse_decode).  Up to 8 selection rows (KV_SHARED, P <= 8) run as
  *   one cluster launch; otherwise 4 launches chained with programmatic
- *   dependent launch.  Requires L <= 64 and P <= 8.
+ *   dependent launch.  Requires L <= 64.
  *   ws: socket_workspace_bytes(cfg, SOCKET_OP_DECODE_STEP, k). */
 socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, void* V,
                                  const void* W, uint8_t* codes, float* vnorm,

@@ -88,7 +88,6 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, vo
                                  void* ws, size_t ws_bytes, cudaStream_t st) {
   const int Lp = code_slots(c.L);
   if (Lp > 64) return fail(SOCKET_EUNSUPPORTED, "decode step: L > 64 not supported");
-  if (c.P > 8) return fail(SOCKET_EUNSUPPORTED, "decode step: P > 8 runs stage by stage");
   const int H_sel = num_sel_rows(c);
   const int NH = c.group_mode == SOCKET_GROUP_PER_QHEAD ? 1 : c.H_q / c.H_kv;
   if (NH != 1 && NH != 2 && NH != 4 && NH != 8)

@@ -224,6 +224,110 @@ score_wide_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ 
   }
 }
 
+// Wide codes with P <= 10 and Lp in {32, 64}: per 32-slot group (= 32 tables,
+// the rotation group), the group-summed tables T_l(r) = sum_h A_h,l(r mod 2^Pl)
+// B_h,l(r >> Pl) are materialized in shared memory ([2^P][32] fp32, <= 128 KB)
+// from the half-table image, so a lookup is one conflict-free LDS as in the
+// byte-code kernel; the CTA sweeps its keys once per group, keeping the first
+// group's partial sums in shared memory.
+template <int NH>
+__global__ void __launch_bounds__(kWideThreads, 1)
+score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ codes,
+                   const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
+                   const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
+                   int G_sel, int N_max, int Lp, int P, int E, int row_floats, long long total_tiles) {
+  extern __shared__ __align__(16) float w2[];
+  const int R = 1 << P, Pl = P / 2, RL = 1 << Pl;
+  float* tab = w2;                          // [R][32]
+  float* ast = tab + R * 32;                // [NH][RL][32] staged A half-tables of the group
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int tiles_per_row = N_max >> 5;
+  const long long tb = total_tiles * blockIdx.x / gridDim.x;
+  const long long te = total_tiles * (blockIdx.x + 1) / gridDim.x;
+  const int groups = Lp / 32;
+  const int EH = R / RL;                    // entries of the high half
+  for (long long t = tb; t < te;) {         // persistent: one row segment at a time
+    const int row = (int)(t / tiles_per_row);
+    const long long seg_end = min(te, (long long)(row + 1) * tiles_per_row);
+    const int t0 = (int)(t - (long long)row * tiles_per_row);
+    const int t1 = (int)(seg_end - (long long)row * tiles_per_row);
+    t = seg_end;
+    const int b = row / H_sel, r = row % H_sel, g = r / G_sel;
+    const int n = seq_lens[b];
+    const uint16_t* crow = codes + ((size_t)b * H_kv + g) * N_max * Lp;
+    const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
+    const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
+    float* srow = scores + (size_t)row * N_max;
+    const float* img = lut_g + (size_t)row * row_floats;
+    const int vt1 = min(t1, (n + 31) >> 5);   // tiles with valid keys
+    for (int gi = 0; gi < groups; ++gi) {
+      if (t0 >= vt1) break;
+      __syncthreads();                        // previous sweep done with tab / ast
+      for (int e = tid; e < NH * RL * 32; e += kWideThreads) {
+        const int col = e & 31, lo = (e >> 5) % RL, h = e / (32 * RL);
+        ast[e] = img[((h * 2 + 0) * E + lo) * 64 + gi * 32 + col];
+      }
+      __syncthreads();
+      for (int task = tid; task < 32 * EH; task += kWideThreads) {
+        const int col = task & 31, hi = task >> 5;
+        float bh[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) bh[h] = img[((h * 2 + 1) * E + hi) * 64 + gi * 32 + col];
+        for (int lo = 0; lo < RL; ++lo) {
+          float T = 0.f;
+#pragma unroll
+          for (int h = 0; h < NH; ++h) T = fmaf(ast[(h * RL + lo) * 32 + col], bh[h], T);
+          tab[(hi * RL + lo) * 32 + col] = T;
+        }
+      }
+      __syncthreads();
+      // sweep: lane = key, slots gi*32 .. gi*32 + 31 (two 16-element chunks); the
+      // first group's partial sum is parked in `scores` (the same thread reads it back)
+      constexpr int kU = 2;                   // tiles in flight per warp
+      for (int ti0 = t0 + warp; ti0 < vt1; ti0 += kU * (kWideThreads / 32)) {
+        uint4 w[kU][4];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int ti = ti0 + u * (kWideThreads / 32);
+          const int j = ti * 32 + lane;
+          if (ti < vt1) {
+            const uint16_t* cp = crow + code_off(j, gi * 32, Lp);
+            const uint16_t* cp2 = crow + code_off(j, gi * 32 + 16, Lp);
+            w[u][0] = ldg_nc_v4(cp);
+            w[u][1] = ldg_nc_v4(cp + 8);
+            w[u][2] = ldg_nc_v4(cp2);
+            w[u][3] = ldg_nc_v4(cp2 + 8);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int ti = ti0 + u * (kWideThreads / 32);
+          if (ti >= vt1) break;
+          const int j = ti * 32 + lane;
+          const uint32_t* wd = reinterpret_cast<const uint32_t*>(w[u]);
+          float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+          for (int sl = 0; sl < 32; ++sl) {
+            const uint32_t code = (sl & 1) ? (wd[sl >> 1] >> 16) : (wd[sl >> 1] & 0xFFFFu);
+            const float v = tab[code * 32 + ((sl + lane) & 31)];
+            if (sl & 1) acc1 += v; else acc0 += v;
+          }
+          const float accg = acc0 + acc1;
+          if (gi + 1 < groups) {
+            srow[j] = gi == 0 ? accg : srow[j] + accg;
+          } else {
+            const float tot = (groups > 1 ? srow[j] : 0.f) + accg;
+            const bool ok = j < n && (!mrow || mrow[j]);
+            srow[j] = ok ? vrow[j] * tot : -INFINITY;
+          }
+        }
+      }
+    }
+    for (int ti = max(t0, vt1) + warp; ti < t1; ti += kWideThreads / 32) srow[ti * 32 + lane] = -INFINITY;
+  }
+}
+
 static socket_status launch_score_wide(const socket_cfg& c, const float* lut, const uint8_t* codes,
                                        const float* vnorm, const int32_t* seq_lens,
                                        const uint8_t* mask, float* scores, cudaStream_t st) {
@@ -239,6 +343,19 @@ static socket_status launch_score_wide(const socket_cfg& c, const float* lut, co
   if (grid.x == 0 || grid.y == 0) return SOCKET_OK;
   const int E = wide_entries(c.P);
   const int row_floats = (int)(bytes / sizeof(float));
+  if (c.P <= 10 && Lp >= 32 && !getenv("SOCKET_WIDE_FACTORED")) {
+    // group-summed tables per 32-slot group (one LDS per lookup)
+    const int R = 1 << c.P, RL = 1 << (c.P / 2);
+    const size_t sm2 = ((size_t)R * 32 + (size_t)NH * RL * 32) * sizeof(float);
+    const long long total_tiles = (long long)c.B * H_sel * (c.N_max / 32);
+    const unsigned pgrid = (unsigned)(total_tiles < kNumSMs ? total_tiles : kNumSMs);
+#define SK_WIDE2(N)                                                                                case N:                                                                                            cudaFuncSetAttribute(score_wide2_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);     score_wide2_kernel<N><<<pgrid, kWideThreads, sm2, st>>>(                                              lut, reinterpret_cast<const uint16_t*>(codes), vnorm, seq_lens, mask, scores, H_sel, c.H_kv,         G_sel, c.N_max, Lp, c.P, E, row_floats, total_tiles); return check_launch("score_wide2_kernel");
+    switch (NH) {
+      SK_WIDE2(1) SK_WIDE2(2) SK_WIDE2(4) SK_WIDE2(8)
+      default: break;
+    }
+#undef SK_WIDE2
+  }
 #define SK_WIDE(N)                                                                             \
   case N:                                                                                      \
     cudaFuncSetAttribute(score_wide_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); \

@@ -36,7 +36,7 @@ class SocketDecoder:
         self.cnt = torch.empty((cfg.B, cfg.H_sel), dtype=torch.int32, device=dev)
         self.out = torch.empty((cfg.B, cfg.H_q, cfg.d), dtype=torch.bfloat16, device=dev)
         self.lse = torch.empty((cfg.B, cfg.H_q), dtype=torch.float32, device=dev)
-        self.fused = cfg.code_slots <= 64 and cfg.P <= 8
+        self.fused = cfg.code_slots <= 64
         self.ws_step = ops.workspace(cfg, _lib.OP_DECODE_STEP, self.k, dev) if self.fused else None
         self.ws_score = ops.workspace(cfg, _lib.OP_SCORE, 1, dev)
         self.ws_dec = ops.workspace(cfg, _lib.OP_SPARSE_DECODE, self.k, dev)

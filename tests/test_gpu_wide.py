@@ -90,7 +90,8 @@ def test_wide_tables(P, L, mode, tau):
 
 
 @pytest.mark.parametrize("P,L,mode,lens", [(10, 60, KV_SHARED, [4096, 3000]), (12, 60, PER_QHEAD, [2048, 17]),
-                                           (16, 16, PER_QHEAD, [4096, 4096]), (11, 8, KV_SHARED, [100, 4096])])
+                                           (16, 16, PER_QHEAD, [4096, 4096]), (11, 8, KV_SHARED, [100, 4096]),
+                                           (9, 33, PER_QHEAD, [4096, 1000]), (10, 20, KV_SHARED, [0, 4095])])
 def test_wide_scores(P, L, mode, lens):
     N = 4096
     cfg, c, W, d = make(2, 8, 2, N, L, P, seed=P * L, mode=mode, lens=lens)
@@ -124,11 +125,11 @@ def test_wide_unsupported_group_size():
 @pytest.mark.parametrize("mode", [KV_SHARED, PER_QHEAD])
 def test_wide_decode_step_end_to_end(mode):
     """RULER-setting step (L = 60, P = 10, 600 bits/token) through SocketDecoder
-    (stage by stage for P > 8): scores, top-k and attention vs the oracle."""
+    (socket_decode_step): scores, top-k and attention vs the oracle."""
     H_q, H_kv, N, k = 8, 2, 4096, 512
     cfg, c, W, d = make(1, H_q, H_kv, N, 60, 10, seed=41, mode=mode)
     dec = SocketDecoder(cfg, d["W"], d["K"], d["V"], k=k)
-    assert not dec.fused
+    assert dec.fused           # socket_decode_step: PDL-chained kernels with the wide score
     dec.prefill()
     out, lse = dec.step(d["q"], d["seq_lens"])
     ref = O.decode_step(c["q"], c["K"], c["V"], W, c["seq_lens"], tau=0.5, k=k, sm_scale=cfg.scale,
