@@ -297,7 +297,8 @@ def run_ours(a):
     clk = clocks.stop()
     step_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / a.steps
     step_ms = max_over_ranks(step_ms)
-    launches_per_step = 4   # fused prologue (append + tables), score, top-k, decode
+    # 1 (one-launch cluster kernel, small batch) or 4 (prologue, score, top-k, decode)
+    launches_per_step = ops.decode_step_launches(cfg)
 
     # ---- (2) per-kernel timing: each stage's call launched R times back to back
     # between two events on its stream (L2 flushed before each burst), so a

@@ -211,6 +211,11 @@ socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, 
                                  float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
                                  void* ws, size_t ws_bytes, void* stream);
 
+/* Number of kernel launches socket_decode_step issues for cfg: 1 (the
+ * one-launch cluster kernel, small batches) or 4 (PDL-chained kernels);
+ * 0 if cfg is invalid. */
+int32_t socket_decode_step_launches(const socket_cfg* cfg);
+
 /* Alg. 3 l.244 TopK with forced sink / local window: per (b, row),
  * with n = seq_lens[b] and valid = (scores != -inf) & (j < n):
  *   k_eff = min(k, #valid); forced F = valid & (j < sink | n - window <= j < n);

@@ -23,6 +23,7 @@ EXPORTS = (
     "socket_topk", "socket_sparse_decode", "socket_lse_combine", "socket_dense_decode",
     "socket_topk_resolve", "socket_last_error", "socket_version", "socket_build_lut",
     "socket_score_lut", "socket_decode_step", "socket_sample_decode",
+    "socket_decode_step_launches",
 )
 
 
@@ -75,6 +76,7 @@ def lib():
         "socket_decode_step": (i32, [cfgp, P, P, P, P, P, P, P, P, i32, P, P, i32, i32, i32, P, P,
                                      P, P, P, P, ctypes.c_size_t, P]),
         "socket_sample_decode": (i32, [cfgp, P, P, P, P, P, i32, P, P, P]),
+        "socket_decode_step_launches": (i32, [cfgp]),
         "socket_last_error": (ctypes.c_char_p, []),
         "socket_version": (i32, []),
     }

@@ -7,6 +7,8 @@
 
 namespace sk {
 
+bool fused_step_applies(const socket_cfg& c);
+
 static thread_local std::string g_last_error;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -202,6 +204,11 @@ socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, 
   return launch_decode_step(*cfg, q, K, V, W, codes, vnorm, seq_lens, mask, append_last != 0,
                             k_new, v_new, k, sink, window, scores, idx, cnt, out, lse, ws, ws_bytes,
                             S(stream));
+}
+
+int32_t socket_decode_step_launches(const socket_cfg* cfg) {
+  if (validate(cfg) != SOCKET_OK) return 0;
+  return fused_step_applies(*cfg) ? 1 : 4;
 }
 
 socket_status socket_topk(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,

@@ -50,7 +50,7 @@ class SocketDecoder:
 
     # --- one decode step --------------------------------------------------------
     def step(self, q: torch.Tensor, seq_lens: torch.Tensor, append: bool = False, mask=None,
-             k_new=None, v_new=None):
+             k_new=None, v_new=None, out=None):
         """One decode step.  append=True first hashes the newest key of every
         sequence (position seq_lens[b] - 1): its K/V rows are either already in
         the cache, or passed as k_new / v_new ([B][H_kv][d]) and stored by the
@@ -62,11 +62,12 @@ class SocketDecoder:
                 self.K[bi, :, n] = k_new
                 self.V[bi, :, n] = v_new
             return self.step_unfused(q, seq_lens, append, mask)
+        o = self.out if out is None else out
         ops.decode_step(self.cfg, q, self.K, self.V, self.W, self.codes, self.vnorm, seq_lens,
                         self.k, append=append, sink=self.sink, window=self.window, mask=mask,
-                        scores=self.scores, idx=self.idx, cnt=self.cnt, out=self.out, lse=self.lse,
+                        scores=self.scores, idx=self.idx, cnt=self.cnt, out=o, lse=self.lse,
                         ws=self.ws_step, k_new=k_new, v_new=v_new)
-        return self.out, self.lse
+        return o, self.lse
 
     def step_unfused(self, q, seq_lens, append: bool = False, mask=None):
         """Same step as separate library calls (one per stage); used for stage
@@ -109,8 +110,9 @@ class SocketDecoder:
         """Allocate pinned host I/O buffers for host_step(): q [B][H_q][d] and the
         new token's K and V rows [B][H_kv][d] packed in one pinned input buffer,
         and a pinned output [B][H_q][d].  host_step() issues one H2D copy of the
-        inputs, the decode step as a CUDA graph (it stores the new rows into the
-        cache at seq_lens[b] - 1 and hashes them) and one D2H copy of the output.
+        inputs and the decode step as a CUDA graph (it stores the new rows into the
+        cache at seq_lens[b] - 1 and hashes them, and writes the output straight
+        into the pinned, UVA-mapped host buffer -- no D2H copy).
         (Memcpy nodes from pinned host memory inside the graph cost ~50 us of
         launch latency per replay on this driver, so the copies stay outside.)
         Returns the pinned views (q_in, k_in, v_in, out)."""
@@ -126,8 +128,16 @@ class SocketDecoder:
         self._in_h.zero_()
         self._in_d.zero_()
 
+        direct = self.fused      # socket_decode_step writes `out` straight into the
+                                 # pinned (UVA-mapped) host buffer: no D2H copy
+        # the one-launch kernel (small batch) reads each input once: it reads q and
+        # the new rows straight from the mapped host buffer (no H2D copy either)
+        self._host_inputs_direct = direct and ops.decode_step_launches(cfg) == 1
+        src_q, src_k, src_v = views(self._in_h) if self._host_inputs_direct else (q_d, k_d, v_d)
+
         def body():
-            self.step(q_d, seq_lens, append=True, k_new=k_d, v_new=v_d)
+            self.step(src_q, seq_lens, append=True, k_new=src_k, v_new=src_v,
+                      out=out_h if direct else None)
 
         s = torch.cuda.Stream(dev)
         s.wait_stream(torch.cuda.current_stream(dev))
@@ -138,13 +148,16 @@ class SocketDecoder:
         with torch.cuda.graph(g):
             body()
         self.graph_host = g
+        self._host_direct = direct
         self._host = (*views(self._in_h), out_h)
         return self._host
 
     def host_step(self):
         """One step from the pinned inputs of bind_host() to its pinned output
         (asynchronous on the current stream)."""
-        self._in_d.copy_(self._in_h, non_blocking=True)
+        if not self._host_inputs_direct:
+            self._in_d.copy_(self._in_h, non_blocking=True)
         self.graph_host.replay()
-        self._host[3].copy_(self.out, non_blocking=True)
+        if not self._host_direct:
+            self._host[3].copy_(self.out, non_blocking=True)
         return self._host[3]

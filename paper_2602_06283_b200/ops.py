@@ -70,6 +70,15 @@ def _need(t, dtype, shape, name):
         raise ValueError(f"{name}: must be a contiguous CUDA tensor")
 
 
+def _need_uva(t, dtype, shape, name):
+    """Like _need, but a pinned (UVA-mapped) host tensor is accepted too: the
+    decode step may read its inputs / write its output in host memory."""
+    if t.is_cuda:
+        return _need(t, dtype, shape, name)
+    if t.dtype != dtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous() or not t.is_pinned():
+        raise ValueError(f"{name}: expected a contiguous {dtype} {tuple(shape)} CUDA or pinned host tensor")
+
+
 def workspace_bytes(cfg: Config, op: int, k: int = 1) -> int:
     c = cfg.c()
     return int(lib().socket_workspace_bytes(ctypes.byref(c), op, k))
@@ -179,10 +188,11 @@ def decode_step(cfg: Config, q, K, V, W, codes, vnorm, seq_lens, k: int, append:
     """One fused decode step (append-hash of key seq_lens[b]-1, tables, scores,
     top-k, sparse decode) -- socket_decode_step.  With k_new / v_new
     ([B][H_kv][d] bf16) the step also stores the new token's rows into K / V."""
+    _need_uva(q, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "q")
     if k_new is not None:
-        _need(k_new, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.d), "k_new")
-        _need(v_new, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.d), "v_new")
-    dev = q.device
+        _need_uva(k_new, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.d), "k_new")
+        _need_uva(v_new, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.d), "v_new")
+    dev = K.device
     if scores is None:
         scores = torch.empty((cfg.B, cfg.H_sel, cfg.N_max), dtype=torch.float32, device=dev)
     if idx is None:
@@ -200,8 +210,14 @@ def decode_step(cfg: Config, q, K, V, W, codes, vnorm, seq_lens, k: int, append:
                                    _p(seq_lens), _p(mask), int(bool(append)), _p(k_new), _p(v_new),
                                    k, sink, window,
                                    _p(scores), _p(idx), _p(cnt), _p(out), _p(lse), _p(ws),
-                                   ws.numel(), _stream(q)))
+                                   ws.numel(), _stream(K)))
     return out, lse
+
+
+def decode_step_launches(cfg: Config) -> int:
+    """Kernel launches of one socket_decode_step for cfg (1 = the one-launch cluster kernel)."""
+    c = cfg.c()
+    return int(lib().socket_decode_step_launches(ctypes.byref(c)))
 
 
 def topk(cfg: Config, scores, seq_lens, k: int, sink: int = 0, window: int = 0,

@@ -514,10 +514,11 @@ def test_decode_step_with_new_rows(one_launch, monkeypatch):
     assert torch.equal(a.idx, bb.idx) and torch.equal(oa, ob) and torch.equal(la, lb)
 
 
-def test_host_step_graph_matches_device_step():
-    """bind_host / host_step (H2D inputs + step + D2H output in one CUDA graph)
-    gives the device step's output in pinned host memory."""
-    cfg, c, W, d = make(4, 8, 2, 2048, 60, 8, seed=53)
+@pytest.mark.parametrize("B", [4, 8])   # 8 rows: one-launch kernel reading host memory; 16: chained
+def test_host_step_graph_matches_device_step(B):
+    """bind_host / host_step (pinned host inputs -> graph step -> pinned host
+    output) gives the device step's output."""
+    cfg, c, W, d = make(B, 8, 2, 2048, 60, 8, seed=53)
     K2, V2 = d["K"].clone(), d["V"].clone()
     a = SocketDecoder(cfg, d["W"], d["K"], d["V"], k=256)
     a.prefill()
