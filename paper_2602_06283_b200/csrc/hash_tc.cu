@@ -250,20 +250,11 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// Code byte of one table from its 8 projections x_0..x_7 (fp32 bit patterns):
-// bit i = (x_i >= 0) taken from the sign bit.  PRMT gathers the four sign
-// bytes of x_0..x_3 (x_4..x_7) into one word; (~w & 0x80808080) * 0x00204081
-// moves bits 7/15/23/31 to bits 28..31 without carries.  (An fp32 sum of
-// exactly -0.0 -- all products -0 -- would read as negative here; it cannot
-// occur unless all 128 products are negative zeros.)
-__device__ __forceinline__ uint32_t sign_byte(const uint32_t* v) {
-  const uint32_t a = __byte_perm(__byte_perm(v[0], v[1], 0x0073), __byte_perm(v[2], v[3], 0x0073), 0x5410);
-  const uint32_t b = __byte_perm(__byte_perm(v[4], v[5], 0x0073), __byte_perm(v[6], v[7], 0x0073), 0x5410);
-  const uint32_t lo = ((~a & 0x80808080u) * 0x00204081u) >> 28;
-  const uint32_t hi = ((~b & 0x80808080u) * 0x00204081u) >> 28;
-  return lo | (hi << 4);
-}
-
+// Sign packing (epilogue below): bit i = (x_i >= 0) is the inverted fp32 sign
+// bit.  One funnel shift per column collects 32 sign bits (column c in bit
+// 31 - c), __brev puts column c in bit c, so byte q is table q of the 32
+// columns.  (An fp32 sum of exactly -0.0 -- all products -0 -- would read as
+// negative here; it cannot occur unless all 128 products are negative zeros.)
 template <int NC>
 __global__ void __launch_bounds__(kTc2Threads, 1)
 hash_keys_tc2_kernel(const __grid_constant__ CUtensorMap tmK, const uint16_t* __restrict__ W,
@@ -395,10 +386,16 @@ hash_keys_tc2_kernel(const __grid_constant__ CUtensorMap tmK, const uint16_t* __
               : "r"(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(slot * MMA_N + col)));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           const uint32_t pmask = (1u << P) - 1u;
+          // 32 sign bits with one funnel shift per column (column c lands in bit
+          // 31 - c), inverted (bit = x >= 0) and bit-reversed: byte qq = table qq
+          uint32_t sg = 0;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) sg = __funnelshift_l(v[c], sg, 1);
+          const uint32_t bits = __brev(~sg);
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq) {
             const int l = (h * MMA_N + col) / 8 + qq;
-            uint32_t code = sign_byte(&v[qq * 8]) & pmask;       // bit i = (x_i >= 0), i < P
+            uint32_t code = (bits >> (8 * qq)) & pmask;          // bit i = (x_i >= 0), i < P
             if (l >= L) code = 0;
             const int sl = (l & ~MM) | ((l - j) & MM);           // slot of table l for key j
             stg[((r >> 5) * NCH + sl / CB) * (32 * CB) + (r & 31) * CB + (sl % CB)] = (uint8_t)code;
