@@ -372,6 +372,275 @@ static socket_status launch_score_wide(const socket_cfg& c, const float* lut, co
   return check_launch("score_wide_kernel");
 }
 
+// ----------------------------------------------------------------------------
+// score kernel, register-fed (default): lane = key, the 64 code bytes and the
+// norm of a lane's key come straight from global memory into registers with
+// 16-byte non-allocating loads, double-buffered (tile i+1 is in flight while
+// tile i is looked up).  Staging the codes through shared memory (cp.async or
+// TMA rings) costs 32 extra shared-memory wavefronts per tile on top of the 64
+// LUT lookups, and shared-memory bandwidth, not HBM, was the limit
+// (ncu / tools/micro/stream_bw.cu: LDG.128 streams reach 6.6 TB/s).
+// ----------------------------------------------------------------------------
+template <int LP>
+struct RegTile {
+  uint32_t w[LP / 4];
+  float vn;
+};
+
+template <int LP>
+__device__ __forceinline__ void load_reg_tile(RegTile<LP>& t, const uint8_t* tile_codes,
+                                              const float* tile_vn, int lane) {
+  constexpr int CB = LP < 16 ? LP : 16;
+#pragma unroll
+  for (int ch = 0; ch < LP / CB; ++ch) {
+    if constexpr (CB == 16) {
+      const uint4 v = ldg_nc_v4(tile_codes + ch * 512 + lane * 16);
+      t.w[ch * 4 + 0] = v.x; t.w[ch * 4 + 1] = v.y; t.w[ch * 4 + 2] = v.z; t.w[ch * 4 + 3] = v.w;
+    } else {
+      const uint2 v = ldg_nc_v2(tile_codes + ch * 256 + lane * 8);
+      t.w[ch * 2 + 0] = v.x; t.w[ch * 2 + 1] = v.y;
+    }
+  }
+  t.vn = __ldg(tile_vn + lane);
+}
+
+template <int LP>
+__global__ void __launch_bounds__(kScoreThreads, 1)
+score_reg_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
+                 const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
+                 const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
+                 int G_sel, int N_max, long long total_tiles) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t bar;
+  constexpr uint32_t LUT_BYTES = 256 * 64 * 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t pk[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m)
+    pk[m] = (uint32_t)(((2 * m + lane) & 31) << 2) | ((uint32_t)(((2 * m + 1 + lane) & 31) << 2) << 8);
+  const int tiles_per_row = N_max >> 5;
+  const long long t_begin = total_tiles * blockIdx.x / gridDim.x;
+  const long long t_end = total_tiles * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: LUT / codes of the predecessor
+  uint32_t phase = 0;
+  for (long long t = t_begin; t < t_end;) {
+    const int row = (int)(t / tiles_per_row);
+    const long long seg_end = min(t_end, (long long)(row + 1) * tiles_per_row);
+    const int tile0 = (int)(t - (long long)row * tiles_per_row);
+    const int tile1 = (int)(seg_end - (long long)row * tiles_per_row);
+    t = seg_end;
+    const int b = row / H_sel, r = row % H_sel, g = r / G_sel;
+    const int n = seq_lens[b];
+    const int vt1 = min(tile1, (n + 31) >> 5);
+    const bool need_lut = tile0 < vt1;
+    if (need_lut && threadIdx.x == 0) {
+      mbar_expect_tx(&bar, LUT_BYTES);
+      const char* src = reinterpret_cast<const char*>(lut_g) + (size_t)row * LUT_BYTES;
+#pragma unroll
+      for (uint32_t off = 0; off < LUT_BYTES; off += 32768) bulk_g2s(smem + off, src + off, 32768, &bar);
+    }
+    const uint8_t* crow = codes + ((size_t)b * H_kv + g) * N_max * LP;
+    const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
+    const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
+    float* srow = scores + (size_t)row * N_max;
+    // my tiles: tile0 + warp + 16 i < vt1, two per iteration with the next two in
+    // flight (4 tiles = 256 B per lane outstanding); the first two load while the
+    // LUT arrives
+    auto score_tile = [&](const RegTile<LP>& tt, int tix) {
+      uint64_t acc = 0ull;
+#pragma unroll
+      for (int s2 = 0; s2 < LP; s2 += 2) {
+        float v[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int ss = s2 + u, sl = ss & 31;
+          const uint32_t sel = (uint32_t)(4 + (sl & 1)) | ((uint32_t)(ss & 3) << 4) | 0x7600u;
+          const uint32_t addr = __byte_perm(tt.w[ss >> 2], pk[sl >> 1], sel);   // code*256 + 4 c
+          v[u] = *reinterpret_cast<const float*>(smem + ((ss & 32) ? 128 : 0) + addr);
+        }
+        const uint64_t pv = (uint64_t)__float_as_uint(v[0]) | ((uint64_t)__float_as_uint(v[1]) << 32);
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(pv));
+      }
+      const float acc0 = __uint_as_float((uint32_t)acc), acc1 = __uint_as_float((uint32_t)(acc >> 32));
+      const int j = tix * 32 + lane;
+      const bool ok = j < n && (!mrow || mrow[j]);
+      srow[j] = ok ? tt.vn * (acc0 + acc1) : -INFINITY;
+    };
+    constexpr int W = kScoreWarps;
+    int ti = tile0 + warp;
+    RegTile<LP> a0, a1, b0, b1;
+    if (ti < vt1) load_reg_tile<LP>(a0, crow + (size_t)ti * 32 * LP, vrow + ti * 32, lane);
+    if (ti + W < vt1) load_reg_tile<LP>(a1, crow + (size_t)(ti + W) * 32 * LP, vrow + (ti + W) * 32, lane);
+    if (need_lut) mbar_wait(&bar, phase);
+    for (; ti < vt1; ti += 2 * W) {
+      if (ti + 2 * W < vt1) load_reg_tile<LP>(b0, crow + (size_t)(ti + 2 * W) * 32 * LP, vrow + (ti + 2 * W) * 32, lane);
+      if (ti + 3 * W < vt1) load_reg_tile<LP>(b1, crow + (size_t)(ti + 3 * W) * 32 * LP, vrow + (ti + 3 * W) * 32, lane);
+      score_tile(a0, ti);
+      if (ti + W < vt1) score_tile(a1, ti + W);
+      a0 = b0;
+      a1 = b1;
+    }
+    for (int tz = max(tile0, vt1) + warp; tz < tile1; tz += kScoreWarps) srow[tz * 32 + lane] = -INFINITY;
+    if (need_lut) phase ^= 1;
+    __syncthreads();   // everyone done with this LUT before it is overwritten
+  }
+}
+
+// ----------------------------------------------------------------------------
+// score kernel, TMA-fed (default): the same lookups as score_kernel, but the
+// codes and norms stream through a CTA-wide ring of 16-tile chunks filled by a
+// dedicated producer warp with cp.async.bulk (TMA) + mbarriers -- a bulk-copy
+// read stream measured 7.1 TB/s on this part vs 6.6 TB/s for LDG.128
+// (tools/micro/stream_bw.cu).  Consumer warp w scores tile w of each chunk; it
+// releases the stage (empty barrier) as soon as its data is in registers.  A
+// row change reloads the row's LUT image once every consumer is done with it.
+// ----------------------------------------------------------------------------
+constexpr int kSc2Consumers = 16;
+constexpr int kSc2Threads = (kSc2Consumers + 1) * 32;   // + producer warp
+constexpr int kSc2ChunkTiles = 16;
+
+template <int LP>
+struct Sc2Geom {
+  static constexpr int TILE = LP * 32;                                  // code bytes per tile
+  static constexpr int STAGE = kSc2ChunkTiles * (TILE + 128);           // codes + norms
+  static constexpr int STAGES = (136 * 1024) / STAGE < 2 ? 2 : ((136 * 1024) / STAGE > 16 ? 16 : (136 * 1024) / STAGE);
+};
+
+template <int LP>
+__global__ void __launch_bounds__(kSc2Threads, 1)
+score_tma_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
+                 const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
+                 const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
+                 int G_sel, int N_max, long long total_tiles) {
+  using GM = Sc2Geom<LP>;
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t full[GM::STAGES], empty[GM::STAGES], lut_full, lut_free;
+  constexpr uint32_t LUT_BYTES = 256 * 64 * 4;
+  char* ring = smem + LUT_BYTES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_per_row = N_max >> 5;
+  const long long tb = total_tiles * blockIdx.x / gridDim.x;
+  const long long te = total_tiles * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < GM::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kSc2Consumers); }
+    mbar_init(&lut_full, 1);
+    mbar_init(&lut_free, kSc2Consumers);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: LUT / codes of the predecessor
+
+  if (warp == kSc2Consumers) {
+    // ---------------- producer ------------------------------------------------
+    if (lane == 0) {
+      int q = 0, gl = 0;          // chunk counter, LUT-load counter
+      for (long long t = tb; t < te;) {
+        const int row = (int)(t / tiles_per_row);
+        const long long seg_end = min(te, (long long)(row + 1) * tiles_per_row);
+        const int t0 = (int)(t - (long long)row * tiles_per_row);
+        const int t1 = (int)(seg_end - (long long)row * tiles_per_row);
+        t = seg_end;
+        const int b = row / H_sel, g = (row % H_sel) / G_sel;
+        const int vt1 = min(t1, (seq_lens[b] + 31) >> 5);
+        if (t0 >= vt1) continue;                              // no data: no LUT, no chunks
+        if (gl > 0) mbar_wait(&lut_free, (gl - 1) & 1);        // consumers done with the old LUT
+        mbar_expect_tx(&lut_full, LUT_BYTES);
+        const char* lsrc = reinterpret_cast<const char*>(lut_g) + (size_t)row * LUT_BYTES;
+        for (uint32_t off = 0; off < LUT_BYTES; off += 32768) bulk_g2s(smem + off, lsrc + off, 32768, &lut_full);
+        ++gl;
+        const uint8_t* crow = codes + ((size_t)b * H_kv + g) * N_max * LP;
+        const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
+        for (int c0 = t0; c0 < vt1; c0 += kSc2ChunkTiles, ++q) {
+          const int nt = min(kSc2ChunkTiles, vt1 - c0);
+          const int st = q % GM::STAGES;
+          mbar_wait(&empty[st], ((q / GM::STAGES) & 1) ^ 1);
+          mbar_expect_tx(&full[st], (uint32_t)nt * (GM::TILE + 128));
+          char* dst = ring + st * GM::STAGE;
+          bulk_g2s(dst, crow + (size_t)c0 * GM::TILE, (uint32_t)nt * GM::TILE, &full[st]);
+          bulk_g2s(dst + kSc2ChunkTiles * GM::TILE, vrow + c0 * 32, (uint32_t)nt * 128, &full[st]);
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumers ---------------------------------------------------
+  uint32_t pk[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m)
+    pk[m] = (uint32_t)(((2 * m + lane) & 31) << 2) | ((uint32_t)(((2 * m + 1 + lane) & 31) << 2) << 8);
+  int q = 0, gl = 0;
+  for (long long t = tb; t < te;) {
+    const int row = (int)(t / tiles_per_row);
+    const long long seg_end = min(te, (long long)(row + 1) * tiles_per_row);
+    const int t0 = (int)(t - (long long)row * tiles_per_row);
+    const int t1 = (int)(seg_end - (long long)row * tiles_per_row);
+    t = seg_end;
+    const int b = row / H_sel;
+    const int n = seq_lens[b];
+    const int vt1 = min(t1, (n + 31) >> 5);
+    const int g = (row % H_sel) / G_sel;
+    const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
+    const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
+    float* srow = scores + (size_t)row * N_max;
+    (void)vrow;
+    if (t0 < vt1) {
+      mbar_wait(&lut_full, gl & 1);
+      ++gl;
+      for (int c0 = t0; c0 < vt1; c0 += kSc2ChunkTiles, ++q) {
+        const int nt = min(kSc2ChunkTiles, vt1 - c0);
+        const int st = q % GM::STAGES;
+        mbar_wait(&full[st], (q / GM::STAGES) & 1);
+        if (warp < nt) {
+          const char* tp = ring + st * GM::STAGE + warp * GM::TILE;
+          constexpr int CB = LP < 16 ? LP : 16;
+          uint32_t w[LP / 4];
+#pragma unroll
+          for (int ch = 0; ch < LP / CB; ++ch) {
+            if constexpr (CB == 16) {
+              const uint4 v = *reinterpret_cast<const uint4*>(tp + ch * 512 + lane * 16);
+              w[ch * 4 + 0] = v.x; w[ch * 4 + 1] = v.y; w[ch * 4 + 2] = v.z; w[ch * 4 + 3] = v.w;
+            } else {
+              const uint2 v = *reinterpret_cast<const uint2*>(tp + ch * 256 + lane * 8);
+              w[ch * 2 + 0] = v.x; w[ch * 2 + 1] = v.y;
+            }
+          }
+          const float vn = *reinterpret_cast<const float*>(ring + st * GM::STAGE + kSc2ChunkTiles * GM::TILE +
+                                                           warp * 128 + lane * 4);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);          // stage data is in registers
+          uint64_t acc = 0ull;
+#pragma unroll
+          for (int s2 = 0; s2 < LP; s2 += 2) {
+            float v[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int ss = s2 + u, sl = ss & 31;
+              const uint32_t sel = (uint32_t)(4 + (sl & 1)) | ((uint32_t)(ss & 3) << 4) | 0x7600u;
+              const uint32_t addr = __byte_perm(w[ss >> 2], pk[sl >> 1], sel);   // code*256 + 4 c
+              v[u] = *reinterpret_cast<const float*>(smem + ((ss & 32) ? 128 : 0) + addr);
+            }
+            const uint64_t pv = (uint64_t)__float_as_uint(v[0]) | ((uint64_t)__float_as_uint(v[1]) << 32);
+            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(pv));
+          }
+          const float acc0 = __uint_as_float((uint32_t)acc), acc1 = __uint_as_float((uint32_t)(acc >> 32));
+          const int j = (c0 + warp) * 32 + lane;
+          const bool ok = j < n && (!mrow || mrow[j]);
+          srow[j] = ok ? vn * (acc0 + acc1) : -INFINITY;
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&lut_free);                // done with this row's LUT
+    }
+    for (int ti = max(t0, vt1) + warp; ti < t1; ti += kSc2Consumers) srow[ti * 32 + lane] = -INFINITY;
+  }
+}
+
 socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint8_t* codes,
                                const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
                                float* scores, cudaStream_t st, bool pdl) {
@@ -393,7 +662,26 @@ socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
 #define SK_SCORE_CASE(LPV)                                                                     \
-  case LPV: {                                                                                  \
+  case LPV: if (getenv("SOCKET_SCORE_TMA")) {                                                  \
+    const size_t smem2 = 256 * 64 * 4 + (size_t)Sc2Geom<LPV>::STAGES * Sc2Geom<LPV>::STAGE;     \
+    auto kfn2 = score_tma_kernel<LPV>;                                                         \
+    cudaFuncSetAttribute(kfn2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);       \
+    cfg.dynamicSmemBytes = smem2;                                                              \
+    cfg.blockDim = dim3(kSc2Threads);                                                          \
+    cudaError_t e2 = cudaLaunchKernelEx(&cfg, kfn2, lut, codes, vnorm, seq_lens, mask, scores, H_sel, \
+                                        c.H_kv, G_sel, c.N_max, total_tiles);                  \
+    if (e2 != cudaSuccess) return fail(SOCKET_ECUDA, std::string("score launch: ") + cudaGetErrorString(e2)); \
+    return check_launch("score_tma_kernel");                                                   \
+  } else if (!getenv("SOCKET_SCORE_V1")) {                                                     \
+    const size_t smem3 = 256 * 64 * 4;                                                         \
+    auto kfn3 = score_reg_kernel<LPV>;                                                         \
+    cudaFuncSetAttribute(kfn3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);       \
+    cfg.dynamicSmemBytes = smem3;                                                              \
+    cudaError_t e3 = cudaLaunchKernelEx(&cfg, kfn3, lut, codes, vnorm, seq_lens, mask, scores, H_sel, \
+                                        c.H_kv, G_sel, c.N_max, total_tiles);                  \
+    if (e3 != cudaSuccess) return fail(SOCKET_ECUDA, std::string("score launch: ") + cudaGetErrorString(e3)); \
+    return check_launch("score_reg_kernel");                                                   \
+  } else {                                                                                     \
     const size_t smem = lut_bytes_per_row(c.L) + (size_t)kScoreWarps * kScoreStages * TileStage<LPV>::BYTES; \
     auto kfn = score_kernel<LPV>;                                                              \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
