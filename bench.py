@@ -345,7 +345,7 @@ def run_ours(a):
     for s_ in ("append_hash", "tables"):
         stages[s_] = {"ms": round(stage_ms[s_], 5), "share": round(stage_ms[s_] / eager_ms, 4)}
     dom = max(("score", "sparse_decode"), key=lambda s_: stage_ms[s_])
-    kern = {"score": "score_kernel", "sparse_decode": "decode_mma_kernel"}[dom]
+    kern = {"score": "score_reg_kernel", "sparse_decode": "decode_mma_kernel"}[dom]
     roof = {"bound": "hbm", "kernel": kern, "achieved": stages[dom]["GB/s"], "peak": hbm,
             "unit": "GB/s", "frac": stages[dom]["frac"], "traffic": TRAFFIC.get(kern),
             "peak_source": peak_src}

@@ -10,7 +10,7 @@ timeout 900 python bench.py --steps 30 --warmup 5 > gpurun_out/bench_$tag.json 2
 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$tag.csv python tools/profile_step.py --steps 3 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"prologue_kernel|score_kernel|topk_cluster|decode_mma" -s 4 -c 4 \
+    -k regex:"prologue_kernel|score_reg_kernel|topk_cluster|decode_mma" -s 4 -c 4 \
     -o gpurun_out/prof_$tag python tools/profile_step.py --steps 2 > gpurun_out/ncu_$tag.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"hash_keys_tc|vnorm" -c 2 \
     -o gpurun_out/prof_prefill_$tag python tools/profile_step.py --steps 1 > gpurun_out/ncu_prefill_$tag.log 2>&1

@@ -39,7 +39,7 @@ def main(src, outdir):
     traffic = {}
     for k, v in summ.items():
         base = k.split("<")[0]
-        if base in ("score_kernel", "decode_mma_kernel", "topk_cluster_kernel", "prologue_kernel") and "dram_read" in v:
+        if base in ("score_kernel", "score_reg_kernel", "decode_mma_kernel", "topk_cluster_kernel", "prologue_kernel") and "dram_read" in v:
             traffic[base] = v["dram_read"] + v.get("dram_write", 0.0)
     json.dump(traffic, open(os.path.join(outdir, "traffic.json"), "w"), indent=1)
     for k, v in summ.items():
