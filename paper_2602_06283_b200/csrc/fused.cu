@@ -150,35 +150,50 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
     }
     __syncthreads();
     FU_STAMP(1);
-    // x[h][w] = q_h . W_w in fp64 on the tensor cores: warp w8 owns W rows 8 w8 .. + 7
-    if (warp * 8 < nw) {
+    // x[h][w] = q_h . W_w in fp64 on the tensor cores: warp w owns W rows
+    // 8 (w & 7) .. + 7 over the K half w >> 3; x = (K half 0) + (K half 1) -- the
+    // same decomposition as the chained prologue's tables tiles, so the LUTs agree
+    // bit for bit
+    {
+      const int nt8 = warp & 7, kh = warp >> 3;
       double d0 = 0.0, d1 = 0.0;
       const int kr = lane & 3, col = lane >> 2;
+      if (nt8 * 8 < nw) {
 #pragma unroll 8
-      for (int k0 = 0; k0 < kD; k0 += 4) {
-        const double av = qs[(k0 + kr) * kFQs + col];
-        const double bv = (double)ws[(k0 + kr) * kFWs + warp * 8 + col];
-        dmma_8x8x4(d0, d1, av, bv);
+        for (int k0 = kh * (kD / 2); k0 < (kh + 1) * (kD / 2); k0 += 4) {
+          const double av = qs[(k0 + kr) * kFQs + col];
+          const double bv = (double)ws[(k0 + kr) * kFWs + nt8 * 8 + col];
+          dmma_8x8x4(d0, d1, av, bv);
+        }
       }
+      __syncthreads();                                   // qs dead: partials go there
+      double* xp = qs;                                   // [kh][h 8][w 64]
+      if (nt8 * 8 < nw) {
+        xp[(kh * 8 + col) * 64 + nt8 * 8 + 2 * (lane & 3)] = d0;
+        xp[(kh * 8 + col) * 64 + nt8 * 8 + 2 * (lane & 3) + 1] = d1;
+      }
+      __syncthreads();
       const float inv_sqrt_d = 0.08838834764831845f;
+      if (kh == 0 && nt8 * 8 < nw) {
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int h = lane >> 2, w = warp * 8 + 2 * (lane & 3) + i;
-        if (h < NH && w < nw) {
-          const double x = i ? d1 : d0;
-          const int tl = w / P, bit = w - tl * P;
-          float fp, fm;
-          if (a.hard) {
-            fp = x >= 0.0 ? 1.f : 0.f;
-            fm = 1.f - fp;
-          } else {
-            const float uu = tanhf((float)x) * inv_sqrt_d;            // Alg. 2 l.217
-            const float av = 2.0f * uu / a.tau;
-            fp = 1.0f / (1.0f + expf(-av));
-            fm = 1.0f / (1.0f + expf(av));
+        for (int i = 0; i < 2; ++i) {
+          const int h = lane >> 2, w = nt8 * 8 + 2 * (lane & 3) + i;
+          if (h < NH && w < nw) {
+            const double x = xp[h * 64 + w] + xp[(8 + h) * 64 + w];
+            const int tl = w / P, bit = w - tl * P;
+            float fp, fm;
+            if (a.hard) {
+              fp = x >= 0.0 ? 1.f : 0.f;
+              fm = 1.f - fp;
+            } else {
+              const float uu = tanhf((float)x) * inv_sqrt_d;            // Alg. 2 l.217
+              const float av = 2.0f * uu / a.tau;
+              fp = 1.0f / (1.0f + expf(-av));
+              fm = 1.0f / (1.0f + expf(av));
+            }
+            s_fx[((h * 8 + bit) * 2 + 1) * 16 + tl] = fp;
+            s_fx[((h * 8 + bit) * 2 + 0) * 16 + tl] = fm;
           }
-          s_fx[((h * 8 + bit) * 2 + 1) * 16 + tl] = fp;
-          s_fx[((h * 8 + bit) * 2 + 0) * 16 + tl] = fm;
         }
       }
     }

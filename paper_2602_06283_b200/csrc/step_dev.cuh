@@ -61,7 +61,7 @@ __device__ __forceinline__ double bf16_to_f64(uint32_t h) {
 //     s = (l & ~M) | ((l - j) & M) of key j; the first table tile also writes
 //     ||v_j|| (vnorm_kernel's summation order).
 // ============================================================================
-constexpr int kPT = 256;   // threads per tile CTA
+constexpr int kPT = 512;   // threads per tile CTA (16 warps)
 constexpr int kTQ = 16;    // query vectors per tables tile
 constexpr int kTT = 8;     // tables per tile
 constexpr int kAK = 32;    // keys per append tile
@@ -198,34 +198,37 @@ __device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, ch
   PRO_STAMP(0);
   PRO_STAMP(1);
   {   // stage q (16 vectors) and W (64 rows): all loads first, then convert
-    uint4 vq, vw[4];
-    const int m = tid & 15, cq = tid >> 4;
+    constexpr int KW = 64 * 16 / kPT;          // W uint4 per thread
+    uint4 vq, vw[KW];
+    const int m = tid & 15, cq = (tid >> 4) & 15;
     vq = make_uint4(0, 0, 0, 0);
-    if (qv0 + m < nqv) vq = __ldg(reinterpret_cast<const uint4*>(a.q + (size_t)(qv0 + m) * kD) + cq);
+    if (tid < 256 && qv0 + m < nqv) vq = __ldg(reinterpret_cast<const uint4*>(a.q + (size_t)(qv0 + m) * kD) + cq);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < KW; ++k) {
       const int e = tid + k * kPT, w = e & 63, c = e >> 6;
       vw[k] = make_uint4(0, 0, 0, 0);
       if (w < nw) vw[k] = __ldg(reinterpret_cast<const uint4*>(a.W + (size_t)(l0 * P + w) * kD) + c);
     }
-    bf16x8_to_f64(vq, qs + (cq * 8) * kQS + m, kQS);
+    if (tid < 256) bf16x8_to_f64(vq, qs + (cq * 8) * kQS + m, kQS);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < KW; ++k) {
       const int e = tid + k * kPT, w = e & 63, c = e >> 6;
       bf16x8_to_f64(vw[k], ws + (c * 8) * kWS + w, kWS);
     }
   }
   __syncthreads();
   PRO_STAMP(2);
-  // X[m][w] = sum_t q_m[t] W_w[t]: warp w8 owns W rows 8 w8 .. 8 w8 + 7 for both
-  // 8-vector halves of the tile (two 8x8 fp64 accumulators), k-steps of 4
+  // X[m][w] = sum_t q_m[t] W_w[t]: warp w owns W rows 8 (w & 7) .. + 7 for both
+  // 8-vector halves of the tile (two 8x8 fp64 accumulators) over the K half
+  // w >> 3 (16 k-steps of 4); x = (K half 0) + (K half 1)
   double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+  const int nt8 = warp & 7, kh = warp >> 3;
   {
     const int kr = lane & 3, col = lane >> 2;
 #pragma unroll 8
-    for (int k0 = 0; k0 < kD; k0 += 4) {
+    for (int k0 = kh * (kD / 2); k0 < (kh + 1) * (kD / 2); k0 += 4) {
       const double* qrow = qs + (k0 + kr) * kQS;
-      const double b = ws[(k0 + kr) * kWS + warp * 8 + col];
+      const double b = ws[(k0 + kr) * kWS + nt8 * 8 + col];
       dmma_8x8x4(c00, c01, qrow[col], b);
       dmma_8x8x4(c10, c11, qrow[8 + col], b);
     }
@@ -234,22 +237,30 @@ __device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, ch
   __syncthreads();   // staging dead: the epilogue arrays reuse it
   double* fx = reinterpret_cast<double*>(smem);                         // [m][bit < 16][s][kFXS]
   float* half = reinterpret_cast<float*>(fx + kTQ * 16 * 2 * kFXS);    // [m][hi][ent][kTT]
+  double* xs = reinterpret_cast<double*>(smem + 64 * 1024);             // [kh][m 16][w 64]
   {
-    const double xv[2][2] = {{c00, c01}, {c10, c11}};
+    const int col = lane >> 2, q2 = 2 * (lane & 3);
+    xs[(kh * 16 + col) * 64 + nt8 * 8 + q2] = c00;
+    xs[(kh * 16 + col) * 64 + nt8 * 8 + q2 + 1] = c01;
+    xs[(kh * 16 + 8 + col) * 64 + nt8 * 8 + q2] = c10;
+    xs[(kh * 16 + 8 + col) * 64 + nt8 * 8 + q2 + 1] = c11;
+  }
+  __syncthreads();
+  {   // sigma factors: 1024 projections over the 512 threads
     const float inv_sqrt_d = 0.08838834764831845f;   // 1/sqrt(128), correctly rounded
 #pragma unroll
-    for (int hm = 0; hm < 2; ++hm)
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int m = hm * 8 + (lane >> 2), w = warp * 8 + 2 * (lane & 3) + i;
+    for (int u = 0; u < kTQ * 64 / kPT; ++u) {
+      const int e = tid + u * kPT, m = e >> 6, w = e & 63;
+      const double xval = xs[m * 64 + w] + xs[(16 + m) * 64 + w];
+      {
         if (w < nw) {
           const int tl = w / P, bit = w - tl * P;
           double fp, fm;
           if (a.hard) {            // Eq. 3: the product over bits is the indicator of b_q
-            fp = xv[hm][i] >= 0.0 ? 1.0 : 0.0;                      // sign(0) = +1 (R-3)
+            fp = xval >= 0.0 ? 1.0 : 0.0;                           // sign(0) = +1 (R-3)
             fm = 1.0 - fp;
           } else {
-            const float uu = tanhf((float)xv[hm][i]) * inv_sqrt_d;  // Alg. 2 l.217
+            const float uu = tanhf((float)xval) * inv_sqrt_d;       // Alg. 2 l.217
             const float av = 2.0f * uu / a.tau;                      // logit gap of bit i
             fp = (double)(1.0f / (1.0f + expf(-av)));                // c_{r,i} = +1 (bit set, R-5)
             fm = (double)(1.0f / (1.0f + expf(av)));                 // c_{r,i} = -1
@@ -258,6 +269,7 @@ __device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, ch
           fx[((m * 16 + bit) * 2 + 0) * kFXS + tl] = fm;
         }
       }
+    }
   }
   __syncthreads();
   if (P > 8) {   // wide codes (NEXT-2): per-head factor half-tables, no group sum
@@ -266,7 +278,7 @@ __device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, ch
     return;
   }
   PRO_STAMP(4);
-  {   // half tables: one (vector, table, half) per thread, 16 entries ((f0 f1) f2) f3
+  if (tid < kTQ * kTT * 2) {   // half tables: one (vector, table, half) per thread, ((f0 f1) f2) f3
     const int tl = tid & 7, hi = (tid >> 3) & 1, m = tid >> 4;
     double f[4][2];
 #pragma unroll
@@ -347,6 +359,24 @@ __device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, ch
   const int nw = (L - l0 < a.tpt ? L - l0 : a.tpt) * P;
   PRO_STAMP(0);
   PRO_STAMP(1);
+  {   // stage W first (independent of the keys): 64 rows x 16 uint4
+    constexpr int KW = 64 * 16 / kPT;
+    uint4 vw[KW];
+#pragma unroll
+    for (int k = 0; k < KW; ++k) {
+      const int e = tid + k * kPT, w = e & 63, c = e >> 6;
+      vw[k] = make_uint4(0, 0, 0, 0);
+      if (w < nw) vw[k] = __ldg(reinterpret_cast<const uint4*>(a.W + (size_t)(l0 * P + w) * kD) + c);
+    }
+#pragma unroll
+    for (int k = 0; k < KW; ++k) {
+      const int e = tid + k * kPT, w = e & 63, c = e >> 6;
+      const uint32_t w4[4] = {vw[k].x, vw[k].y, vw[k].z, vw[k].w};
+#pragma unroll
+      for (int e2 = 0; e2 < 8; ++e2)
+        ws[(c * 8 + e2) * kAWS + w] = (e2 & 1) ? bf16hi(w4[e2 >> 1]) : bf16lo(w4[e2 >> 1]);
+    }
+  }
   if (tid < kAK) {
     const int kk = at * kAK + tid;
     int j = -1, bh = 0;
@@ -363,7 +393,7 @@ __device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, ch
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {   // stage keys: 32 rows x 16 uint4
+  for (int k = 0; k < 32 * 16 / kPT; ++k) {   // stage keys: 32 rows x 16 uint4
     const int e = tid + k * kPT, m = e & 31, c = e >> 5;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (kj[m] >= 0) {
@@ -383,23 +413,14 @@ __device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, ch
     for (int e2 = 0; e2 < 8; ++e2)
       ks[(c * 8 + e2) * kKS + m] = (e2 & 1) ? bf16hi(w4[e2 >> 1]) : bf16lo(w4[e2 >> 1]);
   }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {   // stage W: 64 rows x 16 uint4
-    const int e = tid + k * kPT, w = e & 63, c = e >> 6;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (w < nw) v = __ldg(reinterpret_cast<const uint4*>(a.W + (size_t)(l0 * P + w) * kD) + c);
-    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int e2 = 0; e2 < 8; ++e2)
-      ws[(c * 8 + e2) * kAWS + w] = (e2 & 1) ? bf16hi(w4[e2 >> 1]) : bf16lo(w4[e2 >> 1]);
-  }
+
   __syncthreads();
   PRO_STAMP(2);
-  // keys 2kp, 2kp+1 x W rows 4wq .. 4wq+3
-  const int kp = tid & 15, wq = tid >> 4;
+  // keys 2kp, 2kp+1 x W rows 4wq .. 4wq+3 (threads >= 256 idle here), t ascending
+  const int kp = tid & 15, wq = (tid >> 4) & 15;
   float x[2][4] = {};
 #pragma unroll 8
-  for (int t = 0; t < kD; ++t) {
+  for (int t = 0; t < (tid < 256 ? kD : 0); ++t) {
     const float2 kv = *reinterpret_cast<const float2*>(ks + t * kKS + 2 * kp);
     const float4 wv = *reinterpret_cast<const float4*>(ws + t * kAWS + 4 * wq);
     x[0][0] = fmaf(wv.x, kv.x, x[0][0]); x[0][1] = fmaf(wv.y, kv.x, x[0][1]);
@@ -408,18 +429,20 @@ __device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, ch
     x[1][2] = fmaf(wv.z, kv.y, x[1][2]); x[1][3] = fmaf(wv.w, kv.y, x[1][3]);
   }
   PRO_STAMP(3);
+  if (tid < 256) {
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int w = 4 * wq + j;
-      bits[(2 * kp + i) * 64 + w] = (w < nw && x[i][j] >= 0.f) ? 1 : 0;   // sign(0) = +1 (R-3)
-    }
+      for (int j = 0; j < 4; ++j) {
+        const int w = 4 * wq + j;
+        bits[(2 * kp + i) * 64 + w] = (w < nw && x[i][j] >= 0.f) ? 1 : 0;   // sign(0) = +1 (R-3)
+      }
+  }
   __syncthreads();
   {   // code byte of (key m, table tl): row i -> bit i (R-4)
-    const int m = tid >> 3, tl = tid & 7;
+    const int m = (tid >> 3) & 31, tl = tid & 7;
     const int l = l0 + tl, j = kj[m];
-    if (j >= 0 && tl < a.tpt && l < a.Lp) {
+    if (tid < 256 && j >= 0 && tl < a.tpt && l < a.Lp) {
       uint32_t code = 0;
       for (int i = 0; i < P; ++i) code |= (uint32_t)bits[m * 64 + tl * P + i] << i;
       const int Lp = a.Lp;
@@ -430,7 +453,7 @@ __device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, ch
       else a.codes[o] = (uint8_t)code;
     }
   }
-  if (a.V && wt == 0) {   // ||v_j||: warp w handles keys 4w .. 4w+3
+  if (a.V && wt == 0 && tid < 256) {   // ||v_j||: warp w handles keys 4w .. 4w+3
     const int warp = tid >> 5, lane = tid & 31;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
