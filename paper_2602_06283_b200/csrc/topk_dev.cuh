@@ -337,8 +337,8 @@ __device__ __forceinline__ void topk_core(const TopkArgs& a, uint32_t* keys, Top
       __syncthreads();
       // T = the need2-th largest candidate, above = candidates > T
       uint32_t above;
-      if (C <= 1024u) {
-        // rank counting: candidate i is T iff #greater < need2 <= #greater + #equal
+      if (C <= 192u) {
+        // rank counting (O(C^2), small C): candidate i is T iff #greater < need2 <= #greater + #equal
         for (int i = tid; i < (int)C; i += kTopkThreads) {
           const uint32_t me = S.gcand[i];
           uint32_t gt = 0, eq = 0;

@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--batch", type=int, nargs="+", default=[1, 4, 16])
     ap.add_argument("--ctx", type=int, default=32768)
     ap.add_argument("--sparsity", type=float, default=10.0)
+    ap.add_argument("--hard", action="store_true")
     a = ap.parse_args()
     libpath = build_trace()
     from paper_2602_06283_b200 import _lib
@@ -57,7 +58,7 @@ def main():
         k = int(round(N / a.sparsity))
         q, K, V = datagen.torch_make_cache(bsz, 32, 8, N, 128, seed=1)
         W = torch.from_numpy(datagen.make_projections(4242, 60, 8, 128).view("int16")).cuda().view(torch.bfloat16)
-        cfg = Config(B=bsz, H_q=32, H_kv=8, N_max=N, L=60, P=8, tau=0.5)
+        cfg = Config(B=bsz, H_q=32, H_kv=8, N_max=N, L=60, P=8, tau=0.5, scoring=int(a.hard))
         lens = torch.full((bsz,), N, dtype=torch.int32, device="cuda")
         dec = SocketDecoder(cfg, W, K, V, k=k)
         dec.prefill()
