@@ -9,23 +9,46 @@
 // with the M uniforms u_m in [0, 1) supplied by the caller (the random numbers
 // the method draws are inputs, so the CPU oracle can replay them).
 //
-// One 1024-thread CTA per row:
-//   1. sort (u_m, m) ascending in shared memory (bitonic);
-//   2. thread t owns the contiguous key segment [t S, (t+1) S): segment sums of
-//      s and of w_hat = s / ||v|| (fp32, j ascending), a deterministic block
-//      scan gives the segment offsets off_t and the totals C = C_n, Z = sum w_hat;
-//   3. thread t takes the sorted targets x_m = u_m C in [off_t, off_{t+1}) and
-//      walks its segment once (two pointers): J_m = first j with off_t + prefix > x_m;
-//   4. the CTA gathers v_J / ||v_J|| (warps over contiguous sorted samples,
-//      lanes over 4 dims), reduces across warps in warp order and writes
-//      T = (C / Z) / M * sum, rounded to bf16.
+// One 256-thread CTA per row, 4 CTAs per SM (the whole batch is one wave):
+//   1. the row's keys split into kSub = 4096 sub-blocks of S keys (S = 8 at 32K);
+//      lane pairs sum s and w_hat = s / ||v|| per sub-block with float4 loads; a
+//      block scan turns the sums into sub-block offsets off_t and the totals
+//      C = C_n, Z = sum w_hat;
+//   2. every draw (3 per thread in flight): binary search for the sub-block with
+//      the largest off_t <= x_m = u_m C, then walk its S keys, J_m = first j with
+//      off_t + prefix > x_m -- no sort of the uniforms, every draw costs one
+//      short walk however the mass is spread; J into shared memory;
+//   3. each warp gathers v_J / ||v_J|| for a contiguous run of draws (half-warp
+//      per row, 16-B loads, 16 rows in flight), the CTA reduces across warps in
+//      warp order and writes T = (C / Z) / M * sum, rounded to bf16.
+// fp32 throughout; offsets and the walk are deterministic (no atomics on sums).
 #include "internal.cuh"
 
 namespace sk {
 
-constexpr int kSmpThreads = 1024;
+#ifdef SK_TRACE
+static __device__ unsigned long long g_smp_trace[1024 * 8];
+#define SM_STAMP(i)                                                                        \
+  do {                                                                                     \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_smp_trace[blockIdx.x * 8 + (i)] = clock64(); \
+  } while (0)
+extern "C" int socket_debug_sample_trace(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_smp_trace, (size_t)n * sizeof(unsigned long long));
+}
+#else
+#define SM_STAMP(i) \
+  do {              \
+  } while (0)
+#endif
+
+constexpr int kSmpThreads = 256;
 constexpr int kSmpWarps = kSmpThreads / 32;
 constexpr int kSmpMaxM = 8192;
+constexpr int kSub = 4096;          // CDF sub-blocks per row (the binary-search grid)
+#ifndef SK_SMP_U
+#define SK_SMP_U 16
+#endif
+constexpr int kSmpU = SK_SMP_U;     // V rows in flight per warp in the gather
 
 struct SampleArgs {
   const float* scores;    // [B][H_q][N_max]
@@ -35,7 +58,7 @@ struct SampleArgs {
   const float* uniforms;  // [B][H_q][M]
   int32_t* samples;       // [B][H_q][M] or null
   uint16_t* out;          // [B][H_q][128] bf16
-  int H_q, H_kv, N_max, M, Mp2;
+  int H_q, H_kv, N_max, M;
 };
 
 // 4 consecutive floats at p[j..j+3] (j % 4 == 0, 16-B aligned); lanes >= j1 read as 0
@@ -53,20 +76,12 @@ __device__ __forceinline__ float pick8(const float4& a, const float4& b, int i) 
   return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
 }
 
-__device__ __forceinline__ bool pair_less(float a, int ia, float b, int ib) {
-  return a < b || (a == b && ia < ib);
-}
-
-__global__ void __launch_bounds__(kSmpThreads, 1) sample_decode_kernel(SampleArgs a) {
-  extern __shared__ __align__(16) char smem[];
-  float* su = reinterpret_cast<float*>(smem);            // [Mp2] sorted uniforms
-  int* si = reinterpret_cast<int*>(su + a.Mp2);           // [Mp2] their original positions
-  int* sj = si + a.Mp2;                                   // [M] J of the sorted samples
-  float* red = reinterpret_cast<float*>(sj + a.M);        // [kSmpWarps][128]
-  __shared__ float s_off[kSmpThreads + 1];
+__global__ void __launch_bounds__(kSmpThreads, 4) sample_decode_kernel(SampleArgs a) {
+  __shared__ float s_off[kSub + 1];              // sub-block sums, then their exclusive offsets
+  __shared__ __align__(16) float red[kSmpWarps][kD];
   __shared__ float s_wtot[kSmpWarps], s_stot[kSmpWarps];
-  __shared__ int s_lo[kSmpThreads + 1];
   __shared__ int s_jlast;
+  extern __shared__ int sj[];                    // [M] J of each draw
 
   const int row = blockIdx.x;
   const int b = row / a.H_q, h = row % a.H_q;
@@ -77,176 +92,220 @@ __global__ void __launch_bounds__(kSmpThreads, 1) sample_decode_kernel(SampleArg
   const float* srow = a.scores + (size_t)row * a.N_max;
   const float* vrow = a.vnorm + ((size_t)b * a.H_kv + g) * a.N_max;
 
-  // ---- 1. sort (u, m) ascending ------------------------------------------------
-  for (int i = tid; i < a.Mp2; i += kSmpThreads) {
-    su[i] = i < M ? a.uniforms[(size_t)row * M + i] : INFINITY;
-    si[i] = i;
-  }
   if (tid == 0) s_jlast = -1;
-  __syncthreads();
-  for (int size = 2; size <= a.Mp2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < a.Mp2; i += kSmpThreads) {
-        const int p = i ^ stride;
-        if (p > i) {
-          const bool up = (i & size) == 0;
-          const float x = su[i], y = su[p];
-          const int ix = si[i], iy = si[p];
-          if (pair_less(y, iy, x, ix) == up) { su[i] = y; su[p] = x; si[i] = iy; si[p] = ix; }
+  SM_STAMP(0);
+  // ---- 1. sub-block sums -----------------------------------------------------------
+  // kSub sub-blocks of S keys (S a multiple of 8); a lane pair sums one sub-block
+  // with float4 loads (lane sl covers keys i + 4 sl .. + 3 of every 8), four
+  // sub-blocks per pair in flight.
+  const int S = max(8, ((n + kSub - 1) / kSub + 7) & ~7);
+  constexpr int kGroups = kSmpThreads / 2;
+  const int sl = lane & 1, grp = tid >> 1;
+  float pw = 0.f;                                          // this lane's sum of w_hat
+  int jpos = -1;
+  for (int kb = 0; kb < kSub / kGroups; kb += 4) {
+    float ps[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int i = 0; i < S; i += 8) {
+      float4 sv[4], vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = (grp + (kb + u) * kGroups) * S + i + sl * 4;
+        sv[u] = ld4_masked(srow, j, n);
+        vv[u] = ld4_masked(vrow, j, n);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = (grp + (kb + u) * kGroups) * S + i + sl * 4;
+        const float ss[4] = {sv[u].x, sv[u].y, sv[u].z, sv[u].w};
+        const float vs[4] = {vv[u].x, vv[u].y, vv[u].z, vv[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (ss[e] > 0.f) {                 // -inf (invalid), 0 and padding carry no mass
+            ps[u] += ss[e];
+            pw += vs[e] > 0.f ? __fdividef(ss[e], vs[e]) : 0.f;   // w_hat_j = s_j / ||v_j||  (R-24)
+            jpos = max(jpos, j + e);
+          }
         }
       }
-      __syncthreads();
     }
-  }
-
-  // ---- 2. segment sums and the block scan ----------------------------------------
-  // segments are multiples of 4 keys so they can be read as float4 (j0 16-B aligned)
-  const int S = (((n + kSmpThreads - 1) / kSmpThreads) + 3) & ~3;
-  const int j0 = min(tid * S, n), j1 = min(j0 + S, n);
-  float seg_s = 0.f, seg_w = 0.f;
-  int jpos = -1;
-#pragma unroll 4
-  for (int j = j0; j < j1; j += 4) {
-    const float4 sv = ld4_masked(srow, j, j1);
-    const float4 vv = ld4_masked(vrow, j, j1);
-    const float ss[4] = {sv.x, sv.y, sv.z, sv.w}, vs[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (ss[e] > 0.f) {                     // -inf (invalid), 0 and padding carry no mass
-        seg_s += ss[e];
-        seg_w += vs[e] > 0.f ? ss[e] / vs[e] : 0.f;   // w_hat_j = s_j / ||v_j||  (R-24)
-        jpos = j + e;
-      }
+    for (int u = 0; u < 4; ++u) {
+      const float t = ps[u] + __shfl_xor_sync(0xffffffffu, ps[u], 1);
+      if (sl == 0) s_off[grp + (kb + u) * kGroups] = t;
     }
   }
-  if (jpos >= 0) atomicMax(&s_jlast, jpos);
-  float inc = seg_s, wsum = seg_w;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    pw += __shfl_xor_sync(0xffffffffu, pw, o);
+    jpos = max(jpos, __shfl_xor_sync(0xffffffffu, jpos, o));
+  }
+  __syncthreads();                           // s_jlast init and the sums are visible
+  if (lane == 0) {
+    s_wtot[warp] = pw;
+    if (jpos >= 0) atomicMax(&s_jlast, jpos);
+  }
+  SM_STAMP(1);
+  // ---- 2. exclusive scan of the kSub sums (kPer per thread, then warps) ------------
+  constexpr int kPer = kSub / kSmpThreads;
+  float tsum = 0.f;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) tsum += s_off[tid * kPer + e];
+  float inc = tsum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const float y = __shfl_up_sync(0xffffffffu, inc, o);
     if (lane >= o) inc += y;
   }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
   if (lane == 31) s_stot[warp] = inc;
-  if (lane == 0) s_wtot[warp] = wsum;
   __syncthreads();
   if (warp == 0) {
-    float ti = s_stot[lane];
+    float ti = lane < kSmpWarps ? s_stot[lane] : 0.f;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
+    for (int o = 1; o < kSmpWarps; o <<= 1) {
       const float y = __shfl_up_sync(0xffffffffu, ti, o);
       if (lane >= o) ti += y;
     }
     float tex = __shfl_up_sync(0xffffffffu, ti, 1);
     if (lane == 0) tex = 0.f;
-    s_stot[lane] = tex;                      // exclusive warp offsets
-    float w = s_wtot[lane];
+    float w = lane < kSmpWarps ? s_wtot[lane] : 0.f;
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    __syncwarp();
+    if (lane < kSmpWarps) s_stot[lane] = tex;   // exclusive warp offsets
     if (lane == 0) s_wtot[0] = w;
   }
   __syncthreads();
-  float ex = __shfl_up_sync(0xffffffffu, inc, 1);
-  if (lane == 0) ex = 0.f;
-  const float off = s_stot[warp] + ex;                     // exclusive offset of my segment
-  s_off[tid] = off;
-  if (tid == kSmpThreads - 1) s_off[kSmpThreads] = s_stot[warp] + inc;
-  __syncthreads();
-  const float C = s_off[kSmpThreads];
-  const float Z = s_wtot[0];
-
-  // ---- 3. my targets: sorted x = u C in [off_t, off_{t+1}) ---------------------
-  {   // lo_t = first sorted sample with u C >= off_t (binary search)
-    int lo = 0, hi = M;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (su[mid] * C < off) lo = mid + 1; else hi = mid;
+  {
+    float ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = 0.f;
+    float c = s_stot[warp] + ex;             // exclusive offset of my kPer sub-blocks
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const float v = s_off[tid * kPer + e];
+      s_off[tid * kPer + e] = c;
+      c += v;
     }
-    s_lo[tid] = tid == 0 ? 0 : lo;
-    if (tid == 0) s_lo[kSmpThreads] = M;
+    if (tid == kSmpThreads - 1) s_off[kSub] = c;
   }
   __syncthreads();
+  const float C = s_off[kSub];
+  const float Z = s_wtot[0];
+
+  SM_STAMP(2);
+  // ---- 3. the draws: J_m by thread, into shared memory ----------------------------
+  // Draw m's target x = u_m C lies in the sub-block of the largest t with
+  // off_t <= x (binary search over s_off); the thread walks that sub-block's keys
+  // in order, c = off_t + s_j0 + ..., J = first j with c + s_j > x. A target past
+  // the sub-block's last positive key (fp32 rounding of the offsets) takes that
+  // key; one in a sub-block without mass takes the next key with mass.
   if (C > 0.f) {
-    const int m0 = s_lo[tid], m1 = s_lo[tid + 1];
-    float c = off;            // cumulative mass of the segment's keys before j
-    int j = j0, jl = -1;
-    // the segment is read 8 keys at a time (two float4), the next 8 prefetched
-    int cj = j0;
-    float4 a0 = ld4_masked(srow, cj, j1), a1 = ld4_masked(srow, cj + 4, j1);
-    float4 b0 = ld4_masked(srow, cj + 8, j1), b1 = ld4_masked(srow, cj + 12, j1);
-    for (int m = m0; m < m1; ++m) {
-      const float x = su[m] * C;
-      while (j < j1) {
-        if (j >= cj + 8) {
-          cj += 8;
-          a0 = b0;
-          a1 = b1;
-          b0 = ld4_masked(srow, cj + 8, j1);
-          b1 = ld4_masked(srow, cj + 12, j1);
-        }
-        const float s = pick8(a0, a1, j - cj);
-        if (s > 0.f) {
-          jl = j;
-          if (c + s > x) break;  // J = j; key j stays unconsumed for the next target
-          c += s;
-        }
-        ++j;
+    constexpr int kB = 3;                    // draws per thread in flight
+    for (int m0 = tid; m0 < M; m0 += kB * kSmpThreads) {
+      float x[kB];
+      int t[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int m = m0 + u * kSmpThreads;
+        x[u] = m < M ? a.uniforms[(size_t)row * M + m] * C : 0.f;
+        t[u] = 0;
       }
-      int J;
-      if (j < j1) J = j;                     // first j with C_j > x
-      else J = jl >= 0 ? jl : s_jlast;       // rounding at the segment end
-      sj[m] = J;
-      if (a.samples) a.samples[(size_t)row * M + si[m]] = J;
+#pragma unroll
+      for (int w = kSub / 2; w >= 1; w >>= 1) {   // largest t with off_t <= x (off_0 = 0)
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (s_off[t[u] + w] <= x[u]) t[u] += w;
+      }
+      float4 p0[kB], p1[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int k0 = min(t[u] * S, n), k1 = min(k0 + S, n);
+        p0[u] = ld4_masked(srow, k0, k1);
+        p1[u] = ld4_masked(srow, k0 + 4, k1);
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int m = m0 + u * kSmpThreads;
+        if (m >= M) break;
+        const int k0 = min(t[u] * S, n), k1 = min(k0 + S, n);
+        float c = s_off[t[u]];
+        int jl = -1, J = -2;
+        float4 q0 = p0[u], q1 = p1[u];
+        for (int j = k0; j < k1; j += 8) {
+          if (j > k0) {
+            q0 = ld4_masked(srow, j, k1);
+            q1 = ld4_masked(srow, j + 4, k1);
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float sv = pick8(q0, q1, e);
+            if (J == -2 && sv > 0.f) {
+              jl = j + e;
+              if (c + sv > x[u]) J = j + e;
+              else c += sv;
+            }
+          }
+          if (J != -2) break;
+        }
+        if (J == -2 && jl >= 0) J = jl;
+        for (int j = k1; J == -2 && j < n; ++j)   // empty sub-block: the next key with mass
+          if (srow[j] > 0.f) J = j;
+        if (J == -2) J = s_jlast;
+        sj[m] = J;
+        if (a.samples) a.samples[(size_t)row * M + m] = J;
+      }
     }
   } else if (a.samples) {
     for (int m = tid; m < M; m += kSmpThreads) a.samples[(size_t)row * M + m] = -1;
   }
   __syncthreads();
-
-  // ---- 4. gather v_J / ||v_J|| and reduce ----------------------------------------
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  SM_STAMP(3);
+  // ---- 4. gather v_J / ||v_J||: a contiguous run of draws per warp ----------------
+  // half-warp per row: lane l reads dims 8 (l & 15) .. + 7 of row (l >> 4) of each
+  // pair, kSmpU rows in flight per warp; 1 / ||v_J|| by rcp.approx (1 ulp).
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (C > 0.f) {
+    const int hl = lane >> 4;
+    const uint16_t* vbase = a.V + ((size_t)b * a.H_kv + g) * a.N_max * kD + (lane & 15) * 8;
     const int per = (M + kSmpWarps - 1) / kSmpWarps;
     const int mb = min(warp * per, M), me = min(mb + per, M);
-    const uint16_t* vbase = a.V + ((size_t)b * a.H_kv + g) * a.N_max * kD + lane * 4;
-    constexpr int U = 8;                     // rows in flight per warp
-    for (int m0 = mb; m0 < me; m0 += U) {
-      uint2 u[U];
-      float vn[U];
+    for (int m0 = mb; m0 < me; m0 += kSmpU) {
+      uint4 u[kSmpU / 2];
+      float vn[kSmpU / 2];
 #pragma unroll
-      for (int x = 0; x < U; ++x) {
-        const int m = m0 + x;
-        const int J = m < me ? sj[m] : sj[mb];
-        u[x] = ldg_nc_v2(vbase + (size_t)J * kD);
+      for (int x = 0; x < kSmpU / 2; ++x) {
+        const int J = sj[min(m0 + 2 * x + hl, me - 1)];
+        u[x] = ldg_nc_v4(vbase + (size_t)J * kD);
         vn[x] = __ldg(vrow + J);
       }
 #pragma unroll
-      for (int x = 0; x < U; ++x) {          // accumulate in draw order
-        if (m0 + x >= me) break;
-        const float f = 1.0f / vn[x];
-        acc[0] = fmaf(bf16lo(u[x].x), f, acc[0]);
-        acc[1] = fmaf(bf16hi(u[x].x), f, acc[1]);
-        acc[2] = fmaf(bf16lo(u[x].y), f, acc[2]);
-        acc[3] = fmaf(bf16hi(u[x].y), f, acc[3]);
+      for (int x = 0; x < kSmpU / 2; ++x) {  // accumulate in draw order (per half)
+        if (m0 + 2 * x + hl < me) {
+          float f;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(f) : "f"(vn[x]));
+          const uint32_t w[4] = {u[x].x, u[x].y, u[x].z, u[x].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            acc[2 * e] = fmaf(bf16lo(w[e]), f, acc[2 * e]);
+            acc[2 * e + 1] = fmaf(bf16hi(w[e]), f, acc[2 * e + 1]);
+          }
+        }
       }
     }
   }
 #pragma unroll
-  for (int e = 0; e < 4; ++e) red[warp * kD + lane * 4 + e] = acc[e];
+  for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 16);
+  if (lane < 16) {
+    *reinterpret_cast<float4*>(&red[warp][lane * 8]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(&red[warp][lane * 8 + 4]) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
   __syncthreads();
   if (tid < kD) {
     float t = 0.f;
-    for (int w = 0; w < kSmpWarps; ++w) t += red[w * kD + tid];
+    for (int w = 0; w < kSmpWarps; ++w) t += red[w][tid];
     const float scale = (C > 0.f && Z > 0.f && M > 0) ? (C / Z) / (float)M : 0.f;
     a.out[(size_t)row * kD + tid] = (uint16_t)f2bf_bits(t * scale);
   }
-}
-
-size_t sample_smem_bytes(int M) {
-  int Mp2 = 1;
-  while (Mp2 < M) Mp2 <<= 1;
-  return (size_t)Mp2 * 8 + (size_t)M * 4 + (size_t)kSmpWarps * kD * 4;
+  SM_STAMP(4);
 }
 
 socket_status launch_sample_decode(const socket_cfg& c, const float* scores, const float* vnorm,
@@ -269,11 +328,8 @@ socket_status launch_sample_decode(const socket_cfg& c, const float* scores, con
   a.H_kv = c.H_kv;
   a.N_max = c.N_max;
   a.M = M;
-  int Mp2 = 1;
-  while (Mp2 < M) Mp2 <<= 1;
-  a.Mp2 = Mp2;
-  const size_t sm = sample_smem_bytes(M);
-  cudaFuncSetAttribute(sample_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int sm = M * (int)sizeof(int32_t);
+  cudaFuncSetAttribute(sample_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   sample_decode_kernel<<<rows, kSmpThreads, sm, st>>>(a);
   return check_launch("sample_decode_kernel");
 }

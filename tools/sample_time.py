@@ -34,3 +34,7 @@ for M in (k, 256, 8192):
         e1.synchronize()
         tot += e0.elapsed_time(e1)
     print(f"B={B} rows={B * 32} M={M}: {tot / 10 * 1e3:.1f} us")
+_, J = ops.sample_decode(cfg, sc, dec.vnorm, V, lens, u)
+J = J.view(B * 32, k)
+d = [int(torch.unique(J[r]).numel()) for r in range(0, B * 32, 37)]
+print(f"distinct J per row (M={k}): mean {sum(d) / len(d):.0f}")
