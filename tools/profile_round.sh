@@ -14,4 +14,8 @@ timeout 900 ncu --set full --clock-control none --import-source on \
     -o gpurun_out/prof_$tag python tools/profile_step.py --steps 2 > gpurun_out/ncu_$tag.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"hash_keys_tc|vnorm" -c 2 \
     -o gpurun_out/prof_prefill_$tag python tools/profile_step.py --steps 1 > gpurun_out/ncu_prefill_$tag.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    -k regex:sample_decode -c 6 --log-file gpurun_out/launches_sample_$tag.csv python tools/sample_time.py > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sample_decode -s 3 -c 1 \
+    -o gpurun_out/prof_sample_$tag python tools/sample_time.py > gpurun_out/ncu_sample_$tag.log 2>&1
 echo done
