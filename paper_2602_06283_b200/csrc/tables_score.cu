@@ -230,6 +230,12 @@ score_wide_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ 
 // from the half-table image, so a lookup is one conflict-free LDS as in the
 // byte-code kernel; the CTA sweeps its keys once per group, keeping the first
 // group's partial sums in shared memory.
+#ifndef SK_WIDE_KU
+#define SK_WIDE_KU 2
+#endif
+#ifndef SK_WIDE_PIPE
+#define SK_WIDE_PIPE 1
+#endif
 template <int NH>
 __global__ void __launch_bounds__(kWideThreads, 1)
 score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ codes,
@@ -239,8 +245,10 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
   extern __shared__ __align__(16) float w2[];
   const int R = 1 << P, Pl = P / 2, RL = 1 << Pl;
   float* tab = w2;                          // [R][32]
+  const char* tabc = reinterpret_cast<const char*>(w2);
   float* ast = tab + R * 32;                // [NH][RL][32] staged A half-tables of the group
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t lane4 = 4u * lane;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tiles_per_row = N_max >> 5;
   const long long tb = total_tiles * blockIdx.x / gridDim.x;
@@ -284,45 +292,82 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
       __syncthreads();
       // sweep: lane = key, slots gi*32 .. gi*32 + 31 (two 16-element chunks); the
       // first group's partial sum is parked in `scores` (the same thread reads it back)
-      constexpr int kU = 2;                   // tiles in flight per warp
-      for (int ti0 = t0 + warp; ti0 < vt1; ti0 += kU * (kWideThreads / 32)) {
+      constexpr int kU = SK_WIDE_KU;          // tiles per batch per warp
+      constexpr int kStep = kU * (kWideThreads / 32);
+      const bool last = gi + 1 == groups;
+      struct Batch {
         uint4 w[kU][4];
+        float prev[kU], vn[kU];               // parked partial, ||v_j|| (loaded with the codes)
+      };
+      auto load = [&](Batch& B, int ti0) {
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const int ti = ti0 + u * (kWideThreads / 32);
           const int j = ti * 32 + lane;
+          B.prev[u] = 0.f;
+          B.vn[u] = 0.f;
           if (ti < vt1) {
             const uint16_t* cp = crow + code_off(j, gi * 32, Lp);
             const uint16_t* cp2 = crow + code_off(j, gi * 32 + 16, Lp);
-            w[u][0] = ldg_nc_v4(cp);
-            w[u][1] = ldg_nc_v4(cp + 8);
-            w[u][2] = ldg_nc_v4(cp2);
-            w[u][3] = ldg_nc_v4(cp2 + 8);
+            B.w[u][0] = ldg_nc_v4(cp);
+            B.w[u][1] = ldg_nc_v4(cp + 8);
+            B.w[u][2] = ldg_nc_v4(cp2);
+            B.w[u][3] = ldg_nc_v4(cp2 + 8);
+            if (gi > 0) B.prev[u] = srow[j];
+            if (last) B.vn[u] = __ldg(vrow + j);
           }
         }
+      };
+      auto compute = [&](const Batch& B, int ti0) {
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const int ti = ti0 + u * (kWideThreads / 32);
           if (ti >= vt1) break;
           const int j = ti * 32 + lane;
-          const uint32_t* wd = reinterpret_cast<const uint32_t*>(w[u]);
-          float acc0 = 0.f, acc1 = 0.f;
+          const uint32_t* wd = reinterpret_cast<const uint32_t*>(B.w[u]);
+          // byte offset code * 128 + 4 ((sl + lane) & 31), codes < 2^10: the two
+          // codes of a word are shifted in place and OR-ed with the column offset
+          uint64_t acc = 0ull;
 #pragma unroll
-          for (int sl = 0; sl < 32; ++sl) {
-            const uint32_t code = (sl & 1) ? (wd[sl >> 1] >> 16) : (wd[sl >> 1] & 0xFFFFu);
-            const float v = tab[code * 32 + ((sl + lane) & 31)];
-            if (sl & 1) acc1 += v; else acc0 += v;
+          for (int sl = 0; sl < 32; sl += 2) {
+            const uint32_t wv = wd[sl >> 1];
+            const uint32_t a0 = ((wv << 7) & 0x1FF80u) | ((lane4 + 4u * sl) & 124u);
+            const uint32_t a1 = ((wv >> 9) & 0x1FF80u) | ((lane4 + 4u * sl + 4u) & 124u);
+            const float v0 = *reinterpret_cast<const float*>(tabc + a0);
+            const float v1 = *reinterpret_cast<const float*>(tabc + a1);
+            const uint64_t pv = (uint64_t)__float_as_uint(v0) | ((uint64_t)__float_as_uint(v1) << 32);
+            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(pv));
           }
-          const float accg = acc0 + acc1;
-          if (gi + 1 < groups) {
-            srow[j] = gi == 0 ? accg : srow[j] + accg;
+          const float accg = __uint_as_float((uint32_t)acc) + __uint_as_float((uint32_t)(acc >> 32));
+          if (!last) {
+            srow[j] = gi == 0 ? accg : B.prev[u] + accg;
           } else {
-            const float tot = (groups > 1 ? srow[j] : 0.f) + accg;
+            const float tot = (gi > 0 ? B.prev[u] : 0.f) + accg;
             const bool ok = j < n && (!mrow || mrow[j]);
-            srow[j] = ok ? vrow[j] * tot : -INFINITY;
+            srow[j] = ok ? B.vn[u] * tot : -INFINITY;
           }
         }
+      };
+#if SK_WIDE_PIPE
+      // two batches per warp: the next batch's loads are in flight while the
+      // current one is looked up
+      Batch A, Bn;
+      int ti0 = t0 + warp;
+      if (ti0 < vt1) load(A, ti0);
+      for (; ti0 < vt1; ti0 += 2 * kStep) {
+        if (ti0 + kStep < vt1) load(Bn, ti0 + kStep);
+        compute(A, ti0);
+        if (ti0 + kStep >= vt1) break;
+        if (ti0 + 2 * kStep < vt1) load(A, ti0 + 2 * kStep);
+        compute(Bn, ti0 + kStep);
       }
+#else
+      for (int ti0 = t0 + warp; ti0 < vt1; ti0 += kStep) {
+        Batch A;
+        load(A, ti0);
+        compute(A, ti0);
+      }
+#endif
     }
     for (int ti = max(t0, vt1) + warp; ti < t1; ti += kWideThreads / 32) srow[ti * 32 + lane] = -INFINITY;
   }

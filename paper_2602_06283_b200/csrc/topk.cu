@@ -26,8 +26,6 @@ namespace sk {
 __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs a) {
   extern __shared__ __align__(16) uint32_t keys[];          // [per], per % 128 == 0
   __shared__ TopkShared S;
-  constexpr unsigned kFull = 0xffffffffu;
-
   TK_TRACE(0);
   asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: scores of the predecessor
   TK_TRACE(1);
@@ -36,13 +34,11 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
   const int csize = (int)cluster.num_blocks();
   const int row = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const unsigned lt = (1u << lane) - 1u;
   const int b = row / a.H_sel;
   const int n = a.mode == 0 ? a.seq_lens[b] : a.G * a.k;
   const int base = crank * a.per;
   int len = n - base;
   len = len < 0 ? 0 : (len > a.per ? a.per : len);
-  const int len32 = (len + 31) & ~31;
   const int len128 = (len + 127) & ~127;
   // warp w owns the rounds [r0, r1) of 128 keys; round r covers keys r*128 + x*32 + lane
   const int nr = len128 >> 7;
