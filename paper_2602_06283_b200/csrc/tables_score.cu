@@ -434,21 +434,24 @@ struct RegTile {
 
 template <int LP>
 __device__ __forceinline__ void load_reg_tile(RegTile<LP>& t, const uint8_t* tile_codes,
-                                              const float* tile_vn, int lane) {
+                                              const float* tile_vn, int lane, uint64_t pol) {
   constexpr int CB = LP < 16 ? LP : 16;
 #pragma unroll
   for (int ch = 0; ch < LP / CB; ++ch) {
     if constexpr (CB == 16) {
-      const uint4 v = ldg_nc_v4(tile_codes + ch * 512 + lane * 16);
+      const uint4 v = ldg_nc_v4_hint(tile_codes + ch * 512 + lane * 16, pol);
       t.w[ch * 4 + 0] = v.x; t.w[ch * 4 + 1] = v.y; t.w[ch * 4 + 2] = v.z; t.w[ch * 4 + 3] = v.w;
     } else {
-      const uint2 v = ldg_nc_v2(tile_codes + ch * 256 + lane * 8);
+      const uint2 v = ldg_nc_v2_hint(tile_codes + ch * 256 + lane * 8, pol);
       t.w[ch * 2 + 0] = v.x; t.w[ch * 2 + 1] = v.y;
     }
   }
   t.vn = __ldg(tile_vn + lane);
 }
 
+#ifndef SK_SCORE_L2HINT
+#define SK_SCORE_L2HINT 1
+#endif
 template <int LP>
 __global__ void __launch_bounds__(kScoreThreads, 1)
 score_reg_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
@@ -463,6 +466,11 @@ score_reg_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ co
 #pragma unroll
   for (int m = 0; m < 16; ++m)
     pk[m] = (uint32_t)(((2 * m + lane) & 31) << 2) | ((uint32_t)(((2 * m + 1 + lane) & 31) << 2) << 8);
+#if SK_SCORE_L2HINT
+  const uint64_t pol_code = l2_policy_evict_first(), pol_score = l2_policy_evict_last();
+#else
+  const uint64_t pol_code = l2_policy_evict_normal(), pol_score = l2_policy_evict_normal();
+#endif
   const int tiles_per_row = N_max >> 5;
   const long long t_begin = total_tiles * blockIdx.x / gridDim.x;
   const long long t_end = total_tiles * (blockIdx.x + 1) / gridDim.x;
@@ -512,17 +520,17 @@ score_reg_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ co
       const float acc0 = __uint_as_float((uint32_t)acc), acc1 = __uint_as_float((uint32_t)(acc >> 32));
       const int j = tix * 32 + lane;
       const bool ok = j < n && (!mrow || mrow[j]);
-      srow[j] = ok ? tt.vn * (acc0 + acc1) : -INFINITY;
+      st_f32_hint(srow + j, ok ? tt.vn * (acc0 + acc1) : -INFINITY, pol_score);   // top-k reads it next
     };
     constexpr int W = kScoreWarps;
     int ti = tile0 + warp;
     RegTile<LP> a0, a1, b0, b1;
-    if (ti < vt1) load_reg_tile<LP>(a0, crow + (size_t)ti * 32 * LP, vrow + ti * 32, lane);
-    if (ti + W < vt1) load_reg_tile<LP>(a1, crow + (size_t)(ti + W) * 32 * LP, vrow + (ti + W) * 32, lane);
+    if (ti < vt1) load_reg_tile<LP>(a0, crow + (size_t)ti * 32 * LP, vrow + ti * 32, lane, pol_code);
+    if (ti + W < vt1) load_reg_tile<LP>(a1, crow + (size_t)(ti + W) * 32 * LP, vrow + (ti + W) * 32, lane, pol_code);
     if (need_lut) mbar_wait(&bar, phase);
     for (; ti < vt1; ti += 2 * W) {
-      if (ti + 2 * W < vt1) load_reg_tile<LP>(b0, crow + (size_t)(ti + 2 * W) * 32 * LP, vrow + (ti + 2 * W) * 32, lane);
-      if (ti + 3 * W < vt1) load_reg_tile<LP>(b1, crow + (size_t)(ti + 3 * W) * 32 * LP, vrow + (ti + 3 * W) * 32, lane);
+      if (ti + 2 * W < vt1) load_reg_tile<LP>(b0, crow + (size_t)(ti + 2 * W) * 32 * LP, vrow + (ti + 2 * W) * 32, lane, pol_code);
+      if (ti + 3 * W < vt1) load_reg_tile<LP>(b1, crow + (size_t)(ti + 3 * W) * 32 * LP, vrow + (ti + 3 * W) * 32, lane, pol_code);
       score_tile(a0, ti);
       if (ti + W < vt1) score_tile(a1, ti + W);
       a0 = b0;

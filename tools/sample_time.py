@@ -37,4 +37,4 @@ for M in (k, 256, 8192):
 _, J = ops.sample_decode(cfg, sc, dec.vnorm, V, lens, u)
 J = J.view(B * 32, k)
 d = [int(torch.unique(J[r]).numel()) for r in range(0, B * 32, 37)]
-print(f"distinct J per row (M={k}): mean {sum(d) / len(d):.0f}")
+print(f"distinct J per row (M={k}): mean {sum(d) / len(d):.0f}", flush=True)
