@@ -249,6 +249,7 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
   float* ast = tab + R * 32;                // [NH][RL][32] staged A half-tables of the group
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lane4 = 4u * lane;
+  const uint64_t pol_code = l2_policy_evict_first(), pol_score = l2_policy_evict_last();
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tiles_per_row = N_max >> 5;
   const long long tb = total_tiles * blockIdx.x / gridDim.x;
@@ -309,10 +310,10 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
           if (ti < vt1) {
             const uint16_t* cp = crow + code_off(j, gi * 32, Lp);
             const uint16_t* cp2 = crow + code_off(j, gi * 32 + 16, Lp);
-            B.w[u][0] = ldg_nc_v4(cp);
-            B.w[u][1] = ldg_nc_v4(cp + 8);
-            B.w[u][2] = ldg_nc_v4(cp2);
-            B.w[u][3] = ldg_nc_v4(cp2 + 8);
+            B.w[u][0] = ldg_nc_v4_hint(cp, pol_code);
+            B.w[u][1] = ldg_nc_v4_hint(cp + 8, pol_code);
+            B.w[u][2] = ldg_nc_v4_hint(cp2, pol_code);
+            B.w[u][3] = ldg_nc_v4_hint(cp2 + 8, pol_code);
             if (gi > 0) B.prev[u] = srow[j];
             if (last) B.vn[u] = __ldg(vrow + j);
           }
@@ -344,7 +345,7 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
           } else {
             const float tot = (gi > 0 ? B.prev[u] : 0.f) + accg;
             const bool ok = j < n && (!mrow || mrow[j]);
-            srow[j] = ok ? B.vn[u] * tot : -INFINITY;
+            st_f32_hint(srow + j, ok ? B.vn[u] * tot : -INFINITY, pol_score);   // top-k reads it next
           }
         }
       };
