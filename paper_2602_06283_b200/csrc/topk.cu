@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
   const int crank = (int)cluster.block_rank();
   const int csize = (int)cluster.num_blocks();
   const int row = blockIdx.y;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int b = row / a.H_sel;
   const int n = a.mode == 0 ? a.seq_lens[b] : a.G * a.k;
   const int base = crank * a.per;
