@@ -202,6 +202,10 @@ socket_status socket_score_lut(const socket_cfg* cfg, const void* lut, const uin
  *   socket_sparse_decode).  Up to 8 selection rows (KV_SHARED, P <= 8) run as
  *   one cluster launch; otherwise 4 launches chained with programmatic
  *   dependent launch.  Requires L <= 64.
+ *   q, k_new and v_new may be device pointers or pinned, UVA-mapped host
+ *   pointers (cudaHostAlloc / cudaHostRegister); out may be either too.  On the
+ *   chained path host-resident inputs are first pulled into the workspace by
+ *   one copy kernel (a 5th launch); the one-launch kernel reads them in place.
  *   ws: socket_workspace_bytes(cfg, SOCKET_OP_DECODE_STEP, k). */
 socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, void* V,
                                  const void* W, uint8_t* codes, float* vnorm,
@@ -211,9 +215,9 @@ socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, 
                                  float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
                                  void* ws, size_t ws_bytes, void* stream);
 
-/* Number of kernel launches socket_decode_step issues for cfg: 1 (the
- * one-launch cluster kernel, small batches) or 4 (PDL-chained kernels);
- * 0 if cfg is invalid. */
+/* Number of kernel launches socket_decode_step issues for cfg with device
+ * inputs: 1 (the one-launch cluster kernel, small batches) or 4 (PDL-chained
+ * kernels; 5 when q / k_new / v_new are host-resident); 0 if cfg is invalid. */
 int32_t socket_decode_step_launches(const socket_cfg* cfg);
 
 /* Alg. 3 l.244 TopK with forced sink / local window: per (b, row),

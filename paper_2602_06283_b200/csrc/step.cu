@@ -65,19 +65,61 @@ socket_status launch_prologue(const socket_cfg& c, ProArgs a, bool tables, cudaS
   const int grid = a.n_tab_ctas + n_app;
   if (grid == 0) return SOCKET_OK;
   const size_t sm = prologue_smem_bytes();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kPT);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.pdl ? 1 : 0;
 #define SK_PRO(N)                                                                              \
   case N:                                                                                      \
     cudaFuncSetAttribute(prologue_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    prologue_kernel<N><<<grid, kPT, sm, st>>>(a);                                              \
+    if (cudaLaunchKernelEx(&cfg, prologue_kernel<N>, a) != cudaSuccess)                        \
+      return check_launch("prologue_kernel");                                                  \
     break;
   switch (tables ? NH : 1) { SK_PRO(1) SK_PRO(2) SK_PRO(4) SK_PRO(8) }
 #undef SK_PRO
   return check_launch("prologue_kernel");
 }
 
+// Host-resident step inputs (pinned, UVA-mapped q / k_new / v_new): one copy
+// kernel pulls them into the workspace before the prologue -- 16-B loads, all in
+// flight at once, so the PCIe reads overlap (a DMA copy of the same 192 KB took
+// ~16 us in tools/e2e_probe3.py).
+static size_t stage_bytes(const socket_cfg& c) {
+  return (((size_t)c.B * c.H_q * kD + 2 * (size_t)c.B * c.H_kv * kD) * 2 + 255) & ~(size_t)255;
+}
+
+__global__ void __launch_bounds__(256) stage_inputs_kernel(const uint4* q_h, const uint4* k_h,
+                                                           const uint4* v_h, uint4* dst, int nq, int nk) {
+  const int n = nq + 2 * nk;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint4* src = i < nq ? q_h + i : (i < nq + nk ? k_h + (i - nq) : v_h + (i - nq - nk));
+    dst[i] = *src;
+  }
+}
+
+static bool host_resident(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 size_t decode_step_workspace_bytes(const socket_cfg& c, int k) {
   const size_t lut = ((size_t)c.B * num_sel_rows(c) * lut_row_bytes(c) + 255) & ~(size_t)255;
-  return lut + decode_workspace_bytes(c, k, false);
+  return lut + ((decode_workspace_bytes(c, k, false) + 255) & ~(size_t)255) + stage_bytes(c);
+}
+
+bool decode_step_stages_inputs(const socket_cfg& c, const void* q, const void* k_new, const void* v_new) {
+  return !fused_step_applies(c) && (host_resident(q) || host_resident(k_new) || host_resident(v_new));
 }
 
 socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, void* V,
@@ -101,7 +143,28 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, vo
                              sink, window, scores, idx, cnt, out, lse, st);
   float* lut = static_cast<float*>(ws);
   void* dws = static_cast<char*>(ws) + lut_bytes;
-  const size_t dws_bytes = ws_bytes - lut_bytes;
+  const size_t dws_bytes = (decode_workspace_bytes(c, k, false) + 255) & ~(size_t)255;
+  // ---- host-resident inputs: stage them into the workspace first --------------
+  const bool staged = decode_step_stages_inputs(c, q, k_new, v_new);
+  if (staged) {
+    const int nq = c.B * c.H_q * kD / 8, nk = c.B * c.H_kv * kD / 8;   // 16-B chunks
+    uint16_t* stage = reinterpret_cast<uint16_t*>(static_cast<char*>(dws) + dws_bytes);
+    const bool has_new = k_new != nullptr && v_new != nullptr;
+    const int nk_used = has_new ? nk : 0;
+    const int n = nq + 2 * nk_used;
+    const int blocks = (n + 255) / 256 < 2 * kNumSMs ? (n + 255) / 256 : 2 * kNumSMs;
+    stage_inputs_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint4*>(q),
+                                                static_cast<const uint4*>(k_new),
+                                                static_cast<const uint4*>(v_new),
+                                                reinterpret_cast<uint4*>(stage), nq, nk_used);
+    socket_status s0 = check_launch("stage_inputs_kernel");
+    if (s0 != SOCKET_OK) return s0;
+    q = stage;
+    if (has_new) {
+      k_new = stage + (size_t)nq * 8;
+      v_new = stage + (size_t)(nq + nk) * 8;
+    }
+  }
   // decode tickets live at the end of the decode workspace; find them without launching
   int* tickets = nullptr;
   int n_units = 0;
@@ -128,6 +191,7 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, vo
   pa.n_begin = 0;
   pa.n_count = 1;
   pa.append_last = 1;
+  pa.pdl = staged ? 1 : 0;           // PDL edge after the staging kernel
   s = launch_prologue(c, pa, true, st);
   if (s != SOCKET_OK) return s;
   // ---- score, top-k, decode (PDL chain) ----------------------------------------

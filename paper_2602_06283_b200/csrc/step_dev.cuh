@@ -98,6 +98,7 @@ struct ProArgs {
   int n_wtiles;           // ceil(Lp / tpt)
   int n_tab_ctas;         // ceil(B*H_q / kTQ) * n_wtiles (0: no tables)
   int n_keys, n_begin, n_count, append_last;   // append: key kk -> (bh, j)
+  int pdl;                // launched as a PDL dependent (griddepcontrol.wait first)
 };
 
 // 8 bf16 (one uint4) -> 8 fp64 with integer ops (exact for zero and normal
@@ -479,6 +480,7 @@ socket_status launch_prologue(const socket_cfg& c, ProArgs a, bool tables, cudaS
 template <int NH>
 __global__ void __launch_bounds__(kPT, 2) prologue_kernel(ProArgs a) {
   extern __shared__ __align__(16) char psm[];
+  if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: staged inputs
   if (blockIdx.x == 0 && a.tickets)
     for (int i = threadIdx.x; i < a.n_tickets; i += blockDim.x) a.tickets[i] = 0;
   if ((int)blockIdx.x < a.n_tab_ctas) {

@@ -109,10 +109,11 @@ class SocketDecoder:
     def bind_host(self, seq_lens: torch.Tensor):
         """Allocate pinned host I/O buffers for host_step(): q [B][H_q][d] and the
         new token's K and V rows [B][H_kv][d] packed in one pinned input buffer,
-        and a pinned output [B][H_q][d].  host_step() issues one H2D copy of the
-        inputs and the decode step as a CUDA graph (it stores the new rows into the
-        cache at seq_lens[b] - 1 and hashes them, and writes the output straight
-        into the pinned, UVA-mapped host buffer -- no D2H copy).
+        and a pinned output [B][H_q][d].  host_step() replays the decode step as
+        a CUDA graph that reads the inputs from the pinned, UVA-mapped buffer
+        (staged by one copy kernel on the chained path), stores the new rows into
+        the cache at seq_lens[b] - 1, hashes them, and writes the output straight
+        into the pinned output -- no DMA copy either way.
         (Memcpy nodes from pinned host memory inside the graph cost ~50 us of
         launch latency per replay on this driver, so the copies stay outside.)
         Returns the pinned views (q_in, k_in, v_in, out)."""
@@ -130,9 +131,10 @@ class SocketDecoder:
 
         direct = self.fused      # socket_decode_step writes `out` straight into the
                                  # pinned (UVA-mapped) host buffer: no D2H copy
-        # the one-launch kernel (small batch) reads each input once: it reads q and
-        # the new rows straight from the mapped host buffer (no H2D copy either)
-        self._host_inputs_direct = direct and ops.decode_step_launches(cfg) == 1
+        # and it takes q and the new rows from the mapped host buffer: the
+        # one-launch kernel (small batch) reads each input once in place, the
+        # chained path stages them with one copy kernel (no DMA copy outside the graph)
+        self._host_inputs_direct = direct
         src_q, src_k, src_v = views(self._in_h) if self._host_inputs_direct else (q_d, k_d, v_d)
 
         def body():
