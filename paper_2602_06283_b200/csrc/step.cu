@@ -94,6 +94,9 @@ static size_t stage_bytes(const socket_cfg& c) {
   return (((size_t)c.B * c.H_q * kD + 2 * (size_t)c.B * c.H_kv * kD) * 2 + 255) & ~(size_t)255;
 }
 
+#ifndef SK_STAGE_T
+#define SK_STAGE_T 256
+#endif
 __global__ void __launch_bounds__(256) stage_inputs_kernel(const uint4* q_h, const uint4* k_h,
                                                            const uint4* v_h, uint4* dst, int nq, int nk) {
   const int n = nq + 2 * nk;
@@ -152,8 +155,8 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, vo
     const bool has_new = k_new != nullptr && v_new != nullptr;
     const int nk_used = has_new ? nk : 0;
     const int n = nq + 2 * nk_used;
-    const int blocks = (n + 255) / 256 < 2 * kNumSMs ? (n + 255) / 256 : 2 * kNumSMs;
-    stage_inputs_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint4*>(q),
+    const int blocks = (n + SK_STAGE_T - 1) / SK_STAGE_T < 2 * kNumSMs ? (n + SK_STAGE_T - 1) / SK_STAGE_T : 2 * kNumSMs;
+    stage_inputs_kernel<<<blocks, SK_STAGE_T, 0, st>>>(static_cast<const uint4*>(q),
                                                 static_cast<const uint4*>(k_new),
                                                 static_cast<const uint4*>(v_new),
                                                 reinterpret_cast<uint4*>(stage), nq, nk_used);
