@@ -514,6 +514,33 @@ def test_decode_step_with_new_rows(one_launch, monkeypatch):
     assert torch.equal(a.idx, bb.idx) and torch.equal(oa, ob) and torch.equal(la, lb)
 
 
+@pytest.mark.parametrize("one_launch", [True, False])
+def test_decode_step_host_inputs_equal_device_inputs(one_launch, monkeypatch):
+    """q, k_new and v_new in pinned host memory (read in place by the one-launch
+    kernel, staged by the copy kernel on the chained path) give bit-identical
+    caches, selections and outputs to the same inputs on the device."""
+    if not one_launch:
+        monkeypatch.setenv("SOCKET_NO_FUSED", "1")
+    lens = [2048, 1777]
+    cfg, c, W, d = make(2, 8, 2, 2048, 60, 8, seed=57, seq_lens=lens)
+    g = torch.Generator(device=DEV).manual_seed(5)
+    k_new = torch.randn((2, 2, 128), generator=g, device=DEV).to(torch.bfloat16)
+    v_new = torch.randn((2, 2, 128), generator=g, device=DEV).to(torch.bfloat16)
+    Ka, Va = d["K"].clone(), d["V"].clone()
+    Kb, Vb = d["K"].clone(), d["V"].clone()
+    a = SocketDecoder(cfg, d["W"], Ka, Va, k=300)
+    bb = SocketDecoder(cfg, d["W"], Kb, Vb, k=300)
+    a.prefill()
+    bb.prefill()
+    qh, kh, vh = (t.cpu().pin_memory() for t in (d["q"], k_new, v_new))
+    oa, la = [t.clone() for t in a.step(qh, d["seq_lens"], append=True, k_new=kh, v_new=vh)]
+    ob, lb = [t.clone() for t in bb.step(d["q"], d["seq_lens"], append=True, k_new=k_new, v_new=v_new)]
+    torch.cuda.synchronize()
+    assert torch.equal(Ka, Kb) and torch.equal(Va, Vb)
+    assert torch.equal(a.codes, bb.codes) and torch.equal(a.vnorm, bb.vnorm)
+    assert torch.equal(a.idx, bb.idx) and torch.equal(oa, ob) and torch.equal(la, lb)
+
+
 @pytest.mark.parametrize("B", [4, 8])   # 8 rows: one-launch kernel reading host memory; 16: chained
 def test_host_step_graph_matches_device_step(B):
     """bind_host / host_step (pinned host inputs -> graph step -> pinned host
