@@ -97,6 +97,9 @@ static size_t stage_bytes(const socket_cfg& c) {
 #ifndef SK_STAGE_T
 #define SK_STAGE_T 256
 #endif
+#ifndef SK_STAGE_NEW
+#define SK_STAGE_NEW 1    // 0: the append tiles read host k_new / v_new in place
+#endif
 __global__ void __launch_bounds__(256) stage_inputs_kernel(const uint4* q_h, const uint4* k_h,
                                                            const uint4* v_h, uint4* dst, int nq, int nk) {
   const int n = nq + 2 * nk;
@@ -152,7 +155,7 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, vo
   if (staged) {
     const int nq = c.B * c.H_q * kD / 8, nk = c.B * c.H_kv * kD / 8;   // 16-B chunks
     uint16_t* stage = reinterpret_cast<uint16_t*>(static_cast<char*>(dws) + dws_bytes);
-    const bool has_new = k_new != nullptr && v_new != nullptr;
+    const bool has_new = SK_STAGE_NEW && k_new != nullptr && v_new != nullptr;
     const int nk_used = has_new ? nk : 0;
     const int n = nq + 2 * nk_used;
     const int blocks = (n + SK_STAGE_T - 1) / SK_STAGE_T < 2 * kNumSMs ? (n + SK_STAGE_T - 1) / SK_STAGE_T : 2 * kNumSMs;
