@@ -14,7 +14,9 @@
  *   LSE combine of partials    (Flash-Decode split merge)      socket_lse_combine
  *   dense decode (k = n)       Eq. 1 P:16-22                          socket_dense_decode
  *   whole decode step          P:259-271                              socket_decode_step
- *   sequence-shard resolve     exact global top-k over shards         socket_topk_resolve
+ *   sequence-shard top-k       exact global top-k over shards         socket_topk_digest,
+ *                                                                     _bracket, _window,
+ *                                                                     _resolve, _emit
  *
  * Conventions (all entry points)
  *  - Every pointer argument is DEVICE memory owned by the caller, except the
@@ -26,8 +28,9 @@
  *    on the host.
  *  - bf16 arrays are passed as `const void*` holding IEEE bfloat16 values.
  *  - Errors: host-side validation returns SOCKET_EINVAL (null required pointer,
- *    P not in [1,8], L < 1, d != 128, tau <= 0, k <= 0, sink+window > k,
- *    H_q % H_kv != 0, N_max not a multiple of 32, bad ranges);
+ *    P not in [1,16], L < 1, d <= 0, tau <= 0, k <= 0, sink+window > k,
+ *    H_q % H_kv != 0, N_max not a multiple of 32, index_base < 0, bad
+ *    ranges);
  *    SOCKET_EUNSUPPORTED for valid but not implemented shapes;
  *    SOCKET_EWORKSPACE if ws_bytes is too small; SOCKET_ECUDA if a launch
  *    fails.  The message of the last non-OK status of the calling thread is
@@ -48,7 +51,7 @@
 extern "C" {
 #endif
 
-#define SOCKET_ABI_VERSION 2
+#define SOCKET_ABI_VERSION 3
 
 typedef enum {
   SOCKET_OK = 0,
@@ -82,12 +85,26 @@ typedef struct {
   int32_t d;          /* head dim; must be 128                                     */
   int32_t N_max;      /* token capacity = row stride of K/V/vnorm/scores; %32 == 0 */
   int32_t L;          /* hash tables, >= 1 (Alg. 1 "#tables L")                    */
-  int32_t P;          /* hyperplanes per table, 1..8 (Alg. 1 "#hyperplanes P")     */
+  int32_t P;          /* hyperplanes per table, 1..16 (Alg. 1 "#hyperplanes P");    *
+                       * P <= 8: one code byte per table, P = 9..16: one uint16   */
   float tau;          /* temperature > 0 (Alg. 2)                                  */
   float sm_scale;     /* softmax scale on q.k (reading R-2; usually 1/sqrt(d))     */
   int32_t group_mode; /* socket_group_mode                                         */
   int32_t scoring;    /* socket_scoring; 0 = soft scores (SOCKET, Eq. 4)           */
+  int32_t flags;      /* SOCKET_FLAG_* bits; 0 = defaults                          */
+  int64_t index_base; /* global token position of local row 0 of this buffer      *
+                       * (sequence shards); 0 otherwise.   *
+                       * Keys are at global positions index_base + j, and key j  *
+                       * is valid iff index_base + j < seq_lens[b] (seq_lens are *
+                       * always the sequences' TOTAL lengths).                   */
 } socket_cfg;
+
+/* socket_cfg.flags */
+enum {
+  /* socket_decode_step: never use the one-launch cluster kernel, always the
+   * PDL-chained kernels (both give bit-identical codes, scores and selections) */
+  SOCKET_FLAG_CHAINED_STEP = 1
+};
 
 /* ------------------------------------------------------------------------ *
  * Data layouts (all row-major, innermost last)
@@ -96,7 +113,12 @@ typedef struct {
  *   W       [L][P][d]              bf16   projections W^(l) (Alg. 1 l.201);
  *                                         one W shared by every b and head
  *   vnorm   [B][H_kv][N_max]       fp32   ||v_j||_2
- *   seq_lens[B]                    int32  valid keys are j < seq_lens[b]
+ *   seq_lens[B]                    int32  total length n_b of sequence b; local key j
+ *                                         is valid iff index_base + j < n_b (so with
+ *                                         index_base = 0: j < seq_lens[b]).  The
+ *                                         contract is seq_lens[b] - index_base <= N_max
+ *                                         for the calls that append (decode step);
+ *                                         the others clamp to N_max.
  *   mask    [B][N_max]             uint8  optional; 0 = invalid key (Alg. 4 m_j)
  *   scores  [B][H_sel][N_max]      fp32   -inf for invalid keys (Alg. 4)
  *   idx     [B][H_sel][k]          int32  selected keys, ascending; -1 past cnt
@@ -221,13 +243,17 @@ socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, 
 int32_t socket_decode_step_launches(const socket_cfg* cfg);
 
 /* Alg. 3 l.244 TopK with forced sink / local window: per (b, row),
- * with n = seq_lens[b] and valid = (scores != -inf) & (j < n):
- *   k_eff = min(k, #valid); forced F = valid & (j < sink | n - window <= j < n);
+ * with n = seq_lens[b], position p(j) = index_base + j and
+ * valid = (scores != -inf) & (p(j) < n) & (j < N_max):
+ *   k_eff = min(k, #valid); forced F = valid & (p(j) < sink | n - window <= p(j));
  *   S = F plus the (k_eff - |F|) best remaining keys under the total order
  *   (score descending, index ascending) -- ties to the smaller index (R-15).
  * Writes idx[b][row][0..cnt) ascending, -1 after, cnt[b][row] = k_eff, and if
  * sel_scores != NULL, sel_scores[b][row][i] = scores[idx[i]] (-inf past cnt).
- * Requires k <= N_max, sink + window <= k. */
+ * Positions (sink, window) are global (index_base + j).  Requires k <= N_max,
+ * sink + window <= k.  ws: socket_workspace_bytes(cfg, SOCKET_OP_TOPK, k)
+ * bytes -- 0 unless rows exceed 655360 keys (one cluster's shared memory), in
+ * which case the key slices live in ws (4 B per key). */
 socket_status socket_topk(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,
                           int32_t k, int32_t sink, int32_t window, int32_t* idx, int32_t* cnt,
                           float* sel_scores, void* ws, size_t ws_bytes, void* stream);
@@ -272,18 +298,64 @@ socket_status socket_dense_decode(const socket_cfg* cfg, const void* q, const vo
                                   const void* V, const int32_t* seq_lens, void* out, float* lse,
                                   void* ws, size_t ws_bytes, void* stream);
 
-/* Sequence sharding, exact global top-k.  Shard s of G
- * owns keys [s*N_shard, (s+1)*N_shard).  Each shard runs socket_topk locally
- * (k, sel_scores) and the G candidate lists are all-gathered (rank order):
- *   cand_scores [G][B][H_sel][k] fp32, cand_idx [G][B][H_sel][k] int32 (local ids).
- * This call selects, per (b, row), the k best candidates over all shards under
- * (score desc, global index asc) and writes this rank's share:
- *   idx[b][row][0..cnt) = local indices owned by `rank`, ascending; cnt.
- * Equal to the single-device top-k of the concatenated rows (sink = window = 0). */
-socket_status socket_topk_resolve(const socket_cfg* cfg, const float* cand_scores,
-                                  const int32_t* cand_idx, int32_t G, int32_t rank, int32_t k,
-                                  int32_t* idx, int32_t* cnt, void* ws, size_t ws_bytes,
-                                  void* stream);
+/* ------------------------------------------------------------------------ *
+ * Sequence sharding: exact global top-k over G shards (DESIGN.md "Multi-GPU",
+ * SURVEY 8(e) v2).  Shard s (rank s of G) holds the keys at global positions
+ * [index_base_s, index_base_s + N_max) with index_base_s = s * N_max (shards
+ * in rank order), scores from socket_score with the same cfg.index_base, and
+ * seq_lens = the sequences' TOTAL lengths.  The selection equals socket_topk
+ * over the concatenated rows (Alg. 3 l.244, ties to the smaller GLOBAL index,
+ * reading R-15; sink / window on global positions).  Protocol, with an
+ * all-gather (rank order) of each call's output across the shards:
+ *   1. socket_topk_digest  -> digest [B][H_sel][Q][2]             all-gather
+ *   2. socket_topk_bracket (all digests)      -> state [B][H_sel][SOCKET_TOPK_STATE_WORDS]
+ *   3. socket_topk_window  (state)            -> msg   [B][H_sel][SOCKET_TOPK_MSG_WORDS]
+ *                                                                 all-gather
+ *   4. socket_topk_resolve (all msgs, rank)   -> state (resolved or a narrower bracket)
+ *      repeat 3-4 while some row is unresolved (state word 3 == 0); at most 3
+ *      rounds are ever needed, so a fixed 3 rounds is always exact (extra
+ *      rounds on resolved rows are no-ops)
+ *   5. socket_topk_emit    (state)            -> idx (local indices, ascending), cnt
+ * The state and all messages are identical on every rank except the own-shard
+ * quota words, so every rank resolves the same threshold.  Bytes per shard and
+ * row: digest Q*8, message SOCKET_TOPK_MSG_WORDS*4.  ws: as socket_topk.
+ * ------------------------------------------------------------------------ */
+#define SOCKET_MAX_SHARDS 64
+#define SOCKET_TOPK_STATE_WORDS 8
+#define SOCKET_TOPK_MSG_WORDS (8 + 2048)
+
+/* Digest of this shard's row (k = the GLOBAL budget, shards = G): Q pairs
+ * (edge key, #keys with key >= edge), every count exact, on the monotone u32
+ * key image of the scores (invalid 0, forced sink / window 0xFFFFFFFF):
+ *   (1, #valid), (0xFFFFFFFF, #forced), (max regular key + 1, #forced), then
+ *   the lower edges of the 2048-bin histogram bins that hold local ranks
+ *   spread over (0, 2 ceil(k / shards)] and (.., min(k, #valid)].
+ * Unused pairs are (0, 0).  4 <= Q <= 1024. */
+socket_status socket_topk_digest(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,
+                                 int32_t k, int32_t sink, int32_t window, int32_t shards, int32_t Q,
+                                 uint32_t* digest, void* ws, size_t ws_bytes, void* stream);
+/* Bracket [T_lo, T_hi) holding the global threshold key T of every row, from
+ * the G all-gathered digests [G][B][H_sel][Q][2]; writes the initial state. */
+socket_status socket_topk_bracket(const socket_cfg* cfg, const uint32_t* all_digests, int32_t G,
+                                  int32_t Q, int32_t k, uint32_t* state, void* stream);
+/* Window message of this shard for each unresolved row: header (lo, hi,
+ * #keys >= hi, #keys in [lo, hi), mode, shift) and either the bracket's keys
+ * (mode 0, when they fit 2048) or their 2048-bin histogram (mode 1). */
+socket_status socket_topk_window(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,
+                                 int32_t sink, int32_t window, const uint32_t* state, uint32_t* msg,
+                                 void* ws, size_t ws_bytes, void* stream);
+/* Resolve from the G all-gathered messages [G][B][H_sel][SOCKET_TOPK_MSG_WORDS]:
+ * T exact (state word 3 = 1, word 4 = T, word 5 = this rank's quota of keys
+ * == T, word 7 = this rank's #keys > T) or a narrower bracket. */
+socket_status socket_topk_resolve(const socket_cfg* cfg, const uint32_t* all_msgs, int32_t G,
+                                  int32_t rank, uint32_t* state, void* stream);
+/* This shard's share of the selection: keys > T plus its quota of keys == T,
+ * local indices ascending in idx[b][row][0..cnt) (-1 after; row stride k),
+ * sel_scores optional.  A row whose state is unresolved gets cnt = -1. */
+socket_status socket_topk_emit(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,
+                               int32_t k, int32_t sink, int32_t window, const uint32_t* state,
+                               int32_t* idx, int32_t* cnt, float* sel_scores, void* ws,
+                               size_t ws_bytes, void* stream);
 
 /* Message of the calling thread's last non-OK status ("" if none). */
 const char* socket_last_error(void);

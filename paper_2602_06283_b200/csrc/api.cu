@@ -11,6 +11,18 @@ bool fused_step_applies(const socket_cfg& c);
 
 static thread_local std::string g_last_error;
 
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
 void set_error(const std::string& msg) { g_last_error = msg; }
 socket_status fail(socket_status st, const std::string& msg) {
   g_last_error = msg;
@@ -41,6 +53,8 @@ static socket_status validate(const socket_cfg* c) {
     return fail(SOCKET_EINVAL, "unknown group_mode");
   if (c->scoring != SOCKET_SCORING_SOFT && c->scoring != SOCKET_SCORING_HARD)
     return fail(SOCKET_EINVAL, "unknown scoring");
+  if (c->flags & ~SOCKET_FLAG_CHAINED_STEP) return fail(SOCKET_EINVAL, "unknown flags");
+  if (c->index_base < 0) return fail(SOCKET_EINVAL, "index_base must be >= 0");
   return SOCKET_OK;
 }
 
@@ -84,6 +98,9 @@ size_t socket_workspace_bytes(const socket_cfg* c, int32_t op, int32_t k) {
       return align16(decode_workspace_bytes(*c, 1, true));
     case SOCKET_OP_DECODE_STEP:
       return align16(decode_step_workspace_bytes(*c, k > 0 ? k : 1));
+    case SOCKET_OP_TOPK:
+    case SOCKET_OP_RESOLVE:
+      return align16(topk_workspace_bytes(*c));
     default:
       return 0;
   }
@@ -196,6 +213,7 @@ socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, 
   SK_NONNULL(ws);
   if ((k_new == nullptr) != (v_new == nullptr)) return fail(SOCKET_EINVAL, "k_new and v_new must both be set or both NULL");
   if (k_new && !append_last) return fail(SOCKET_EINVAL, "k_new / v_new need append_last");
+  if (cfg->index_base != 0) return fail(SOCKET_EUNSUPPORTED, "decode step: index_base must be 0");
   if (k <= 0) return fail(SOCKET_EINVAL, "k must be >= 1");
   if (k > cfg->N_max) return fail(SOCKET_EINVAL, "k > N_max");
   if (sink < 0 || window < 0 || (long long)sink + window > k)
@@ -211,39 +229,94 @@ int32_t socket_decode_step_launches(const socket_cfg* cfg) {
   return fused_step_applies(*cfg) ? 1 : 4;
 }
 
+static socket_status check_topk_args(int32_t k, int32_t sink, int32_t window) {
+  if (k <= 0) return fail(SOCKET_EINVAL, "k must be >= 1");
+  if (sink < 0 || window < 0 || (long long)sink + window > k)
+    return fail(SOCKET_EINVAL, "need 0 <= sink, window and sink + window <= k");
+  return SOCKET_OK;
+}
+
 socket_status socket_topk(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,
                           int32_t k, int32_t sink, int32_t window, int32_t* idx, int32_t* cnt,
                           float* sel_scores, void* ws, size_t ws_bytes, void* stream) {
-  (void)ws;
-  (void)ws_bytes;
   SK_CHECK(validate(cfg));
   SK_NONNULL(scores);
   SK_NONNULL(seq_lens);
   SK_NONNULL(idx);
   SK_NONNULL(cnt);
-  if (k <= 0) return fail(SOCKET_EINVAL, "k must be >= 1");
+  SK_CHECK(check_topk_args(k, sink, window));
   if (k > cfg->N_max) return fail(SOCKET_EINVAL, "k > N_max");
-  if (sink < 0 || window < 0 || (long long)sink + window > k)
-    return fail(SOCKET_EINVAL, "need 0 <= sink, window and sink + window <= k");
   if (cfg->B == 0) return SOCKET_OK;
-  return launch_topk(*cfg, scores, seq_lens, k, sink, window, idx, cnt, sel_scores, S(stream));
+  return launch_topk(*cfg, scores, seq_lens, k, sink, window, idx, cnt, sel_scores, ws, ws_bytes,
+                     S(stream));
 }
 
-socket_status socket_topk_resolve(const socket_cfg* cfg, const float* cand_scores,
-                                  const int32_t* cand_idx, int32_t G, int32_t rank, int32_t k,
-                                  int32_t* idx, int32_t* cnt, void* ws, size_t ws_bytes,
-                                  void* stream) {
-  (void)ws;
-  (void)ws_bytes;
+socket_status socket_topk_digest(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,
+                                 int32_t k, int32_t sink, int32_t window, int32_t shards, int32_t Q,
+                                 uint32_t* digest, void* ws, size_t ws_bytes, void* stream) {
   SK_CHECK(validate(cfg));
-  SK_NONNULL(cand_scores);
-  SK_NONNULL(cand_idx);
-  SK_NONNULL(idx);
-  SK_NONNULL(cnt);
-  if (G < 1 || rank < 0 || rank >= G) return fail(SOCKET_EINVAL, "need 0 <= rank < G");
+  SK_NONNULL(scores);
+  SK_NONNULL(seq_lens);
+  SK_NONNULL(digest);
+  SK_CHECK(check_topk_args(k, sink, window));
+  if (shards < 1 || shards > SOCKET_MAX_SHARDS) return fail(SOCKET_EINVAL, "shards must be in [1, 64]");
+  if (Q < 4 || Q > 1024) return fail(SOCKET_EINVAL, "Q must be in [4, 1024]");
+  if (cfg->B == 0) return SOCKET_OK;
+  return launch_topk_digest(*cfg, scores, seq_lens, k, sink, window, shards, Q, digest, ws, ws_bytes,
+                            S(stream));
+}
+
+socket_status socket_topk_bracket(const socket_cfg* cfg, const uint32_t* all_digests, int32_t G,
+                                  int32_t Q, int32_t k, uint32_t* state, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(all_digests);
+  SK_NONNULL(state);
+  if (G < 1 || G > SOCKET_MAX_SHARDS) return fail(SOCKET_EINVAL, "G must be in [1, 64]");
+  if (Q < 4 || Q > 1024 || (size_t)2 * G * Q * 4 > 200 * 1024)
+    return fail(SOCKET_EINVAL, "Q must be in [4, 1024] and G * Q <= 25600");
   if (k <= 0) return fail(SOCKET_EINVAL, "k must be >= 1");
   if (cfg->B == 0) return SOCKET_OK;
-  return launch_topk_resolve(*cfg, cand_scores, cand_idx, G, rank, k, idx, cnt, S(stream));
+  return launch_topk_bracket(*cfg, all_digests, G, Q, k, state, S(stream));
+}
+
+socket_status socket_topk_window(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,
+                                 int32_t sink, int32_t window, const uint32_t* state, uint32_t* msg,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(scores);
+  SK_NONNULL(seq_lens);
+  SK_NONNULL(state);
+  SK_NONNULL(msg);
+  if (sink < 0 || window < 0) return fail(SOCKET_EINVAL, "need 0 <= sink, window");
+  if (cfg->B == 0) return SOCKET_OK;
+  return launch_topk_window(*cfg, scores, seq_lens, sink, window, state, msg, ws, ws_bytes, S(stream));
+}
+
+socket_status socket_topk_resolve(const socket_cfg* cfg, const uint32_t* all_msgs, int32_t G,
+                                  int32_t rank, uint32_t* state, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(all_msgs);
+  SK_NONNULL(state);
+  if (G < 1 || G > SOCKET_MAX_SHARDS || rank < 0 || rank >= G)
+    return fail(SOCKET_EINVAL, "need 1 <= G <= 64 and 0 <= rank < G");
+  if (cfg->B == 0) return SOCKET_OK;
+  return launch_topk_resolve(*cfg, all_msgs, G, rank, state, S(stream));
+}
+
+socket_status socket_topk_emit(const socket_cfg* cfg, const float* scores, const int32_t* seq_lens,
+                               int32_t k, int32_t sink, int32_t window, const uint32_t* state,
+                               int32_t* idx, int32_t* cnt, float* sel_scores, void* ws,
+                               size_t ws_bytes, void* stream) {
+  SK_CHECK(validate(cfg));
+  SK_NONNULL(scores);
+  SK_NONNULL(seq_lens);
+  SK_NONNULL(state);
+  SK_NONNULL(idx);
+  SK_NONNULL(cnt);
+  SK_CHECK(check_topk_args(k, sink, window));
+  if (cfg->B == 0) return SOCKET_OK;
+  return launch_topk_emit(*cfg, scores, seq_lens, k, sink, window, state, idx, cnt, sel_scores, ws,
+                          ws_bytes, S(stream));
 }
 
 socket_status socket_sparse_decode(const socket_cfg* cfg, const void* q, const void* K,
@@ -290,6 +363,7 @@ socket_status socket_sample_decode(const socket_cfg* cfg, const float* scores, c
   SK_NONNULL(seq_lens);
   SK_NONNULL(uniforms);
   SK_NONNULL(out);
+  if (cfg->index_base != 0) return fail(SOCKET_EUNSUPPORTED, "sample decode: index_base must be 0");
   return launch_sample_decode(*cfg, scores, vnorm, V, seq_lens, uniforms, M, samples, out, S(stream));
 }
 

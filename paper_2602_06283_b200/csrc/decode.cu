@@ -84,10 +84,10 @@ static void decode_geometry(const socket_cfg& c, int k, bool dense, int& units, 
   const int H_sel = per_q ? c.H_q : c.H_kv;
   units = c.B * H_sel;
   NH = per_q ? 1 : c.H_q / c.H_kv;
-  const char* tune = getenv("SOCKET_DECODE_TARGET");   // tuning experiments only
-  // ~0.86 of one wave at 2 CTAs per SM: a single wave of balanced splits was the
-  // fastest geometry in tools/tune_step.py sweeps (B 4-16, 5x-10x, 32K)
-  const int target = tune ? atoi(tune) : 256;
+  // ~0.86 of one wave at 2 CTAs per SM (256 CTAs on 148 SMs): a single wave of
+  // balanced splits was the fastest geometry in tools/tune_step.py sweeps
+  // (B 4-16, 5x-10x, 32K)
+  const int target = num_sms() * 173 / 100;
   pick_splits(units, dense ? c.N_max : k, kMmaGran, kMmaMaxRps, target, n_splits, rps);
 }
 

@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
         for (int e2 = 0; e2 < 8; ++e2) ws[(cw * 8 + e2) * kFWs + w] = (e2 & 1) ? bf16hi(w4[e2 >> 1]) : bf16lo(w4[e2 >> 1]);
       }
     }
-    const bool app = a.do_append && n > 0;
+    const bool app = a.do_append && n > 0 && n <= a.N_max;   // outgrown cache: no write
     if (app && tid < kD) {
       const size_t crow = (((size_t)b * a.H_kv + g) * a.N_max + n - 1) * kD;
       if (a.k_new) {   // the new rows come from k_new / v_new; CTA 0 stores them in the cache
@@ -384,7 +384,8 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
   FU_STAMP(5);
   // ===== C. exact top-k over the cluster =============================================
   TopkArgs ta = {};
-  ta.mode = 0;
+  ta.op = 0;
+  ta.index_base = 0;
   ta.scores = a.scores;
   ta.seq_lens = a.seq_lens;
   ta.rows = (int)gridDim.y;
@@ -589,7 +590,7 @@ static bool fused_geometry(const socket_cfg& c, int& CS, int& S) {
   for (int cs : {8, 4}) {   // clusters of 16 do not all fit one wave
     if (c.N_max % (cs * 128) != 0) continue;
     const int s = c.N_max / cs;
-    if (s > 8192 || rows * cs > kNumSMs) continue;
+    if (s > 8192 || rows * cs > num_sms()) continue;
     if ((Lp + cs - 1) / cs * c.P > 64) continue;   // <= 64 W rows per CTA (staging, 8 DMMA warps)
     CS = cs;
     S = s;
@@ -600,7 +601,7 @@ static bool fused_geometry(const socket_cfg& c, int& CS, int& S) {
 
 bool fused_step_applies(const socket_cfg& c) {
   int CS, S;
-  if (getenv("SOCKET_NO_FUSED")) return false;
+  if (c.flags & SOCKET_FLAG_CHAINED_STEP) return false;
   return fused_geometry(c, CS, S);
 }
 

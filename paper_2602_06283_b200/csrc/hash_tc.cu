@@ -4,30 +4,22 @@
 // then sign -> bit i of table l (R-3, R-4) and a byte per (key, table) in the
 // bank-rotated code layout.
 //
-// Persistent CTA (128 threads = 4 warps, one CTA per SM):
-//   * W (Lp tables x 8 rows, rows i >= P and tables l >= L zero) stays resident
-//     in shared memory in the canonical no-swizzle K-major core-matrix layout:
-//       byte(row n, element d) = ((d / 8) * (NC / 8) + n / 8) * 128 + (n % 8) * 16 + (d % 8) * 2
-//     (core matrix = 8 rows x 16 B; SBO = 128 B between 8-row groups, LBO =
-//     NC/8 * 128 B between the two 8-element K chunks of one MMA);
-//   * 128-key tiles of K are double-buffered into the same layout by cp.async;
-//   * thread 0 issues 8 k-steps x (NC / 256) tcgen05.mma (M = 128, N <= 256,
-//     K = 16) into a TMEM accumulator of NC fp32 columns (lane = key) and
-//     commits to an mbarrier;
-//   * the 4 warps read their 32 TMEM lanes (tcgen05.ld.32x32b.x32), take the
-//     signs, and write the code bytes (rotated slots) into a shared staging
-//     tile that is copied out with 16-byte stores.
+// Persistent, warp-specialized CTA (one per SM), described at the kernel
+// below; W (Lp tables x 8 rows, rows i >= P and tables l >= L zero) stays
+// resident in shared memory in the canonical no-swizzle K-major core-matrix
+// layout:
+//   byte(row n, element d) = ((d / 8) * (NC / 8) + n / 8) * 128 + (n % 8) * 16 + (d % 8) * 2
+// (core matrix = 8 rows x 16 B; SBO = 128 B between 8-row groups, LBO =
+// NC/8 * 128 B between the two 8-element K chunks of one MMA).
 // fp32 accumulation order differs from the CUDA-core path, so bits whose
 // projection is within rounding of 0 may differ; both are checked against the
 // fp64 oracle under the margin rule (tests/test_gpu_parity.py).
 #include <cuda.h>
-#include <cstdlib>
 
 #include "internal.cuh"
 
 namespace sk {
 
-constexpr int kTcThreads = 128;
 constexpr int kTcM = 128;                     // keys per tile (UMMA_M)
 constexpr int kTcK = kD;                      // 128 = 8 k-steps of 16
 
@@ -59,161 +51,8 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   return d;                                        // base offset 0, layout SWIZZLE_NONE
 }
 
-template <int NC>
-__global__ void __launch_bounds__(kTcThreads, 1)
-hash_keys_tc_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict__ W,
-                    uint8_t* __restrict__ codes, int BH, int N_max, int L, int P, int n_begin,
-                    int n_end) {
-  constexpr int LP = NC / 8;                       // code slots per key
-  constexpr int MMA_N = NC < 256 ? NC : 256;
-  constexpr int NHALF = NC / MMA_N;
-  constexpr uint32_t W_BYTES = NC * kTcK * 2;
-  constexpr uint32_t A_BYTES = kTcM * kTcK * 2;    // 32 KB
-  constexpr int CB = LP < 16 ? LP : 16;
-  constexpr int NCH = LP / CB;
-  constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MMA_N >> 3) << 17) |
-                             ((uint32_t)(kTcM >> 4) << 24);
-  extern __shared__ __align__(1024) char smem[];
-  char* sW = smem;
-  char* sA = smem + W_BYTES;                       // 2 buffers
-  uint8_t* stage = reinterpret_cast<uint8_t*>(smem + W_BYTES + 2 * A_BYTES);   // kTcM * LP bytes
-  __shared__ uint64_t mma_bar;
-  __shared__ uint32_t tmem_base_sh;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  // ---- one-time setup: W resident in smem, TMEM allocation, mbarrier --------
-  const uint32_t sW_u = smem_u32(sW), sA_u = smem_u32(sA);
-  for (int c = tid; c < NC * (kTcK / 8); c += kTcThreads) {   // 16-byte chunks of W^T rows
-    const int n = c / (kTcK / 8), kc = c % (kTcK / 8);
-    const int l = n >> 3, i = n & 7;
-    const bool v = l < L && i < P;
-    const uint16_t* src = W + ((size_t)(v ? l : 0) * P + (v ? i : 0)) * kD + kc * 8;
-    tc_cp16(sW_u + (uint32_t)((kc * (NC / 8) + (n >> 3)) * 128 + (n & 7) * 16), src, v);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_base_sh)),
-                 "n"(NC < 32 ? 32 : NC));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) tc_mbar_init(&mma_bar, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = tmem_base_sh;
-
-  const int tiles_per_row = (N_max + kTcM - 1) / kTcM;
-  const int t_lo = n_begin / kTcM, t_hi = (n_end - 1) / kTcM;      // tile range inside a row
-  const int tiles_in_range = t_hi - t_lo + 1;
-  const long long total = (long long)BH * tiles_in_range;
-  (void)tiles_per_row;
-
-  auto issue_A = [&](long long t, int buf) {
-    const int bh = (int)(t / tiles_in_range), tile = t_lo + (int)(t % tiles_in_range);
-    const uint16_t* Kb = K + ((size_t)bh * N_max + (size_t)tile * kTcM) * kD;
-    const uint32_t dst = sA_u + buf * A_BYTES;
-    for (int c = tid; c < kTcM * (kTcK / 8); c += kTcThreads) {   // 2048 chunks
-      const int r = c / (kTcK / 8), kc = c % (kTcK / 8);
-      const bool v = tile * kTcM + r < N_max;
-      tc_cp16(dst + (uint32_t)((kc * (kTcM / 8) + (r >> 3)) * 128 + (r & 7) * 16),
-              Kb + (size_t)(v ? r : 0) * kD + kc * 8, v);
-    }
-  };
-
-  long long t = blockIdx.x;
-  if (t < total) issue_A(t, 0);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  uint32_t phase = 0;
-  int buf = 0;
-  for (; t < total; t += gridDim.x) {
-    const long long tn = t + gridDim.x;
-    if (tn < total) issue_A(tn, buf ^ 1);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");     // W and tile t have landed
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    // ---- MMA: X = K_tile . W^T (single issuing thread) -------------------------
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-      for (int ks = 0; ks < kTcK / 16; ++ks) {
-        const uint64_t ad = umma_desc(sA_u + buf * A_BYTES + ks * 2 * (kTcM / 8) * 128,
-                                      (kTcM / 8) * 128, 128);
-#pragma unroll
-        for (int hf = 0; hf < NHALF; ++hf) {
-          const uint64_t bd = umma_desc(sW_u + ks * 2 * (NC / 8) * 128 + hf * (MMA_N / 8) * 128,
-                                        (NC / 8) * 128, 128);
-          const uint32_t acc = ks > 0 ? 1u : 0u;
-          asm volatile(
-              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + hf * MMA_N),
-              "l"(ad), "l"(bd), "r"(IDESC), "r"(acc));
-        }
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(&mma_bar))
-                   : "memory");
-    }
-    tc_mbar_wait(&mma_bar, phase);
-    phase ^= 1;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // ---- epilogue: TMEM -> signs -> code bytes --------------------------------
-    const int bh = (int)(t / tiles_in_range), tile = t_lo + (int)(t % tiles_in_range);
-    const int r = warp * 32 + lane;                  // key row of this thread (TMEM lane)
-    const int j = tile * kTcM + r;                   // row-local key index
-    constexpr int MM = (LP < 32 ? LP : 32) - 1;
-#pragma unroll 1
-    for (int c0 = 0; c0 < NC; c0 += 32) {            // 4 tables per load
-      uint32_t v[32];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-            "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
-            "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
-            "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-          : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int l = c0 / 8 + q;
-        uint32_t code = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (i < P) code |= (__uint_as_float(v[q * 8 + i]) >= 0.f ? 1u : 0u) << i;   // sign(0)=+1
-        if (l >= L) code = 0;
-        const int s = (l & ~MM) | ((l - j) & MM);     // slot of table l for key j
-        stage[((r >> 5) * NCH + s / CB) * (32 * CB) + (r & 31) * CB + (s % CB)] = (uint8_t)code;
-      }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();                                 // staging complete, TMEM free
-    // ---- copy out: thread per (key, chunk) of CB bytes, in-range keys only ---
-    uint8_t* cbase = codes + (size_t)bh * N_max * LP + (size_t)tile * kTcM * LP;
-    for (int x = tid; x < kTcM * NCH; x += kTcThreads) {
-      const int ch = x / kTcM, rr = x % kTcM;
-      const int jj = tile * kTcM + rr;
-      if (jj < n_begin || jj >= n_end) continue;
-      const int off = ((rr >> 5) * NCH + ch) * (32 * CB) + (rr & 31) * CB;
-      if constexpr (CB == 16) *reinterpret_cast<uint4*>(cbase + off) = *reinterpret_cast<const uint4*>(stage + off);
-      else *reinterpret_cast<uint2*>(cbase + off) = *reinterpret_cast<const uint2*>(stage + off);
-    }
-    __syncthreads();                                 // staging reusable; buffer `buf` free
-    buf ^= 1;
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "n"(NC < 32 ? 32 : NC));
-}
-
 // ----------------------------------------------------------------------------
-// v2: warp-specialized, MMA overlapped with the epilogue.
+// Warp-specialized, MMA overlapped with the epilogue.
 //   warp 0 (1 lane): TMA producer -- 16 tensor-map box loads {8 elems, 128 rows}
 //                    per 128-key tile land each K chunk directly in the
 //                    core-matrix layout; 2-stage ring (full/empty mbarriers);
@@ -459,7 +298,7 @@ static socket_status launch_hash_keys_tc2(const socket_cfg& c, const void* K, co
     return SOCKET_OK;
   const int t_lo = n_begin / kTcM, t_hi = (n_begin + n_count - 1) / kTcM;
   const long long total = (long long)c.B * c.H_kv * (t_hi - t_lo + 1);
-  const int grid = (int)(total < kNumSMs ? total : kNumSMs);
+  const int grid = (int)(total < num_sms() ? total : num_sms());
   const size_t smem = (size_t)NC * kTcK * 2 + 2 * (size_t)kTcM * kTcK * 2 + 2 * (size_t)kTcM * Lp;
 #define SK_TC2(NCV)                                                                                 \
   case NCV: {                                                                                       \
@@ -491,34 +330,7 @@ socket_status launch_hash_keys_tc(const socket_cfg& c, const void* K, const void
   const int Lp = code_slots(c.L);
   const int NC = Lp * 8;
   if (NC > 512 || n_count < kTcM) return SOCKET_OK;    // CUDA-core path
-  if (!getenv("SOCKET_HASH_TC_V1")) {
-    socket_status s2 = launch_hash_keys_tc2(c, K, W, codes, n_begin, n_count, st, used);
-    if (s2 != SOCKET_OK || *used) return s2;
-  }
-  const int t_lo = n_begin / kTcM, t_hi = (n_begin + n_count - 1) / kTcM;
-  const long long total = (long long)c.B * c.H_kv * (t_hi - t_lo + 1);
-  const int grid = (int)(total < kNumSMs ? total : kNumSMs);
-  const size_t smem = (size_t)NC * kTcK * 2 + 2 * (size_t)kTcM * kTcK * 2 + (size_t)kTcM * Lp;
-#define SK_TC(NCV)                                                                                  \
-  case NCV: {                                                                                       \
-    cudaFuncSetAttribute(hash_keys_tc_kernel<NCV>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                         (int)smem);                                                                \
-    hash_keys_tc_kernel<NCV><<<grid, kTcThreads, smem, st>>>((const uint16_t*)K, (const uint16_t*)W, \
-                                                             codes, c.B * c.H_kv, c.N_max, c.L,    \
-                                                             c.P, n_begin, n_begin + n_count);     \
-    break;                                                                                          \
-  }
-  switch (NC) {
-    SK_TC(64)
-    SK_TC(128)
-    SK_TC(256)
-    SK_TC(512)
-    default:
-      return SOCKET_OK;
-  }
-#undef SK_TC
-  *used = true;
-  return check_launch("hash_keys_tc_kernel");
+  return launch_hash_keys_tc2(c, K, W, codes, n_begin, n_count, st, used);
 }
 
 }  // namespace sk

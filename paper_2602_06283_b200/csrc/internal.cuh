@@ -18,7 +18,9 @@ socket_status fail(socket_status st, const std::string& msg);
 socket_status check_launch(const char* what);
 
 constexpr int kD = 128;           // head dim supported by every kernel
-constexpr int kNumSMs = 148;      // B200
+// SM count of the current device (queried once per device; MIG / green
+// contexts report their own count)
+int num_sms();
 constexpr int kLutPanelCols = 64; // LUT row = 64 fp32 columns = 256 B
 constexpr int kLutRows = 256;     // 2^P rows for P <= 8
 
@@ -68,10 +70,22 @@ socket_status launch_score(const socket_cfg& c, const float* lut, const uint8_t*
                            float* scores, cudaStream_t st);
 socket_status launch_topk(const socket_cfg& c, const float* scores, const int32_t* seq_lens,
                           int k, int sink, int window, int32_t* idx, int32_t* cnt,
-                          float* sel_scores, cudaStream_t st);
-socket_status launch_topk_resolve(const socket_cfg& c, const float* cand_scores,
-                                  const int32_t* cand_idx, int G, int rank, int k, int32_t* idx,
-                                  int32_t* cnt, cudaStream_t st);
+                          float* sel_scores, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t topk_workspace_bytes(const socket_cfg& c);
+socket_status launch_topk_digest(const socket_cfg& c, const float* scores, const int32_t* seq_lens,
+                                 int k, int sink, int window, int shards, int Q, uint32_t* digest,
+                                 void* ws, size_t ws_bytes, cudaStream_t st);
+socket_status launch_topk_bracket(const socket_cfg& c, const uint32_t* digests, int G, int Q, int k,
+                                  uint32_t* state, cudaStream_t st);
+socket_status launch_topk_window(const socket_cfg& c, const float* scores, const int32_t* seq_lens,
+                                 int sink, int window, const uint32_t* state, uint32_t* msg,
+                                 void* ws, size_t ws_bytes, cudaStream_t st);
+socket_status launch_topk_resolve(const socket_cfg& c, const uint32_t* msgs, int G, int rank,
+                                  uint32_t* state, cudaStream_t st);
+socket_status launch_topk_emit(const socket_cfg& c, const float* scores, const int32_t* seq_lens,
+                               int k, int sink, int window, const uint32_t* state, int32_t* idx,
+                               int32_t* cnt, float* sel_scores, void* ws, size_t ws_bytes,
+                               cudaStream_t st);
 size_t decode_workspace_bytes(const socket_cfg& c, int k, bool dense);
 socket_status launch_decode(const socket_cfg& c, const void* q, const void* K, const void* V,
                             const int32_t* idx, const int32_t* cnt, int k,
@@ -156,6 +170,13 @@ __device__ __forceinline__ uint2 ldg_nc_v2(const void* p) {
                : "=r"(r.x), "=r"(r.y)
                : "l"(p));
   return r;
+}
+
+// keys of a buffer at global positions index_base + j are valid iff
+// index_base + j < seq_len (socket_cfg.index_base); local valid count:
+__device__ __forceinline__ int local_len(int seq_len, long long index_base, int N_max) {
+  const long long n = (long long)seq_len - index_base;
+  return n < 0 ? 0 : (n > N_max ? N_max : (int)n);
 }
 
 // monotone map fp32 -> u32 (larger float <=> larger key)

@@ -14,6 +14,8 @@
 // griddepcontrol.wait before it reads its predecessor's output, so its launch
 // and prologue overlap the predecessor's tail.  Inside a CUDA graph the edges
 // become programmatic dependencies.
+#include <algorithm>
+
 #include "step_dev.cuh"
 
 namespace sk {
@@ -37,7 +39,7 @@ socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint
                                float* scores, cudaStream_t st, bool pdl);
 socket_status launch_topk_pdl(const socket_cfg& c, const float* scores, const int32_t* seq_lens,
                               int k, int sink, int window, int32_t* idx, int32_t* cnt,
-                              float* sel_scores, cudaStream_t st, bool pdl);
+                              float* sel_scores, cudaStream_t st, bool pdl, void* ws, size_t ws_bytes);
 socket_status launch_decode_pdl(const socket_cfg& c, const void* q, const void* K, const void* V,
                                 const int32_t* idx, const int32_t* cnt, int k, void* out,
                                 float* lse, void* ws, size_t ws_bytes, cudaStream_t st, bool pdl,
@@ -94,12 +96,7 @@ static size_t stage_bytes(const socket_cfg& c) {
   return (((size_t)c.B * c.H_q * kD + 2 * (size_t)c.B * c.H_kv * kD) * 2 + 255) & ~(size_t)255;
 }
 
-#ifndef SK_STAGE_T
-#define SK_STAGE_T 256
-#endif
-#ifndef SK_STAGE_NEW
-#define SK_STAGE_NEW 1    // 0: the append tiles read host k_new / v_new in place
-#endif
+constexpr int kStageThreads = 256;
 __global__ void __launch_bounds__(256) stage_inputs_kernel(const uint4* q_h, const uint4* k_h,
                                                            const uint4* v_h, uint4* dst, int nq, int nk) {
   const int n = nq + 2 * nk;
@@ -121,7 +118,8 @@ static bool host_resident(const void* p) {
 
 size_t decode_step_workspace_bytes(const socket_cfg& c, int k) {
   const size_t lut = ((size_t)c.B * num_sel_rows(c) * lut_row_bytes(c) + 255) & ~(size_t)255;
-  return lut + ((decode_workspace_bytes(c, k, false) + 255) & ~(size_t)255) + stage_bytes(c);
+  return lut + ((decode_workspace_bytes(c, k, false) + 255) & ~(size_t)255) + stage_bytes(c) +
+         topk_workspace_bytes(c);
 }
 
 bool decode_step_stages_inputs(const socket_cfg& c, const void* q, const void* k_new, const void* v_new) {
@@ -155,11 +153,11 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, vo
   if (staged) {
     const int nq = c.B * c.H_q * kD / 8, nk = c.B * c.H_kv * kD / 8;   // 16-B chunks
     uint16_t* stage = reinterpret_cast<uint16_t*>(static_cast<char*>(dws) + dws_bytes);
-    const bool has_new = SK_STAGE_NEW && k_new != nullptr && v_new != nullptr;
+    const bool has_new = k_new != nullptr && v_new != nullptr;
     const int nk_used = has_new ? nk : 0;
     const int n = nq + 2 * nk_used;
-    const int blocks = (n + SK_STAGE_T - 1) / SK_STAGE_T < 2 * kNumSMs ? (n + SK_STAGE_T - 1) / SK_STAGE_T : 2 * kNumSMs;
-    stage_inputs_kernel<<<blocks, SK_STAGE_T, 0, st>>>(static_cast<const uint4*>(q),
+    const int blocks = std::min((n + kStageThreads - 1) / kStageThreads, 2 * num_sms());
+    stage_inputs_kernel<<<blocks, kStageThreads, 0, st>>>(static_cast<const uint4*>(q),
                                                 static_cast<const uint4*>(k_new),
                                                 static_cast<const uint4*>(v_new),
                                                 reinterpret_cast<uint4*>(stage), nq, nk_used);
@@ -203,7 +201,9 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, vo
   // ---- score, top-k, decode (PDL chain) ----------------------------------------
   s = launch_score_pdl(c, lut, codes, vnorm, seq_lens, mask, scores, st, true);
   if (s != SOCKET_OK) return s;
-  s = launch_topk_pdl(c, scores, seq_lens, k, sink, window, idx, cnt, nullptr, st, true);
+  const size_t tws_bytes = topk_workspace_bytes(c);   // key slices of rows > 655360 keys
+  void* tws = static_cast<char*>(dws) + dws_bytes + stage_bytes(c);
+  s = launch_topk_pdl(c, scores, seq_lens, k, sink, window, idx, cnt, nullptr, st, true, tws, tws_bytes);
   if (s != SOCKET_OK) return s;
   return launch_decode_pdl(c, q, K, V, idx, cnt, k, out, lse, dws, dws_bytes, st, true, nullptr,
                            nullptr);

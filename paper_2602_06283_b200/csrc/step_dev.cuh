@@ -386,7 +386,7 @@ __device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, ch
       j = a.n_begin + kk % a.n_count;
       if (a.append_last) {               // decode step: the newest key j = seq_lens[b] - 1
         const int n = a.seq_lens[bh / a.H_kv];
-        j = n > 0 ? n - 1 : -1;
+        j = (n > 0 && n <= a.N_max) ? n - 1 : -1;   // a cache that outgrew N_max: no write
       }
     }
     kj[tid] = j;

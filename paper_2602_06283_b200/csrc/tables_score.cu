@@ -8,7 +8,7 @@
 //   score kernel's shared-memory image ("LUT"): panels of [256 rows][64 cols]
 //   fp32 where column c holds table c (Lp >= 32) or table c mod Lp (Lp < 32).
 //
-// score_kernel: streams the tiled codes with 128-bit loads, lane = key j mod
+// score_reg_kernel: streams the tiled codes with 128-bit loads, lane = key j mod
 // 32.  At slot step s lane l reads LUT column (s & 32) | ((s + l) & 31), so the
 // 32 lanes hit 32 distinct banks (conflict-free).
 #include "step_dev.cuh"
@@ -32,131 +32,6 @@ socket_status launch_query_tables(const socket_cfg& c, const void* q, const void
 // ----------------------------------------------------------------------------
 constexpr int kScoreThreads = 512;            // 16 warps, one CTA per SM (persistent)
 constexpr int kScoreWarps = kScoreThreads / 32;
-constexpr int kScoreStages = 4;               // per-warp cp.async ring depth (tiles)
-
-// Score kernel: persistent CTAs, each over a contiguous range of 32-key tiles
-// of the (row, tile) space; a row change reloads the row's LUT image (TMA bulk
-// copy + mbarrier).  Lane l of a warp scores key j = 32 t + l of tile t: at
-// slot step s it reads LUT column c(s, l) = (s & 32) | ((s + l) & 31) (bank
-// (s + l) mod 32: all 32 lanes on distinct banks).  The byte offset
-// code * 256 + 4 c(s, l) is one PRMT of the code word with a per-lane packed
-// column-offset register (two slots per register, upper bytes zero).
-template <int LP>
-__global__ void __launch_bounds__(kScoreThreads, 1)
-score_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
-             const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
-             const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
-             int G_sel, int N_max, long long total_tiles) {
-  extern __shared__ __align__(128) char smem[];
-  __shared__ uint64_t bar;
-  constexpr int PANELS = LP <= 64 ? 1 : (LP + 63) / 64;
-  constexpr uint32_t LUT_BYTES = PANELS * 256 * 64 * 4;
-  using TS = TileStage<LP>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t ring = smem_u32(smem + LUT_BYTES) + (uint32_t)warp * (kScoreStages * TS::BYTES);
-  const char* ringp = smem + LUT_BYTES + warp * (kScoreStages * TS::BYTES);
-  // packed column offsets: pk[m] = {4 c(2m, l), 4 c(2m+1, l), 0, 0} for slots 0..31
-  uint32_t pk[16];
-#pragma unroll
-  for (int m = 0; m < 16; ++m)
-    pk[m] = (uint32_t)(((2 * m + lane) & 31) << 2) | ((uint32_t)(((2 * m + 1 + lane) & 31) << 2) << 8);
-  const int tiles_per_row = N_max >> 5;
-  const long long t_begin = total_tiles * blockIdx.x / gridDim.x;
-  const long long t_end = total_tiles * (blockIdx.x + 1) / gridDim.x;
-  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: LUT / codes of the predecessor
-  if (threadIdx.x == 0) mbar_init(&bar, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-  uint32_t phase = 0;
-  long long t = t_begin;
-  while (t < t_end) {
-    const int row = (int)(t / tiles_per_row);
-    const long long row_end = (long long)(row + 1) * tiles_per_row;
-    const long long seg_end = row_end < t_end ? row_end : t_end;
-    const int b = row / H_sel, r = row % H_sel;
-    const int g = r / G_sel;                       // kv head of this selection row
-    const int n = seq_lens[b];
-    const int valid_tiles = (n + 31) >> 5;
-    const int tile0 = (int)(t - (long long)row * tiles_per_row);
-    const int tile1 = (int)(seg_end - (long long)row * tiles_per_row);
-    const int vt1 = tile1 < valid_tiles ? tile1 : valid_tiles;   // tiles that need codes
-    const bool need_lut = tile0 < vt1;
-    if (need_lut && threadIdx.x == 0) {
-      mbar_expect_tx(&bar, LUT_BYTES);
-      const char* src = reinterpret_cast<const char*>(lut_g) + (size_t)row * LUT_BYTES;
-      constexpr uint32_t kChunk = 32768;
-#pragma unroll
-      for (uint32_t off = 0; off < LUT_BYTES; off += kChunk) bulk_g2s(smem + off, src + off, kChunk, &bar);
-    }
-    const uint8_t* crow = codes + ((size_t)b * H_kv + g) * N_max * LP;
-    const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
-    const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
-    float* srow = scores + (size_t)row * N_max;
-    // tiles of this warp that need codes: tile0 + warp + 16 i < vt1
-    const int first = tile0 + warp;
-    const int my = first < vt1 ? (vt1 - first + kScoreWarps - 1) / kScoreWarps : 0;
-#pragma unroll
-    for (int s2 = 0; s2 < kScoreStages - 1; ++s2) {
-      if (s2 < my) {
-        const int ti = first + s2 * kScoreWarps;
-        issue_tile<LP>(ring + s2 * TS::BYTES, crow + (size_t)ti * 32 * LP, vrow + ti * 32, lane);
-      }
-      cpa_commit();
-    }
-    if (need_lut) mbar_wait(&bar, phase);
-    for (int i = 0; i < my; ++i) {
-      const int inext = i + kScoreStages - 1;
-      if (inext < my) {
-        const int ti = first + inext * kScoreWarps;
-        issue_tile<LP>(ring + (inext % kScoreStages) * TS::BYTES, crow + (size_t)ti * 32 * LP,
-                       vrow + ti * 32, lane);
-      }
-      cpa_commit();
-      cpa_wait<kScoreStages - 1>();
-      const char* st = ringp + (i % kScoreStages) * TS::BYTES;
-      uint32_t w[LP / 4];
-#pragma unroll
-      for (int ch = 0; ch < TS::NCH; ++ch) {
-        if constexpr (TS::CB == 16) {
-          const uint4 v = *reinterpret_cast<const uint4*>(st + ch * 512 + lane * 16);
-          w[ch * 4 + 0] = v.x; w[ch * 4 + 1] = v.y; w[ch * 4 + 2] = v.z; w[ch * 4 + 3] = v.w;
-        } else {
-          const uint2 v = *reinterpret_cast<const uint2*>(st + ch * 256 + lane * 8);
-          w[ch * 2 + 0] = v.x; w[ch * 2 + 1] = v.y;
-        }
-      }
-      const float vn = *reinterpret_cast<const float*>(st + TS::CODE_BYTES + lane * 4);
-      // even slots accumulate in .x, odd slots in .y (one packed FADD2 per pair)
-      uint64_t acc = 0ull;
-#pragma unroll
-      for (int s2 = 0; s2 < LP; s2 += 2) {
-        float v[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int ss = s2 + u, sl = ss & 31;
-          const uint32_t sel = (uint32_t)(4 + (sl & 1)) | ((uint32_t)(ss & 3) << 4) | 0x7600u;
-          const uint32_t addr = __byte_perm(w[ss >> 2], pk[sl >> 1], sel);   // code*256 + 4 c
-          v[u] = *reinterpret_cast<const float*>(smem + (size_t)(ss >> 6) * (256 * 64 * 4) +
-                                                 ((ss & 32) ? 128 : 0) + addr);
-        }
-        const uint64_t pv = (uint64_t)__float_as_uint(v[0]) | ((uint64_t)__float_as_uint(v[1]) << 32);
-        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(pv));
-      }
-      const float acc0 = __uint_as_float((uint32_t)acc), acc1 = __uint_as_float((uint32_t)(acc >> 32));
-      const int ti = first + i * kScoreWarps;
-      const int j = ti * 32 + lane;
-      const bool ok = j < n && (!mrow || mrow[j]);
-      srow[j] = ok ? vn * (acc0 + acc1) : -INFINITY;
-    }
-    // tiles past seq_len (no codes needed): -inf
-    for (int ti = (vt1 > tile0 ? vt1 : tile0) + warp; ti < tile1; ti += kScoreWarps)
-      srow[ti * 32 + lane] = -INFINITY;
-    cpa_wait<0>();
-    if (need_lut) phase ^= 1;
-    __syncthreads();   // everyone done with this LUT before it is overwritten
-    t = seg_end;
-  }
-}
 
 // ----------------------------------------------------------------------------
 // wide-code score kernel (P > 8, NEXT-2): codes are uint16, the LUT image holds
@@ -173,7 +48,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
 score_wide_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ codes,
                   const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
                   const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
-                  int G_sel, int N_max, int Lp, int P, int E, int row_floats) {
+                  int G_sel, int N_max, int Lp, int P, int E, int row_floats, long long index_base) {
   extern __shared__ __align__(16) float wlut[];
   const int row = blockIdx.y;
   const int b = row / H_sel, r = row % H_sel, g = r / G_sel;
@@ -183,7 +58,7 @@ score_wide_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ 
   for (int i = threadIdx.x; i < row_floats / 4; i += kWideThreads)
     reinterpret_cast<float4*>(wlut)[i] = src[i];
   __syncthreads();
-  const int n = seq_lens[b];
+  const int n = local_len(seq_lens[b], index_base, N_max);
   const int Pl = P / 2;
   const uint32_t lomask = (1u << Pl) - 1u;
   const int CB = Lp < 16 ? Lp : 16;
@@ -230,18 +105,13 @@ score_wide_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ 
 // from the half-table image, so a lookup is one conflict-free LDS as in the
 // byte-code kernel; the CTA sweeps its keys once per group, keeping the first
 // group's partial sums in shared memory.
-#ifndef SK_WIDE_KU
-#define SK_WIDE_KU 2
-#endif
-#ifndef SK_WIDE_PIPE
-#define SK_WIDE_PIPE 1
-#endif
 template <int NH>
 __global__ void __launch_bounds__(kWideThreads, 1)
 score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ codes,
                    const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
                    const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
-                   int G_sel, int N_max, int Lp, int P, int E, int row_floats, long long total_tiles) {
+                   int G_sel, int N_max, int Lp, int P, int E, int row_floats, long long total_tiles,
+                   long long index_base) {
   extern __shared__ __align__(16) float w2[];
   const int R = 1 << P, Pl = P / 2, RL = 1 << Pl;
   float* tab = w2;                          // [R][32]
@@ -263,7 +133,7 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
     const int t1 = (int)(seg_end - (long long)row * tiles_per_row);
     t = seg_end;
     const int b = row / H_sel, r = row % H_sel, g = r / G_sel;
-    const int n = seq_lens[b];
+    const int n = local_len(seq_lens[b], index_base, N_max);
     const uint16_t* crow = codes + ((size_t)b * H_kv + g) * N_max * Lp;
     const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
     const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
@@ -293,7 +163,7 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
       __syncthreads();
       // sweep: lane = key, slots gi*32 .. gi*32 + 31 (two 16-element chunks); the
       // first group's partial sum is parked in `scores` (the same thread reads it back)
-      constexpr int kU = SK_WIDE_KU;          // tiles per batch per warp
+      constexpr int kU = 2;                   // tiles per batch per warp
       constexpr int kStep = kU * (kWideThreads / 32);
       const bool last = gi + 1 == groups;
       struct Batch {
@@ -349,7 +219,6 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
           }
         }
       };
-#if SK_WIDE_PIPE
       // two batches per warp: the next batch's loads are in flight while the
       // current one is looked up
       Batch A, Bn;
@@ -362,13 +231,6 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
         if (ti0 + 2 * kStep < vt1) load(A, ti0 + 2 * kStep);
         compute(Bn, ti0 + kStep);
       }
-#else
-      for (int ti0 = t0 + warp; ti0 < vt1; ti0 += kStep) {
-        Batch A;
-        load(A, ti0);
-        compute(A, ti0);
-      }
-#endif
     }
     for (int ti = max(t0, vt1) + warp; ti < t1; ti += kWideThreads / 32) srow[ti * 32 + lane] = -INFINITY;
   }
@@ -389,13 +251,19 @@ static socket_status launch_score_wide(const socket_cfg& c, const float* lut, co
   if (grid.x == 0 || grid.y == 0) return SOCKET_OK;
   const int E = wide_entries(c.P);
   const int row_floats = (int)(bytes / sizeof(float));
-  if (c.P <= 10 && Lp >= 32 && !getenv("SOCKET_WIDE_FACTORED")) {
+  if (c.P <= 10 && Lp >= 32 && true) {
     // group-summed tables per 32-slot group (one LDS per lookup)
     const int R = 1 << c.P, RL = 1 << (c.P / 2);
     const size_t sm2 = ((size_t)R * 32 + (size_t)NH * RL * 32) * sizeof(float);
     const long long total_tiles = (long long)c.B * H_sel * (c.N_max / 32);
-    const unsigned pgrid = (unsigned)(total_tiles < kNumSMs ? total_tiles : kNumSMs);
-#define SK_WIDE2(N)                                                                                case N:                                                                                            cudaFuncSetAttribute(score_wide2_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);     score_wide2_kernel<N><<<pgrid, kWideThreads, sm2, st>>>(                                              lut, reinterpret_cast<const uint16_t*>(codes), vnorm, seq_lens, mask, scores, H_sel, c.H_kv,         G_sel, c.N_max, Lp, c.P, E, row_floats, total_tiles); return check_launch("score_wide2_kernel");
+    const unsigned pgrid = (unsigned)(total_tiles < num_sms() ? total_tiles : num_sms());
+#define SK_WIDE2(N)                                                                          \
+  case N:                                                                                    \
+    cudaFuncSetAttribute(score_wide2_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2); \
+    score_wide2_kernel<N><<<pgrid, kWideThreads, sm2, st>>>(                                 \
+        lut, reinterpret_cast<const uint16_t*>(codes), vnorm, seq_lens, mask, scores, H_sel, c.H_kv, \
+        G_sel, c.N_max, Lp, c.P, E, row_floats, total_tiles, c.index_base);                  \
+    return check_launch("score_wide2_kernel");
     switch (NH) {
       SK_WIDE2(1) SK_WIDE2(2) SK_WIDE2(4) SK_WIDE2(8)
       default: break;
@@ -407,7 +275,7 @@ static socket_status launch_score_wide(const socket_cfg& c, const float* lut, co
     cudaFuncSetAttribute(score_wide_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); \
     score_wide_kernel<N><<<grid, kWideThreads, bytes, st>>>(                                   \
         lut, reinterpret_cast<const uint16_t*>(codes), vnorm, seq_lens, mask, scores, H_sel, c.H_kv, \
-        G_sel, c.N_max, Lp, c.P, E, row_floats);                                               \
+        G_sel, c.N_max, Lp, c.P, E, row_floats, c.index_base);                                 \
     break;
   switch (NH) {
     SK_WIDE(1) SK_WIDE(2) SK_WIDE(4) SK_WIDE(8)
@@ -450,15 +318,12 @@ __device__ __forceinline__ void load_reg_tile(RegTile<LP>& t, const uint8_t* til
   t.vn = __ldg(tile_vn + lane);
 }
 
-#ifndef SK_SCORE_L2HINT
-#define SK_SCORE_L2HINT 1
-#endif
 template <int LP>
 __global__ void __launch_bounds__(kScoreThreads, 1)
 score_reg_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
                  const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
                  const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
-                 int G_sel, int N_max, long long total_tiles) {
+                 int G_sel, int N_max, long long total_tiles, long long index_base) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t bar;
   constexpr uint32_t LUT_BYTES = 256 * 64 * 4;
@@ -467,11 +332,7 @@ score_reg_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ co
 #pragma unroll
   for (int m = 0; m < 16; ++m)
     pk[m] = (uint32_t)(((2 * m + lane) & 31) << 2) | ((uint32_t)(((2 * m + 1 + lane) & 31) << 2) << 8);
-#if SK_SCORE_L2HINT
   const uint64_t pol_code = l2_policy_evict_first(), pol_score = l2_policy_evict_last();
-#else
-  const uint64_t pol_code = l2_policy_evict_normal(), pol_score = l2_policy_evict_normal();
-#endif
   const int tiles_per_row = N_max >> 5;
   const long long t_begin = total_tiles * blockIdx.x / gridDim.x;
   const long long t_end = total_tiles * (blockIdx.x + 1) / gridDim.x;
@@ -487,7 +348,7 @@ score_reg_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ co
     const int tile1 = (int)(seg_end - (long long)row * tiles_per_row);
     t = seg_end;
     const int b = row / H_sel, r = row % H_sel, g = r / G_sel;
-    const int n = seq_lens[b];
+    const int n = local_len(seq_lens[b], index_base, N_max);
     const int vt1 = min(tile1, (n + 31) >> 5);
     const bool need_lut = tile0 < vt1;
     if (need_lut && threadIdx.x == 0) {
@@ -543,158 +404,6 @@ score_reg_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ co
   }
 }
 
-// ----------------------------------------------------------------------------
-// score kernel, TMA-fed (default): the same lookups as score_kernel, but the
-// codes and norms stream through a CTA-wide ring of 16-tile chunks filled by a
-// dedicated producer warp with cp.async.bulk (TMA) + mbarriers -- a bulk-copy
-// read stream measured 7.1 TB/s on this part vs 6.6 TB/s for LDG.128
-// (tools/micro/stream_bw.cu).  Consumer warp w scores tile w of each chunk; it
-// releases the stage (empty barrier) as soon as its data is in registers.  A
-// row change reloads the row's LUT image once every consumer is done with it.
-// ----------------------------------------------------------------------------
-constexpr int kSc2Consumers = 16;
-constexpr int kSc2Threads = (kSc2Consumers + 1) * 32;   // + producer warp
-constexpr int kSc2ChunkTiles = 16;
-
-template <int LP>
-struct Sc2Geom {
-  static constexpr int TILE = LP * 32;                                  // code bytes per tile
-  static constexpr int STAGE = kSc2ChunkTiles * (TILE + 128);           // codes + norms
-  static constexpr int STAGES = (136 * 1024) / STAGE < 2 ? 2 : ((136 * 1024) / STAGE > 16 ? 16 : (136 * 1024) / STAGE);
-};
-
-template <int LP>
-__global__ void __launch_bounds__(kSc2Threads, 1)
-score_tma_kernel(const float* __restrict__ lut_g, const uint8_t* __restrict__ codes,
-                 const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
-                 const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
-                 int G_sel, int N_max, long long total_tiles) {
-  using GM = Sc2Geom<LP>;
-  extern __shared__ __align__(128) char smem[];
-  __shared__ __align__(8) uint64_t full[GM::STAGES], empty[GM::STAGES], lut_full, lut_free;
-  constexpr uint32_t LUT_BYTES = 256 * 64 * 4;
-  char* ring = smem + LUT_BYTES;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles_per_row = N_max >> 5;
-  const long long tb = total_tiles * blockIdx.x / gridDim.x;
-  const long long te = total_tiles * (blockIdx.x + 1) / gridDim.x;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < GM::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kSc2Consumers); }
-    mbar_init(&lut_full, 1);
-    mbar_init(&lut_free, kSc2Consumers);
-  }
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: LUT / codes of the predecessor
-
-  if (warp == kSc2Consumers) {
-    // ---------------- producer ------------------------------------------------
-    if (lane == 0) {
-      int q = 0, gl = 0;          // chunk counter, LUT-load counter
-      for (long long t = tb; t < te;) {
-        const int row = (int)(t / tiles_per_row);
-        const long long seg_end = min(te, (long long)(row + 1) * tiles_per_row);
-        const int t0 = (int)(t - (long long)row * tiles_per_row);
-        const int t1 = (int)(seg_end - (long long)row * tiles_per_row);
-        t = seg_end;
-        const int b = row / H_sel, g = (row % H_sel) / G_sel;
-        const int vt1 = min(t1, (seq_lens[b] + 31) >> 5);
-        if (t0 >= vt1) continue;                              // no data: no LUT, no chunks
-        if (gl > 0) mbar_wait(&lut_free, (gl - 1) & 1);        // consumers done with the old LUT
-        mbar_expect_tx(&lut_full, LUT_BYTES);
-        const char* lsrc = reinterpret_cast<const char*>(lut_g) + (size_t)row * LUT_BYTES;
-        for (uint32_t off = 0; off < LUT_BYTES; off += 32768) bulk_g2s(smem + off, lsrc + off, 32768, &lut_full);
-        ++gl;
-        const uint8_t* crow = codes + ((size_t)b * H_kv + g) * N_max * LP;
-        const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
-        for (int c0 = t0; c0 < vt1; c0 += kSc2ChunkTiles, ++q) {
-          const int nt = min(kSc2ChunkTiles, vt1 - c0);
-          const int st = q % GM::STAGES;
-          mbar_wait(&empty[st], ((q / GM::STAGES) & 1) ^ 1);
-          mbar_expect_tx(&full[st], (uint32_t)nt * (GM::TILE + 128));
-          char* dst = ring + st * GM::STAGE;
-          bulk_g2s(dst, crow + (size_t)c0 * GM::TILE, (uint32_t)nt * GM::TILE, &full[st]);
-          bulk_g2s(dst + kSc2ChunkTiles * GM::TILE, vrow + c0 * 32, (uint32_t)nt * 128, &full[st]);
-        }
-      }
-    }
-    return;
-  }
-  // ---------------- consumers ---------------------------------------------------
-  uint32_t pk[16];
-#pragma unroll
-  for (int m = 0; m < 16; ++m)
-    pk[m] = (uint32_t)(((2 * m + lane) & 31) << 2) | ((uint32_t)(((2 * m + 1 + lane) & 31) << 2) << 8);
-  int q = 0, gl = 0;
-  for (long long t = tb; t < te;) {
-    const int row = (int)(t / tiles_per_row);
-    const long long seg_end = min(te, (long long)(row + 1) * tiles_per_row);
-    const int t0 = (int)(t - (long long)row * tiles_per_row);
-    const int t1 = (int)(seg_end - (long long)row * tiles_per_row);
-    t = seg_end;
-    const int b = row / H_sel;
-    const int n = seq_lens[b];
-    const int vt1 = min(t1, (n + 31) >> 5);
-    const int g = (row % H_sel) / G_sel;
-    const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
-    const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
-    float* srow = scores + (size_t)row * N_max;
-    (void)vrow;
-    if (t0 < vt1) {
-      mbar_wait(&lut_full, gl & 1);
-      ++gl;
-      for (int c0 = t0; c0 < vt1; c0 += kSc2ChunkTiles, ++q) {
-        const int nt = min(kSc2ChunkTiles, vt1 - c0);
-        const int st = q % GM::STAGES;
-        mbar_wait(&full[st], (q / GM::STAGES) & 1);
-        if (warp < nt) {
-          const char* tp = ring + st * GM::STAGE + warp * GM::TILE;
-          constexpr int CB = LP < 16 ? LP : 16;
-          uint32_t w[LP / 4];
-#pragma unroll
-          for (int ch = 0; ch < LP / CB; ++ch) {
-            if constexpr (CB == 16) {
-              const uint4 v = *reinterpret_cast<const uint4*>(tp + ch * 512 + lane * 16);
-              w[ch * 4 + 0] = v.x; w[ch * 4 + 1] = v.y; w[ch * 4 + 2] = v.z; w[ch * 4 + 3] = v.w;
-            } else {
-              const uint2 v = *reinterpret_cast<const uint2*>(tp + ch * 256 + lane * 8);
-              w[ch * 2 + 0] = v.x; w[ch * 2 + 1] = v.y;
-            }
-          }
-          const float vn = *reinterpret_cast<const float*>(ring + st * GM::STAGE + kSc2ChunkTiles * GM::TILE +
-                                                           warp * 128 + lane * 4);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[st]);          // stage data is in registers
-          uint64_t acc = 0ull;
-#pragma unroll
-          for (int s2 = 0; s2 < LP; s2 += 2) {
-            float v[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int ss = s2 + u, sl = ss & 31;
-              const uint32_t sel = (uint32_t)(4 + (sl & 1)) | ((uint32_t)(ss & 3) << 4) | 0x7600u;
-              const uint32_t addr = __byte_perm(w[ss >> 2], pk[sl >> 1], sel);   // code*256 + 4 c
-              v[u] = *reinterpret_cast<const float*>(smem + ((ss & 32) ? 128 : 0) + addr);
-            }
-            const uint64_t pv = (uint64_t)__float_as_uint(v[0]) | ((uint64_t)__float_as_uint(v[1]) << 32);
-            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(pv));
-          }
-          const float acc0 = __uint_as_float((uint32_t)acc), acc1 = __uint_as_float((uint32_t)(acc >> 32));
-          const int j = (c0 + warp) * 32 + lane;
-          const bool ok = j < n && (!mrow || mrow[j]);
-          srow[j] = ok ? vn * (acc0 + acc1) : -INFINITY;
-        } else {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[st]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&lut_free);                // done with this row's LUT
-    }
-    for (int ti = max(t0, vt1) + warp; ti < t1; ti += kSc2Consumers) srow[ti * 32 + lane] = -INFINITY;
-  }
-}
-
 socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint8_t* codes,
                                const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
                                float* scores, cudaStream_t st, bool pdl) {
@@ -703,7 +412,7 @@ socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint
   const int H_sel = num_sel_rows(c);
   const int G_sel = c.group_mode == SOCKET_GROUP_PER_QHEAD ? c.H_q / c.H_kv : 1;
   const long long total_tiles = (long long)c.B * H_sel * (c.N_max / 32);
-  long long grid = kNumSMs;
+  long long grid = num_sms();
   if (grid > total_tiles) grid = total_tiles;
   if (grid < 1) return SOCKET_OK;
   cudaLaunchConfig_t cfg = {};
@@ -716,34 +425,15 @@ socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
 #define SK_SCORE_CASE(LPV)                                                                     \
-  case LPV: if (getenv("SOCKET_SCORE_TMA")) {                                                  \
-    const size_t smem2 = 256 * 64 * 4 + (size_t)Sc2Geom<LPV>::STAGES * Sc2Geom<LPV>::STAGE;     \
-    auto kfn2 = score_tma_kernel<LPV>;                                                         \
-    cudaFuncSetAttribute(kfn2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);       \
-    cfg.dynamicSmemBytes = smem2;                                                              \
-    cfg.blockDim = dim3(kSc2Threads);                                                          \
-    cudaError_t e2 = cudaLaunchKernelEx(&cfg, kfn2, lut, codes, vnorm, seq_lens, mask, scores, H_sel, \
-                                        c.H_kv, G_sel, c.N_max, total_tiles);                  \
-    if (e2 != cudaSuccess) return fail(SOCKET_ECUDA, std::string("score launch: ") + cudaGetErrorString(e2)); \
-    return check_launch("score_tma_kernel");                                                   \
-  } else if (!getenv("SOCKET_SCORE_V1")) {                                                     \
+  case LPV: {                                                                                  \
     const size_t smem3 = 256 * 64 * 4;                                                         \
     auto kfn3 = score_reg_kernel<LPV>;                                                         \
     cudaFuncSetAttribute(kfn3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);       \
     cfg.dynamicSmemBytes = smem3;                                                              \
     cudaError_t e3 = cudaLaunchKernelEx(&cfg, kfn3, lut, codes, vnorm, seq_lens, mask, scores, H_sel, \
-                                        c.H_kv, G_sel, c.N_max, total_tiles);                  \
+                                        c.H_kv, G_sel, c.N_max, total_tiles, c.index_base);    \
     if (e3 != cudaSuccess) return fail(SOCKET_ECUDA, std::string("score launch: ") + cudaGetErrorString(e3)); \
     return check_launch("score_reg_kernel");                                                   \
-  } else {                                                                                     \
-    const size_t smem = lut_bytes_per_row(c.L) + (size_t)kScoreWarps * kScoreStages * TileStage<LPV>::BYTES; \
-    auto kfn = score_kernel<LPV>;                                                              \
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
-    cfg.dynamicSmemBytes = smem;                                                               \
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, lut, codes, vnorm, seq_lens, mask, scores, H_sel, \
-                                       c.H_kv, G_sel, c.N_max, total_tiles);                   \
-    if (e != cudaSuccess) return fail(SOCKET_ECUDA, std::string("score launch: ") + cudaGetErrorString(e)); \
-    return check_launch("score_kernel");                                                       \
   }
   switch (Lp) {
     SK_SCORE_CASE(8)

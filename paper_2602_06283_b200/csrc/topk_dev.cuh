@@ -33,29 +33,43 @@ static __device__ unsigned long long g_topk_trace[4096 * 16];   // per translati
 #endif
 
 struct TopkArgs {
-  // mode 0: scores [rows][N_max], n = seq_lens[b]
-  // mode 1: resolve; candidates cand_scores [G][rows][k]; n = G*k
-  int mode;
+  // scores [rows][N_max] of keys at global positions index_base + j; the row
+  // length is seq_lens[b] (total), the local valid count local_len(...)
   const float* scores;
   const int32_t* seq_lens;
-  const float* cand_scores;
-  const int32_t* cand_idx;
-  int rows, H_sel, N_max, k, sink, window, G, rank;
-  int per;                 // slice length per CTA (multiple of 32)
+  int rows, H_sel, N_max, k, sink, window;
+  long long index_base;
+  int per;                 // slice length per CTA (multiple of 128)
+  uint32_t* gkeys;         // nullptr: slices in shared memory; else [rows][csize][per] global
   int32_t* idx;
   int32_t* cnt;
   float* sel_scores;
+  // sequence-shard protocol: op 0 = select (socket_topk),
+  // 1 = digest, 2 = window message, 3 = emit with a resolved threshold
+  int op;
+  int Q;                   // op 1: digest pairs per row
+  uint32_t* digest;        // op 1 out: [rows][Q][2] (edge key, #keys >= edge)
+  const uint32_t* state;   // op 2, 3 in: [rows][kStateWords]
+  uint32_t* msg;           // op 2 out: [rows][kMsgWords]
 };
 
+// per-row state of the shard resolve (see shard_topk.cu)
+constexpr int kStateWords = 8;   // lo, hi (0 = 2^32), k_eff, resolved, T, quota, need, -
+constexpr int kMsgHdr = 8;       // lo, hi, above, wc, mode (0 keys, 1 histogram), sh, -, -
+constexpr int kMsgCap = kBins;   // keys or histogram bins per message
+constexpr int kMsgWords = kMsgHdr + kMsgCap;
+
 __device__ __forceinline__ float load_elem(const TopkArgs& a, int row, int e) {
-  if (a.mode == 0) return a.scores[(size_t)row * a.N_max + e];
-  const int s = e / a.k, i = e % a.k;
-  return a.cand_scores[((size_t)s * a.rows + row) * a.k + i];
+  return a.scores[(size_t)row * a.N_max + e];
 }
 
-__device__ __forceinline__ uint32_t make_key(float s, int e, int n, int sink, int window, int mode) {
+// monotone key of local key e of a row with total length n_glob (invalid = 0,
+// forced sink / local-window key = 0xFFFFFFFF; positions are global)
+__device__ __forceinline__ uint32_t make_key(float s, int e, int n_glob, long long index_base, int sink,
+                                             int window) {
   if (s == -INFINITY) return 0u;
-  if (mode == 0 && (e < sink || e >= n - window)) return 0xFFFFFFFFu;
+  const long long pos = index_base + e;
+  if (pos < sink || pos >= (long long)n_glob - window) return 0xFFFFFFFFu;
   return f2key(s);
 }
 
@@ -94,6 +108,10 @@ struct __align__(16) TopkShared {
   alignas(16) uint32_t stat[8];  // nvalid, nforced, kmin, kmax, ncand, above, gt, eq (read remotely)
   uint32_t dec[4];
 };
+
+__device__ __forceinline__ void topk_emit(const TopkArgs& a, uint32_t* keys, TopkShared& S, int row, int base,
+                                          int len, uint32_t T, uint32_t quota, uint32_t k_out, bool counted,
+                                          int32_t* sel_local, int* sel_lo, int* sel_cnt);
 
 // Local exact select over a small candidate array: the `need`-th largest key
 // (1-based) and how many candidates are strictly greater.
@@ -157,13 +175,12 @@ __device__ __forceinline__ void topk_core(const TopkArgs& a, uint32_t* keys, Top
   const int crank = (int)cluster.block_rank();
   const int csize = (int)cluster.num_blocks();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const unsigned lt = (1u << lane) - 1u;
   const int len32 = (len + 31) & ~31;
   const int len128 = (len + 127) & ~127;
   const int nr = len128 >> 7;
   const int rpw = max(1, (nr + kTopkWarps - 1) / kTopkWarps);
   const int r0 = warp * rpw, r1 = min(nr, r0 + rpw);
-  (void)len32;
+  (void)n;
   if (tid < 8) S.stat[tid] = (tid == 2) ? 0xFFFFFFFFu : 0u;   // kmin starts at +max
   if (tid < kTopkWarps) { S.wgt[tid] = 0; S.weq[tid] = 0; }
   if (tid < 2) S.acc[tid] = 0;
@@ -441,189 +458,141 @@ __device__ __forceinline__ void topk_core(const TopkArgs& a, uint32_t* keys, Top
   }
 
   // ---- stable compaction ------------------------------------------------------
-  // Output position of a selected key = gt_rank + min(eq_rank, quota), where
-  // gt_rank / eq_rank count keys > T / == T at smaller indices (row-global).
-  int em_all = 0;
   TK_TRACE(10);
-  if (a.mode == 0) {
-    int gbase, ebase;   // row-global ranks of this warp's first key
-    uint32_t cta_gb = 0, cta_eb = 0, cta_gt = 0, cta_eq = 0;   // this CTA's share (sel_local)
-    if (counted) {
-      uint32_t gb = S.acc[0], eb = S.acc[1];
-      for (int r = 0; r < crank; ++r) gb += S.rab[r];
-      uint32_t gw = 0, ew = 0;
-      for (int w = 0; w < warp; ++w) { gw += S.wab[w] + S.wgt[w]; ew += S.weq[w]; }
-      gbase = (int)(gb + gw);
-      ebase = (int)(eb + ew);
-      cta_gb = gb;
-      cta_eb = eb;
-      for (int w = 0; w < kTopkWarps; ++w) { cta_gt += S.wab[w] + S.wgt[w]; cta_eq += S.weq[w]; }
-    } else {
-      // everything / only forced keys selected, or the radix fallback: count pass
-      uint32_t g = 0, e = 0;
-      for (int r = r0; r < r1; ++r) {
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          const uint32_t key = keys[r * 128 + x * 32 + lane];
-          g += __popc(__ballot_sync(kFull, key > T));
-          e += __popc(__ballot_sync(kFull, key != 0u && key == T));
-        }
-      }
-      if (lane == 0) { S.scan[warp] = (int)g; S.scan2[warp] = (int)e; }
-      __syncthreads();
-      uint32_t gw = 0, ew = 0, gtot = 0, etot = 0;
-#pragma unroll
-      for (int w = 0; w < kTopkWarps; ++w) {
-        const uint32_t xg = (uint32_t)S.scan[w], xe = (uint32_t)S.scan2[w];
-        gw += w < warp ? xg : 0u; ew += w < warp ? xe : 0u;
-        gtot += xg; etot += xe;
-      }
-      if (tid == 0) { S.stat[6] = gtot; S.stat[7] = etot; }
-      cluster.sync();
-      uint32_t gb = 0, eb = 0;
-      for (int r = 0; r < crank; ++r) {
-        const uint32_t* rs = cluster.map_shared_rank(S.stat, r);
-        gb += rs[6];
-        eb += rs[7];
-      }
-      gbase = (int)(gb + gw);
-      ebase = (int)(eb + ew);
-      cta_gb = gb;
-      cta_eb = eb;
-      cta_gt = gtot;
-      cta_eq = etot;
-    }
-    TK_TRACE(11);
-    const int sel0 = (int)cta_gb + min((int)cta_eb, (int)quota);
-    if (sel_lo) {
-      *sel_lo = sel0;
-      *sel_cnt = (int)(cta_gb + cta_gt) + min((int)(cta_eb + cta_eq), (int)quota) - sel0;
-    }
-    em_all = (int)k_eff;
-    int32_t* orow = a.idx + (size_t)row * a.k;
-    float* srow = a.sel_scores ? a.sel_scores + (size_t)row * a.k : nullptr;
-    const int q = (int)quota;
+  topk_emit(a, keys, S, row, base, len, T, quota, k_eff, counted, sel_local, sel_lo, sel_cnt);
+}
+
+// Stable compaction of a row's selection: keys > T plus the first `quota` keys
+// == T in index order, written in ascending index order.  Output position of a
+// selected key = gt_rank + min(eq_rank, quota), where gt_rank / eq_rank count
+// keys > T / == T at smaller indices (row-global).  If `counted`, the per-warp
+// counts come from topk_core's candidate pass (S.wab / S.wgt / S.weq / S.rab /
+// S.acc); otherwise a count pass computes them.  k_out = the row's total count
+// (written to cnt by CTA 0).  Ends with a cluster barrier.
+__device__ __forceinline__ void topk_emit(const TopkArgs& a, uint32_t* keys, TopkShared& S, int row, int base,
+                                          int len, uint32_t T, uint32_t quota, uint32_t k_out, bool counted,
+                                          int32_t* sel_local, int* sel_lo, int* sel_cnt) {
+  constexpr unsigned kFull = 0xffffffffu;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int len128 = (len + 127) & ~127;
+  const int nr = len128 >> 7;
+  const int rpw = max(1, (nr + kTopkWarps - 1) / kTopkWarps);
+  const int r0 = warp * rpw, r1 = min(nr, r0 + rpw);
+  int gbase, ebase;   // row-global ranks of this warp's first key
+  uint32_t cta_gb = 0, cta_eb = 0, cta_gt = 0, cta_eq = 0;   // this CTA's share (sel_local)
+  if (counted) {
+    uint32_t gb = S.acc[0], eb = S.acc[1];
+    for (int r = 0; r < crank; ++r) gb += S.rab[r];
+    uint32_t gw = 0, ew = 0;
+    for (int w = 0; w < warp; ++w) { gw += S.wab[w] + S.wgt[w]; ew += S.weq[w]; }
+    gbase = (int)(gb + gw);
+    ebase = (int)(eb + ew);
+    cta_gb = gb;
+    cta_eb = eb;
+    for (int w = 0; w < kTopkWarps; ++w) { cta_gt += S.wab[w] + S.wgt[w]; cta_eq += S.weq[w]; }
+  } else {
+    // count pass: keys > T / == T per warp, then per CTA, then cluster prefix
+    uint32_t g = 0, e = 0;
     for (int r = r0; r < r1; ++r) {
-      // lane owns keys 4 lane .. 4 lane + 3 of the round (index order within the
-      // round = lane-major); ties at T (rare) take the per-32 ballot path below
-      const int i0 = r * 128 + lane * 4;
-      const uint4 kv = *reinterpret_cast<const uint4*>(keys + i0);
-      const uint32_t k4[4] = {kv.x, kv.y, kv.z, kv.w};
-      const bool anyeq = (k4[0] == T) | (k4[1] == T) | (k4[2] == T) | (k4[3] == T);
-      if (!__any_sync(kFull, anyeq && T != 0u)) {
-        unsigned gm[4];
-        int pre = 0, tot = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          gm[e] = __ballot_sync(kFull, k4[e] > T);
-          pre += __popc(gm[e] & lt);
-          tot += __popc(gm[e]);
-        }
-        int pos = gbase + pre + min(ebase, q);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (k4[e] > T) {
-            orow[pos] = base + i0 + e;
-            if (srow) srow[pos] = load_elem(a, row, base + i0 + e);
-            if (sel_local) sel_local[pos - sel0] = base + i0 + e;
-            ++pos;
-          }
-        }
-        gbase += tot;
-        continue;
-      }
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
-        const int i = r * 128 + x * 32 + lane;
-        const uint32_t key = keys[i];
-        const bool isgt = key > T, iseq = key != 0u && key == T;
-        const unsigned gmx = __ballot_sync(kFull, isgt), em = __ballot_sync(kFull, iseq);
-        const int gr = gbase + __popc(gmx & lt), er = ebase + __popc(em & lt);
-        if (isgt || (iseq && er < q)) {
-          const int p = gr + min(er, q);
-          orow[p] = base + i;
-          if (srow) srow[p] = load_elem(a, row, base + i);
-          if (sel_local) sel_local[p - sel0] = base + i;
+        const uint32_t key = keys[r * 128 + x * 32 + lane];
+        g += __popc(__ballot_sync(kFull, key > T));
+        e += __popc(__ballot_sync(kFull, key != 0u && key == T));
+      }
+    }
+    if (lane == 0) { S.scan[warp] = (int)g; S.scan2[warp] = (int)e; }
+    __syncthreads();
+    uint32_t gw = 0, ew = 0, gtot = 0, etot = 0;
+#pragma unroll
+    for (int w = 0; w < kTopkWarps; ++w) {
+      const uint32_t xg = (uint32_t)S.scan[w], xe = (uint32_t)S.scan2[w];
+      gw += w < warp ? xg : 0u; ew += w < warp ? xe : 0u;
+      gtot += xg; etot += xe;
+    }
+    if (tid == 0) { S.stat[6] = gtot; S.stat[7] = etot; }
+    cluster.sync();
+    uint32_t gb = 0, eb = 0;
+    for (int r = 0; r < crank; ++r) {
+      const uint32_t* rs = cluster.map_shared_rank(S.stat, r);
+      gb += rs[6];
+      eb += rs[7];
+    }
+    gbase = (int)(gb + gw);
+    ebase = (int)(eb + ew);
+    cta_gb = gb;
+    cta_eb = eb;
+    cta_gt = gtot;
+    cta_eq = etot;
+  }
+  TK_TRACE(11);
+  const int sel0 = (int)cta_gb + min((int)cta_eb, (int)quota);
+  if (sel_lo) {
+    *sel_lo = sel0;
+    *sel_cnt = (int)(cta_gb + cta_gt) + min((int)(cta_eb + cta_eq), (int)quota) - sel0;
+  }
+  int32_t* orow = a.idx + (size_t)row * a.k;
+  float* srow = a.sel_scores ? a.sel_scores + (size_t)row * a.k : nullptr;
+  const int q = (int)quota;
+  for (int r = r0; r < r1; ++r) {
+    // lane owns keys 4 lane .. 4 lane + 3 of the round (index order within the
+    // round = lane-major); ties at T (rare) take the per-32 ballot path below
+    const int i0 = r * 128 + lane * 4;
+    const uint4 kv = *reinterpret_cast<const uint4*>(keys + i0);
+    const uint32_t k4[4] = {kv.x, kv.y, kv.z, kv.w};
+    const bool anyeq = (k4[0] == T) | (k4[1] == T) | (k4[2] == T) | (k4[3] == T);
+    if (!__any_sync(kFull, anyeq && T != 0u)) {
+      unsigned gm[4];
+      int pre = 0, tot = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        gm[e] = __ballot_sync(kFull, k4[e] > T);
+        pre += __popc(gm[e] & lt);
+        tot += __popc(gm[e]);
+      }
+      int pos = gbase + pre + min(ebase, q);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (k4[e] > T) {
+          orow[pos] = base + i0 + e;
+          if (srow) srow[pos] = load_elem(a, row, base + i0 + e);
+          if (sel_local) sel_local[pos - sel0] = base + i0 + e;
+          ++pos;
         }
-        gbase += __popc(gmx);
-        ebase += __popc(em);
       }
+      gbase += tot;
+      continue;
     }
-  } else {
-    const int groups = len32 >> 5;
-    const int gpw = (groups + kTopkWarps - 1) / kTopkWarps;
-    const int g0 = warp * gpw;
-    const int g1 = min(groups, g0 + gpw);
-    int eq_w = 0;
-    for (int gi = g0; gi < g1; ++gi) {
-      const uint32_t key = keys[gi * 32 + lane];
-      eq_w += __popc(__ballot_sync(0xffffffffu, key != 0u && key == T));
-    }
-    int eq_tot;
-    const int eq_pre = block_excl_scan_warps(eq_w, S.scan, warp, lane, eq_tot);
-    if (tid == 0) S.stat[6] = (uint32_t)eq_tot;
-    cluster.sync();
-    int eq_before = 0;
-    for (int c = 0; c < crank; ++c) eq_before += (int)*cluster.map_shared_rank(&S.stat[6], c);
-    const int emit_lo = a.rank * a.k;
-    const int emit_hi = (a.rank + 1) * a.k;
-    int em_w = 0;
-    {
-      int eq_run = eq_before + eq_pre;
-      for (int gi = g0; gi < g1; ++gi) {
-        const int i = gi * 32 + lane;
-        const uint32_t key = keys[i];
-        const bool valid = key != 0u;
-        const unsigned eb = __ballot_sync(0xffffffffu, valid && key == T);
-        const int my_eq = eq_run + __popc(eb & ((1u << lane) - 1u));
-        const int e = base + i;
-        const bool sel = valid && (key > T || (key == T && (uint32_t)my_eq < quota)) &&
-                         e >= emit_lo && e < emit_hi;
-        em_w += __popc(__ballot_sync(0xffffffffu, sel));
-        eq_run += __popc(eb);
-      }
-    }
-    int em_tot;
-    const int em_pre = block_excl_scan_warps(em_w, S.scan, warp, lane, em_tot);
-    if (tid == 0) S.stat[7] = (uint32_t)em_tot;
-    cluster.sync();
-    int em_before = 0;
-    for (int c = 0; c < csize; ++c) {
-      const int x = (int)*cluster.map_shared_rank(&S.stat[7], c);
-      em_all += x;
-      em_before += c < crank ? x : 0;
-    }
-    int eq_run = eq_before + eq_pre;
-    int pos = em_before + em_pre;
-    int32_t* orow = a.idx + (size_t)row * a.k;
-    for (int gi = g0; gi < g1; ++gi) {
-      const int i = gi * 32 + lane;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int i = r * 128 + x * 32 + lane;
       const uint32_t key = keys[i];
-      const bool valid = key != 0u;
-      const unsigned eb = __ballot_sync(0xffffffffu, valid && key == T);
-      const int my_eq = eq_run + __popc(eb & ((1u << lane) - 1u));
-      const int e = base + i;
-      const bool sel = valid && (key > T || (key == T && (uint32_t)my_eq < quota)) &&
-                       e >= emit_lo && e < emit_hi;
-      const unsigned sb = __ballot_sync(0xffffffffu, sel);
-      if (sel) orow[pos + __popc(sb & ((1u << lane) - 1u))] =
-          a.cand_idx[((size_t)a.rank * a.rows + row) * a.k + (e - emit_lo)];
-      pos += __popc(sb);
-      eq_run += __popc(eb);
+      const bool isgt = key > T, iseq = key != 0u && key == T;
+      const unsigned gmx = __ballot_sync(kFull, isgt), em = __ballot_sync(kFull, iseq);
+      const int gr = gbase + __popc(gmx & lt), er = ebase + __popc(em & lt);
+      if (isgt || (iseq && er < q)) {
+        const int p = gr + min(er, q);
+        orow[p] = base + i;
+        if (srow) srow[p] = load_elem(a, row, base + i);
+        if (sel_local) sel_local[p - sel0] = base + i;
+      }
+      gbase += __popc(gmx);
+      ebase += __popc(em);
     }
   }
   TK_TRACE(12);
   if (crank == 0) {
-    int32_t* orow = a.idx + (size_t)row * a.k;
-    for (int p = em_all + tid; p < a.k; p += kTopkThreads) {
+    for (int p = (int)k_out + tid; p < a.k; p += kTopkThreads) {
       orow[p] = -1;
-      if (a.sel_scores) a.sel_scores[(size_t)row * a.k + p] = -INFINITY;
+      if (srow) srow[p] = -INFINITY;
     }
-    if (tid == 0) a.cnt[row] = em_all;
+    if (tid == 0) a.cnt[row] = (int)k_out;
   }
   TK_TRACE(13);
   cluster.sync();   // keep shared memory alive until every CTA finished remote reads
-  TK_TRACE(14);
 }
 
 }  // namespace sk

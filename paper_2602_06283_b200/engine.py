@@ -116,7 +116,8 @@ class SocketDecoder:
         into the pinned output -- no DMA copy either way.
         (Memcpy nodes from pinned host memory inside the graph cost ~50 us of
         launch latency per replay on this driver, so the copies stay outside.)
-        Returns the pinned views (q_in, k_in, v_in, out)."""
+        Binding does not modify the cache: its warm-up step runs without the
+        append.  Returns the pinned views (q_in, k_in, v_in, out)."""
         cfg, dev = self.cfg, self.device
         nq = cfg.B * cfg.H_q * cfg.d
         nk = cfg.B * cfg.H_kv * cfg.d
@@ -141,10 +142,13 @@ class SocketDecoder:
             self.step(src_q, seq_lens, append=True, k_new=src_k, v_new=src_v,
                       out=out_h if direct else None)
 
+        # warm-up outside the graph WITHOUT the append: it exercises the same
+        # launches but leaves the cache, codes and norms of key seq_lens[b] - 1
+        # untouched (the pinned k/v inputs are still zeros here)
         s = torch.cuda.Stream(dev)
         s.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(s):
-            body()
+            self.step(src_q, seq_lens, append=False, out=out_h if direct else None)
         torch.cuda.current_stream(dev).wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):

@@ -34,11 +34,14 @@ class Config:
     group_mode: int = KV_SHARED
     d: int = 128
     scoring: int = 0       # SOCKET_SCORING_SOFT (Eq. 4); 1 = hard LSH collision counts (Eq. 3)
+    flags: int = 0         # SOCKET_FLAG_* (1 = chained decode step, never the one-launch kernel)
+    index_base: int = 0    # global position of local key 0 (sequence shards)
 
     def c(self) -> SocketCfg:
         s = self.sm_scale if self.sm_scale is not None else 1.0 / math.sqrt(self.d)
         return SocketCfg(self.B, self.H_q, self.H_kv, self.d, self.N_max, self.L, self.P,
-                         float(self.tau), float(s), int(self.group_mode), int(self.scoring))
+                         float(self.tau), float(s), int(self.group_mode), int(self.scoring),
+                         int(self.flags), int(self.index_base))
 
     @property
     def H_sel(self) -> int:
@@ -147,16 +150,35 @@ def query_tables(cfg: Config, q, W):
     return t
 
 
-def score(cfg: Config, q, W, codes, vnorm, seq_lens, mask=None, out=None, ws=None):
-    """Eq. 4 + Alg. 4 scores [B][H_sel][N_max] (fp32, -inf for invalid keys)."""
-    _need(q, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "q")
+def _need_index(cfg: Config, codes, vnorm, seq_lens, mask=None):
+    _need(codes, torch.uint8, (codes_bytes(cfg),), "codes")
+    _need(vnorm, torch.float32, (cfg.B, cfg.H_kv, cfg.N_max), "vnorm")
     _need(seq_lens, torch.int32, (cfg.B,), "seq_lens")
     if mask is not None:
         _need(mask, torch.uint8, (cfg.B, cfg.N_max), "mask")
+
+
+def _need_ws(ws, cfg: Config, op: int, k: int, name="ws"):
+    if not ws.is_cuda or ws.dtype != torch.uint8 or ws.numel() < workspace_bytes(cfg, op, k):
+        raise ValueError(f"{name}: expected a CUDA uint8 buffer of >= {workspace_bytes(cfg, op, k)} bytes")
+
+
+def _need_kv(cfg: Config, K, V):
+    _need(K, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.N_max, cfg.d), "K")
+    _need(V, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.N_max, cfg.d), "V")
+
+
+def score(cfg: Config, q, W, codes, vnorm, seq_lens, mask=None, out=None, ws=None):
+    """Eq. 4 + Alg. 4 scores [B][H_sel][N_max] (fp32, -inf for invalid keys)."""
+    _need(q, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "q")
+    _need(W, torch.bfloat16, (cfg.L, cfg.P, cfg.d), "W")
+    _need_index(cfg, codes, vnorm, seq_lens, mask)
     if out is None:
         out = torch.empty((cfg.B, cfg.H_sel, cfg.N_max), dtype=torch.float32, device=q.device)
+    _need(out, torch.float32, (cfg.B, cfg.H_sel, cfg.N_max), "scores")
     if ws is None:
         ws = workspace(cfg, _lib.OP_SCORE, 1, q.device)
+    _need_ws(ws, cfg, _lib.OP_SCORE, 1)
     c = cfg.c()
     check(lib().socket_score(ctypes.byref(c), _p(q), _p(W), _p(codes), _p(vnorm), _p(seq_lens),
                              _p(mask), _p(out), _p(ws), ws.numel(), _stream(q)))
@@ -165,8 +187,11 @@ def score(cfg: Config, q, W, codes, vnorm, seq_lens, mask=None, out=None, ws=Non
 
 def build_lut(cfg: Config, q, W, lut=None):
     """Alg. 2 tables as the score kernel's shared-memory image (opaque buffer)."""
+    _need(q, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "q")
+    _need(W, torch.bfloat16, (cfg.L, cfg.P, cfg.d), "W")
     if lut is None:
         lut = workspace(cfg, _lib.OP_SCORE, 1, q.device)
+    _need_ws(lut, cfg, _lib.OP_SCORE, 1, "lut")
     c = cfg.c()
     check(lib().socket_build_lut(ctypes.byref(c), _p(q), _p(W), _p(lut), lut.numel(), _stream(q)))
     return lut
@@ -174,8 +199,11 @@ def build_lut(cfg: Config, q, W, lut=None):
 
 def score_lut(cfg: Config, lut, codes, vnorm, seq_lens, mask=None, out=None):
     """Eq. 4 + Alg. 4 scores from a LUT built by build_lut."""
+    _need_ws(lut, cfg, _lib.OP_SCORE, 1, "lut")
+    _need_index(cfg, codes, vnorm, seq_lens, mask)
     if out is None:
         out = torch.empty((cfg.B, cfg.H_sel, cfg.N_max), dtype=torch.float32, device=lut.device)
+    _need(out, torch.float32, (cfg.B, cfg.H_sel, cfg.N_max), "scores")
     c = cfg.c()
     check(lib().socket_score_lut(ctypes.byref(c), _p(lut), _p(codes), _p(vnorm), _p(seq_lens),
                                  _p(mask), _p(out), _stream(lut)))
@@ -192,6 +220,9 @@ def decode_step(cfg: Config, q, K, V, W, codes, vnorm, seq_lens, k: int, append:
     if k_new is not None:
         _need_uva(k_new, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.d), "k_new")
         _need_uva(v_new, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.d), "v_new")
+    _need_kv(cfg, K, V)
+    _need(W, torch.bfloat16, (cfg.L, cfg.P, cfg.d), "W")
+    _need_index(cfg, codes, vnorm, seq_lens, mask)
     dev = K.device
     if scores is None:
         scores = torch.empty((cfg.B, cfg.H_sel, cfg.N_max), dtype=torch.float32, device=dev)
@@ -205,6 +236,12 @@ def decode_step(cfg: Config, q, K, V, W, codes, vnorm, seq_lens, k: int, append:
         lse = torch.empty((cfg.B, cfg.H_q), dtype=torch.float32, device=dev)
     if ws is None:
         ws = workspace(cfg, _lib.OP_DECODE_STEP, k, dev)
+    _need(scores, torch.float32, (cfg.B, cfg.H_sel, cfg.N_max), "scores")
+    _need(idx, torch.int32, (cfg.B, cfg.H_sel, k), "idx")
+    _need(cnt, torch.int32, (cfg.B, cfg.H_sel), "cnt")
+    _need_uva(out, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "out")
+    _need(lse, torch.float32, (cfg.B, cfg.H_q), "lse")
+    _need_ws(ws, cfg, _lib.OP_DECODE_STEP, k)
     c = cfg.c()
     check(lib().socket_decode_step(ctypes.byref(c), _p(q), _p(K), _p(V), _p(W), _p(codes), _p(vnorm),
                                    _p(seq_lens), _p(mask), int(bool(append)), _p(k_new), _p(v_new),
@@ -221,9 +258,11 @@ def decode_step_launches(cfg: Config) -> int:
 
 
 def topk(cfg: Config, scores, seq_lens, k: int, sink: int = 0, window: int = 0,
-         idx=None, cnt=None, sel_scores=None, want_scores: bool = False):
-    """Alg. 3 l.244 TopK: idx [B][H_sel][k] ascending (-1 past cnt), cnt [B][H_sel]."""
+         idx=None, cnt=None, sel_scores=None, want_scores: bool = False, ws=None):
+    """Alg. 3 l.244 TopK: idx [B][H_sel][k] ascending (-1 past cnt), cnt [B][H_sel].
+    Rows longer than 655360 keys keep their key slices in `ws`."""
     _need(scores, torch.float32, (cfg.B, cfg.H_sel, cfg.N_max), "scores")
+    _need(seq_lens, torch.int32, (cfg.B,), "seq_lens")
     dev = scores.device
     if idx is None:
         idx = torch.empty((cfg.B, cfg.H_sel, k), dtype=torch.int32, device=dev)
@@ -231,21 +270,123 @@ def topk(cfg: Config, scores, seq_lens, k: int, sink: int = 0, window: int = 0,
         cnt = torch.empty((cfg.B, cfg.H_sel), dtype=torch.int32, device=dev)
     if want_scores and sel_scores is None:
         sel_scores = torch.empty((cfg.B, cfg.H_sel, k), dtype=torch.float32, device=dev)
+    _need(idx, torch.int32, (cfg.B, cfg.H_sel, k), "idx")
+    _need(cnt, torch.int32, (cfg.B, cfg.H_sel), "cnt")
+    if sel_scores is not None:
+        _need(sel_scores, torch.float32, (cfg.B, cfg.H_sel, k), "sel_scores")
+    if ws is None and workspace_bytes(cfg, _lib.OP_TOPK, k) > 0:
+        ws = workspace(cfg, _lib.OP_TOPK, k, dev)
     c = cfg.c()
     check(lib().socket_topk(ctypes.byref(c), _p(scores), _p(seq_lens), k, sink, window, _p(idx),
-                            _p(cnt), _p(sel_scores), None, 0, _stream(scores)))
+                            _p(cnt), _p(sel_scores), _p(ws), 0 if ws is None else ws.numel(),
+                            _stream(scores)))
     return (idx, cnt, sel_scores) if want_scores else (idx, cnt)
+
+
+# ---------------------------------------------------------------------------
+# sequence-shard exact top-k (include/socket_b200.h)
+# ---------------------------------------------------------------------------
+def topk_digest(cfg: Config, scores, seq_lens, k: int, shards: int, Q: int = 64, sink: int = 0,
+                window: int = 0, digest=None, ws=None):
+    """This shard's digest [B][H_sel][Q][2] (int32 view of u32 (edge key, #keys >= edge))."""
+    _need(scores, torch.float32, (cfg.B, cfg.H_sel, cfg.N_max), "scores")
+    _need(seq_lens, torch.int32, (cfg.B,), "seq_lens")
+    if digest is None:
+        digest = torch.empty((cfg.B, cfg.H_sel, Q, 2), dtype=torch.int32, device=scores.device)
+    _need(digest, torch.int32, (cfg.B, cfg.H_sel, Q, 2), "digest")
+    if ws is None and workspace_bytes(cfg, _lib.OP_TOPK, k) > 0:
+        ws = workspace(cfg, _lib.OP_TOPK, k, scores.device)
+    c = cfg.c()
+    check(lib().socket_topk_digest(ctypes.byref(c), _p(scores), _p(seq_lens), k, sink, window, shards,
+                                   Q, _p(digest), _p(ws), 0 if ws is None else ws.numel(),
+                                   _stream(scores)))
+    return digest
+
+
+def topk_bracket(cfg: Config, all_digests, k: int, state=None):
+    """Initial per-row state [B][H_sel][8] from the G gathered digests [G][B][H_sel][Q][2]."""
+    G, Q = int(all_digests.shape[0]), int(all_digests.shape[3])
+    _need(all_digests, torch.int32, (G, cfg.B, cfg.H_sel, Q, 2), "all_digests")
+    if state is None:
+        state = torch.empty((cfg.B, cfg.H_sel, _lib.TOPK_STATE_WORDS), dtype=torch.int32,
+                            device=all_digests.device)
+    _need(state, torch.int32, (cfg.B, cfg.H_sel, _lib.TOPK_STATE_WORDS), "state")
+    c = cfg.c()
+    check(lib().socket_topk_bracket(ctypes.byref(c), _p(all_digests), G, Q, k, _p(state),
+                                    _stream(all_digests)))
+    return state
+
+
+def topk_window(cfg: Config, scores, seq_lens, state, sink: int = 0, window: int = 0, msg=None,
+                ws=None):
+    """This shard's window message [B][H_sel][8 + 2048] for the state's brackets."""
+    _need(scores, torch.float32, (cfg.B, cfg.H_sel, cfg.N_max), "scores")
+    _need(seq_lens, torch.int32, (cfg.B,), "seq_lens")
+    _need(state, torch.int32, (cfg.B, cfg.H_sel, _lib.TOPK_STATE_WORDS), "state")
+    if msg is None:
+        msg = torch.empty((cfg.B, cfg.H_sel, _lib.TOPK_MSG_WORDS), dtype=torch.int32, device=scores.device)
+    _need(msg, torch.int32, (cfg.B, cfg.H_sel, _lib.TOPK_MSG_WORDS), "msg")
+    if ws is None and workspace_bytes(cfg, _lib.OP_TOPK, 1) > 0:
+        ws = workspace(cfg, _lib.OP_TOPK, 1, scores.device)
+    c = cfg.c()
+    check(lib().socket_topk_window(ctypes.byref(c), _p(scores), _p(seq_lens), sink, window, _p(state),
+                                   _p(msg), _p(ws), 0 if ws is None else ws.numel(), _stream(scores)))
+    return msg
+
+
+def topk_resolve(cfg: Config, all_msgs, rank: int, state):
+    """Resolve (or narrow) every row's threshold from the G gathered messages."""
+    G = int(all_msgs.shape[0])
+    _need(all_msgs, torch.int32, (G, cfg.B, cfg.H_sel, _lib.TOPK_MSG_WORDS), "all_msgs")
+    _need(state, torch.int32, (cfg.B, cfg.H_sel, _lib.TOPK_STATE_WORDS), "state")
+    c = cfg.c()
+    check(lib().socket_topk_resolve(ctypes.byref(c), _p(all_msgs), G, rank, _p(state),
+                                    _stream(all_msgs)))
+    return state
+
+
+def topk_emit(cfg: Config, scores, seq_lens, k: int, state, sink: int = 0, window: int = 0,
+              idx=None, cnt=None, sel_scores=None, ws=None):
+    """This shard's share of the global selection (local indices ascending, cnt)."""
+    _need(scores, torch.float32, (cfg.B, cfg.H_sel, cfg.N_max), "scores")
+    _need(seq_lens, torch.int32, (cfg.B,), "seq_lens")
+    _need(state, torch.int32, (cfg.B, cfg.H_sel, _lib.TOPK_STATE_WORDS), "state")
+    dev = scores.device
+    if idx is None:
+        idx = torch.empty((cfg.B, cfg.H_sel, k), dtype=torch.int32, device=dev)
+    if cnt is None:
+        cnt = torch.empty((cfg.B, cfg.H_sel), dtype=torch.int32, device=dev)
+    _need(idx, torch.int32, (cfg.B, cfg.H_sel, k), "idx")
+    _need(cnt, torch.int32, (cfg.B, cfg.H_sel), "cnt")
+    if ws is None and workspace_bytes(cfg, _lib.OP_TOPK, k) > 0:
+        ws = workspace(cfg, _lib.OP_TOPK, k, dev)
+    c = cfg.c()
+    check(lib().socket_topk_emit(ctypes.byref(c), _p(scores), _p(seq_lens), k, sink, window, _p(state),
+                                 _p(idx), _p(cnt), _p(sel_scores), _p(ws),
+                                 0 if ws is None else ws.numel(), _stream(scores)))
+    return idx, cnt
 
 
 def sparse_decode(cfg: Config, q, K, V, idx, cnt, k: int, out=None, lse=None, partial=None,
                   ws=None, want_out: bool = True):
     """Eq. 2 exact attention over the selected rows; out bf16 [B][H_q][d], lse fp32."""
+    _need(q, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "q")
+    _need_kv(cfg, K, V)
+    _need(idx, torch.int32, (cfg.B, cfg.H_sel, k), "idx")
+    _need(cnt, torch.int32, (cfg.B, cfg.H_sel), "cnt")
+    if partial is not None:
+        _need(partial, torch.float32, (cfg.B, cfg.H_q, cfg.d + 2), "partial")
     dev = q.device
     if want_out and out is None:
         out = torch.empty((cfg.B, cfg.H_q, cfg.d), dtype=torch.bfloat16, device=dev)
         lse = torch.empty((cfg.B, cfg.H_q), dtype=torch.float32, device=dev) if lse is None else lse
     if ws is None:
         ws = workspace(cfg, _lib.OP_SPARSE_DECODE, k, dev)
+    _need_ws(ws, cfg, _lib.OP_SPARSE_DECODE, k)
+    if out is not None:
+        _need(out, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "out")
+    if lse is not None:
+        _need(lse, torch.float32, (cfg.B, cfg.H_q), "lse")
     c = cfg.c()
     check(lib().socket_sparse_decode(ctypes.byref(c), _p(q), _p(K), _p(V), _p(idx), _p(cnt), k,
                                      _p(out), _p(lse), _p(partial), _p(ws), ws.numel(), _stream(q)))
@@ -260,11 +401,17 @@ def sample_decode(cfg: Config, scores, vnorm, V, seq_lens, uniforms, samples=Non
     _need(scores, torch.float32, (cfg.B, cfg.H_q, cfg.N_max), "scores")
     M = int(uniforms.shape[-1])
     _need(uniforms, torch.float32, (cfg.B, cfg.H_q, M), "uniforms")
+    _need(vnorm, torch.float32, (cfg.B, cfg.H_kv, cfg.N_max), "vnorm")
+    _need(V, torch.bfloat16, (cfg.B, cfg.H_kv, cfg.N_max, cfg.d), "V")
+    _need(seq_lens, torch.int32, (cfg.B,), "seq_lens")
     dev = scores.device
     if out is None:
         out = torch.empty((cfg.B, cfg.H_q, cfg.d), dtype=torch.bfloat16, device=dev)
     if want_samples and samples is None:
         samples = torch.empty((cfg.B, cfg.H_q, M), dtype=torch.int32, device=dev)
+    _need(out, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "out")
+    if samples is not None:
+        _need(samples, torch.int32, (cfg.B, cfg.H_q, M), "samples")
     c = cfg.c()
     check(lib().socket_sample_decode(ctypes.byref(c), _p(scores), _p(vnorm), _p(V), _p(seq_lens),
                                      _p(uniforms), M, _p(samples), _p(out), _stream(scores)))
@@ -273,6 +420,9 @@ def sample_decode(cfg: Config, scores, vnorm, V, seq_lens, uniforms, samples=Non
 
 def dense_decode(cfg: Config, q, K, V, seq_lens, out=None, lse=None, ws=None):
     """Eq. 1 dense flash-decode over j < seq_lens[b] (the k = n baseline)."""
+    _need(q, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "q")
+    _need_kv(cfg, K, V)
+    _need(seq_lens, torch.int32, (cfg.B,), "seq_lens")
     dev = q.device
     if out is None:
         out = torch.empty((cfg.B, cfg.H_q, cfg.d), dtype=torch.bfloat16, device=dev)
@@ -280,6 +430,9 @@ def dense_decode(cfg: Config, q, K, V, seq_lens, out=None, lse=None, ws=None):
         lse = torch.empty((cfg.B, cfg.H_q), dtype=torch.float32, device=dev)
     if ws is None:
         ws = workspace(cfg, _lib.OP_DENSE_DECODE, 1, dev)
+    _need_ws(ws, cfg, _lib.OP_DENSE_DECODE, 1)
+    _need(out, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "out")
+    _need(lse, torch.float32, (cfg.B, cfg.H_q), "lse")
     c = cfg.c()
     check(lib().socket_dense_decode(ctypes.byref(c), _p(q), _p(K), _p(V), _p(seq_lens), _p(out),
                                     _p(lse), _p(ws), ws.numel(), _stream(q)))
@@ -295,23 +448,9 @@ def lse_combine(cfg: Config, partials, out=None, lse=None):
         out = torch.empty((cfg.B, cfg.H_q, cfg.d), dtype=torch.bfloat16, device=dev)
     if lse is None:
         lse = torch.empty((cfg.B, cfg.H_q), dtype=torch.float32, device=dev)
+    _need(out, torch.bfloat16, (cfg.B, cfg.H_q, cfg.d), "out")
+    _need(lse, torch.float32, (cfg.B, cfg.H_q), "lse")
     c = cfg.c()
     check(lib().socket_lse_combine(ctypes.byref(c), _p(partials), G, _p(out), _p(lse),
                                    _stream(partials)))
     return out, lse
-
-
-def topk_resolve(cfg: Config, cand_scores, cand_idx, rank: int, k: int, idx=None, cnt=None):
-    """Exact global top-k share of `rank` from all-gathered shard candidates."""
-    G = cand_scores.shape[0]
-    _need(cand_scores, torch.float32, (G, cfg.B, cfg.H_sel, k), "cand_scores")
-    _need(cand_idx, torch.int32, (G, cfg.B, cfg.H_sel, k), "cand_idx")
-    dev = cand_scores.device
-    if idx is None:
-        idx = torch.empty((cfg.B, cfg.H_sel, k), dtype=torch.int32, device=dev)
-    if cnt is None:
-        cnt = torch.empty((cfg.B, cfg.H_sel), dtype=torch.int32, device=dev)
-    c = cfg.c()
-    check(lib().socket_topk_resolve(ctypes.byref(c), _p(cand_scores), _p(cand_idx), G, rank, k,
-                                    _p(idx), _p(cnt), None, 0, _stream(cand_scores)))
-    return idx, cnt

@@ -1,13 +1,15 @@
 """Oracle-backed local-ops provider with the call signatures of
 paper_2602_06283_b200.ops, used ONLY by the CPU (gloo) tests of the shard
 layer (tests/test_dist_gloo.py).  It lets dist.py's orchestration -- the
-collectives, rank order, shard offsets and the exact resolve -- be checked on
-CPU processes; the CUDA kernels themselves are covered by the -m gpu tests.
+collectives, rank order, shard offsets and the exact sequence-shard top-k
+protocol (tests/shard_model.py) -- be checked on CPU processes; the CUDA
+kernels themselves are covered by the -m gpu tests.
 """
 import numpy as np
 import torch
 
 import oracle as O
+import shard_model as SM
 
 
 def _w(t):
@@ -36,8 +38,14 @@ def score(cfg, q, W, codes, vnorm, seq_lens, mask=None, out=None, ws=None):
         for r in range(cfg.H_sel):
             g = r if cfg.group_mode == O.GROUP_KV_SHARED else r // G
             w = O.soft_scores(T[b, r], codes[b, g].numpy())
-            s[b, r] = O.masked_value_scores(w, vnorm[b, g].double().numpy(), int(seq_lens[b]))
-    return torch.from_numpy(s)
+            n = max(0, min(int(seq_lens[b]) - cfg.index_base, cfg.N_max))   # global lengths
+            s[b, r] = O.masked_value_scores(w, vnorm[b, g].double().numpy(), n)
+    # the product's scores are fp32: round so the protocol sees the same kind of keys
+    t = torch.from_numpy(s).float()
+    if out is not None:
+        out.copy_(t)
+        return out
+    return t
 
 
 def topk(cfg, scores, seq_lens, k, sink=0, window=0, idx=None, cnt=None, sel_scores=None,
@@ -56,17 +64,61 @@ def topk(cfg, scores, seq_lens, k, sink=0, window=0, idx=None, cnt=None, sel_sco
     return (idx, cnt, sc) if want_scores else (idx, cnt)
 
 
-def topk_resolve(cfg, cand_scores, cand_idx, rank, k, idx=None, cnt=None):
-    G, B, H = cand_scores.shape[:3]
-    idx = torch.full((B, H, k), -1, dtype=torch.int32)
-    cnt = torch.zeros((B, H), dtype=torch.int32)
-    for b in range(B):
-        for r in range(H):
-            s = cand_scores[:, b, r].reshape(-1).numpy()        # position p = shard * k + i
-            S = O.topk_select(s, k, G * k)
-            mine = [int(cand_idx[rank, b, r, p % k]) for p in S if p // k == rank]
-            idx[b, r, :len(mine)] = torch.tensor(mine, dtype=torch.int32)
-            cnt[b, r] = len(mine)
+def _keys(cfg, scores, seq_lens, b, r, sink, window):
+    return SM.row_keys(scores[b, r].float().numpy(), int(seq_lens[b]), cfg.index_base, cfg.N_max,
+                       sink, window)
+
+
+def topk_digest(cfg, scores, seq_lens, k, shards, Q=64, sink=0, window=0, digest=None, ws=None):
+    d = torch.zeros((cfg.B, cfg.H_sel, Q, 2), dtype=torch.int64)
+    for b in range(cfg.B):
+        for r in range(cfg.H_sel):
+            d[b, r] = torch.tensor(SM.digest(_keys(cfg, scores, seq_lens, b, r, sink, window), k, shards, Q))
+    return d
+
+
+def topk_bracket(cfg, all_digests, k, state=None):
+    st = torch.zeros((cfg.B, cfg.H_sel, 8), dtype=torch.int64)
+    for b in range(cfg.B):
+        for r in range(cfg.H_sel):
+            digs = [[tuple(int(x) for x in p) for p in all_digests[s, b, r].tolist()]
+                    for s in range(all_digests.shape[0])]
+            st[b, r] = torch.tensor(SM.state_to_words(SM.bracket(digs, k)))
+    if state is not None:
+        state.copy_(st)
+        return state
+    return st
+
+
+def topk_window(cfg, scores, seq_lens, state, sink=0, window=0, msg=None, ws=None):
+    m = torch.zeros((cfg.B, cfg.H_sel, 8 + SM.CAP), dtype=torch.int64)
+    for b in range(cfg.B):
+        for r in range(cfg.H_sel):
+            st = SM.words_to_state(state[b, r].tolist())
+            m[b, r] = torch.tensor(SM.msg_to_words(SM.window(_keys(cfg, scores, seq_lens, b, r, sink, window), st)))
+    return m
+
+
+def topk_resolve(cfg, all_msgs, rank, state):
+    for b in range(cfg.B):
+        for r in range(cfg.H_sel):
+            msgs = [SM.words_to_msg(all_msgs[s, b, r].tolist()) for s in range(all_msgs.shape[0])]
+            st = SM.resolve(msgs, rank, SM.words_to_state(state[b, r].tolist()))
+            state[b, r] = torch.tensor(SM.state_to_words(st))
+    return state
+
+
+def topk_emit(cfg, scores, seq_lens, k, state, sink=0, window=0, idx=None, cnt=None, sel_scores=None,
+              ws=None):
+    for b in range(cfg.B):
+        for r in range(cfg.H_sel):
+            sel = SM.emit(_keys(cfg, scores, seq_lens, b, r, sink, window), SM.words_to_state(state[b, r].tolist()))
+            idx[b, r] = -1
+            if sel is None:
+                cnt[b, r] = -1
+                continue
+            idx[b, r, :len(sel)] = torch.tensor(sel, dtype=torch.int32)
+            cnt[b, r] = len(sel)
     return idx, cnt
 
 

@@ -42,7 +42,7 @@ def test_library_is_sm100a(L):
 
 
 def test_version_and_slots(L):
-    assert L.socket_version() == 2
+    assert L.socket_version() == 3
     assert [L.socket_code_slots(x) for x in (0, 1, 8, 9, 16, 17, 32, 33, 60, 64, 65, 128)] == \
         [0, 8, 8, 16, 16, 32, 32, 64, 64, 64, 96, 128]
 
@@ -58,6 +58,7 @@ def _cfg(**kw):
     (dict(L=0), 1), (dict(P=0), 1), (dict(P=17), 1), (dict(tau=0.0), 1),
     (dict(tau=-1.0), 1), (dict(d=64), 2), (dict(d=0), 1), (dict(H_q=6, H_kv=4), 1),
     (dict(N_max=100), 1), (dict(group_mode=7), 1), (dict(L=200), 2), (dict(scoring=2), 1),
+    (dict(flags=4), 1), (dict(index_base=-1), 1),
 ])
 def test_invalid_config_rejected(L, bad, status):
     c = _cfg(**bad)
@@ -84,8 +85,18 @@ def test_invalid_arguments_rejected(L):
     need = L.socket_workspace_bytes(ctypes.byref(c), 4, 16)
     assert need > 0
     assert L.socket_sparse_decode(ctypes.byref(c), d, d, d, d, d, 16, d, None, None, d, 16, None) == 4
-    # resolve rank out of range
-    assert L.socket_topk_resolve(ctypes.byref(c), d, d, 2, 2, 4, d, d, None, 0, None) == 1
+    # shard protocol: rank / shard count / Q out of range
+    assert L.socket_topk_resolve(ctypes.byref(c), d, 2, 2, d, None) == 1
+    assert L.socket_topk_resolve(ctypes.byref(c), d, 65, 0, d, None) == 1
+    assert L.socket_topk_digest(ctypes.byref(c), d, d, 4, 0, 0, 0, 64, d, None, 0, None) == 1
+    assert L.socket_topk_digest(ctypes.byref(c), d, d, 4, 0, 0, 2, 2, d, None, 0, None) == 1
+    assert L.socket_topk_bracket(ctypes.byref(c), d, 2, 64, 0, d, None) == 1
+    assert L.socket_topk_emit(ctypes.byref(c), d, d, 4, 3, 2, d, d, d, None, None, 0, None) == 1
+    # the decode step and sampling are single-buffer calls: index_base must be 0
+    cs = _cfg(index_base=64)
+    need = L.socket_workspace_bytes(ctypes.byref(cs), 7, 8)
+    assert L.socket_decode_step(ctypes.byref(cs), d, d, d, d, d, d, d, None, 0, None, None, 8, 0, 0,
+                                d, d, d, d, None, d, need, None) == 2
     # null cfg
     assert L.socket_query_tables(None, d, d, d, None) == 1
 
@@ -99,3 +110,8 @@ def test_workspace_sizes(L):
     # decode: split partials (m, l, o[128]) per (b, q head, split) + one ticket per unit
     w = L.socket_workspace_bytes(ctypes.byref(c), 4, 3277)
     assert w >= 2 * 32 * 130 * 4 + 2 * 8 * 4
+    # top-k: rows that fit one cluster's shared memory need no workspace; 1M-key
+    # rows keep their key slices in it (4 B per key)
+    assert L.socket_workspace_bytes(ctypes.byref(c), 3, 3277) == 0
+    c3 = _cfg(B=1, H_q=32, H_kv=8, N_max=1 << 20, L=60)
+    assert L.socket_workspace_bytes(ctypes.byref(c3), 3, 104858) == 8 * (1 << 20) * 4

@@ -26,6 +26,12 @@ from paper_2602_06283_b200 import Config, KV_SHARED, PER_QHEAD, SocketDecoder  #
 DEV = "cuda"
 
 
+def chained(cfg, on=True):
+    """cfg with SOCKET_FLAG_CHAINED_STEP: socket_decode_step never uses the one-launch kernel."""
+    import dataclasses
+    return dataclasses.replace(cfg, flags=1) if on else cfg
+
+
 def make(B, H_q, H_kv, N, L, P, seed=0, seq_lens=None, variant="gauss", tau=0.5, mode=KV_SHARED,
          n_needle=0):
     c = datagen.make_case(B, H_q, H_kv, N, 128, seed, variant=variant, seq_lens=seq_lens,
@@ -364,37 +370,6 @@ def test_cuda_graph_replay_matches_eager():
     assert torch.equal(out_e, out_g) and torch.equal(lse_e, lse_g)     # deterministic
 
 
-def test_topk_resolve_virtual_shards():
-    """Sequence sharding on one device: G virtual shards -> local top-k ->
-    (gathered) candidates -> resolve == single-device top-k of the whole row."""
-    G, Ns, k = 4, 4096, 1500
-    cfg_full = Config(B=2, H_q=8, H_kv=2, N_max=G * Ns, L=16, P=8)
-    cfg_sh = Config(B=2, H_q=8, H_kv=2, N_max=Ns, L=16, P=8)
-    g = torch.Generator(device=DEV).manual_seed(7)
-    full = (torch.randint(0, 50, (2, 2, G * Ns), generator=g, device=DEV).float() / 50)  # ties
-    full[1, :, 10000:] = -math.inf
-    lens_full = torch.tensor([G * Ns, 10000], dtype=torch.int32, device=DEV)
-    idx_full, cnt_full = ops.topk(cfg_full, full, lens_full, k)
-    cs, ci = [], []
-    for s in range(G):
-        part = full[:, :, s * Ns:(s + 1) * Ns].contiguous()
-        lens = torch.clamp(lens_full - s * Ns, 0, Ns).to(torch.int32)
-        i, n, sc = ops.topk(cfg_sh, part, lens, k, want_scores=True)
-        cs.append(sc)
-        ci.append(i)
-    cs, ci = torch.stack(cs), torch.stack(ci)
-    got = [[] for _ in range(2 * 2)]
-    for s in range(G):
-        i, n = ops.topk_resolve(cfg_sh, cs, ci, s, k)
-        for row in range(4):
-            b, r = divmod(row, 2)
-            got[row] += [int(x) + s * Ns for x in i[b, r, :n[b, r]].tolist()]
-    for row in range(4):
-        b, r = divmod(row, 2)
-        ref = idx_full[b, r, :cnt_full[b, r]].tolist()
-        assert got[row] == ref
-
-
 @pytest.mark.parametrize("B,k", [(16, 3277)])
 def test_full_size_c2_sampled(B, k):
     """BASELINE config 2 at full size (32 q / 8 kv heads, 32K, L=60, P=8,
@@ -449,14 +424,13 @@ def test_decode_step_fused_matches_unfused():
 
 
 @pytest.mark.parametrize("one_launch", [True, False])
-def test_decode_step_ragged_sink_window_mask_vs_oracle(one_launch, monkeypatch):
+def test_decode_step_ragged_sink_window_mask_vs_oracle(one_launch):
     """socket_decode_step with ragged lengths (the append hashes key seq_lens[b]-1
     of each sequence), sink/window forcing and a key mask, against the oracle --
     through the one-launch cluster kernel and through the PDL-chained kernels."""
-    if not one_launch:
-        monkeypatch.setenv("SOCKET_NO_FUSED", "1")
     lens = [3000, 4096, 1]
     cfg, c, W, d = make(3, 8, 2, 4096, 16, 8, seed=43, seq_lens=lens)
+    cfg = chained(cfg, not one_launch)
     k, sink, window = 300, 4, 16
     dec = SocketDecoder(cfg, d["W"], d["K"], d["V"], k=k, sink=sink, window=window)
     dec.prefill(n_tokens=4096)
@@ -488,13 +462,12 @@ def test_decode_step_ragged_sink_window_mask_vs_oracle(one_launch, monkeypatch):
 
 
 @pytest.mark.parametrize("one_launch", [True, False])
-def test_decode_step_with_new_rows(one_launch, monkeypatch):
+def test_decode_step_with_new_rows(one_launch):
     """socket_decode_step(k_new, v_new) stores the new token's rows into the
     cache at seq_lens[b] - 1 and gives exactly the result of writing them first."""
-    if not one_launch:
-        monkeypatch.setenv("SOCKET_NO_FUSED", "1")
     lens = [2048, 1500]
     cfg, c, W, d = make(2, 8, 2, 2048, 60, 8, seed=51, seq_lens=lens)
+    cfg = chained(cfg, not one_launch)
     g = torch.Generator(device=DEV).manual_seed(3)
     k_new = torch.randn((2, 2, 128), generator=g, device=DEV).to(torch.bfloat16)
     v_new = torch.randn((2, 2, 128), generator=g, device=DEV).to(torch.bfloat16)
@@ -515,14 +488,13 @@ def test_decode_step_with_new_rows(one_launch, monkeypatch):
 
 
 @pytest.mark.parametrize("one_launch", [True, False])
-def test_decode_step_host_inputs_equal_device_inputs(one_launch, monkeypatch):
+def test_decode_step_host_inputs_equal_device_inputs(one_launch):
     """q, k_new and v_new in pinned host memory (read in place by the one-launch
     kernel, staged by the copy kernel on the chained path) give bit-identical
     caches, selections and outputs to the same inputs on the device."""
-    if not one_launch:
-        monkeypatch.setenv("SOCKET_NO_FUSED", "1")
     lens = [2048, 1777]
     cfg, c, W, d = make(2, 8, 2, 2048, 60, 8, seed=57, seq_lens=lens)
+    cfg = chained(cfg, not one_launch)
     g = torch.Generator(device=DEV).manual_seed(5)
     k_new = torch.randn((2, 2, 128), generator=g, device=DEV).to(torch.bfloat16)
     v_new = torch.randn((2, 2, 128), generator=g, device=DEV).to(torch.bfloat16)
@@ -570,7 +542,7 @@ def test_host_step_graph_matches_device_step(B):
     (1, 4, 2, 8192, 60, [8190], 1, 0, 0),          # hard-LSH tables, n not a multiple of 32
     (4, 8, 2, 2048, 60, [2048, 1, 700, 2047], 0, 0, 4),
 ])
-def test_one_launch_step_matches_chained(B, H_q, H_kv, N, L, lens, scoring, sink, window, monkeypatch):
+def test_one_launch_step_matches_chained(B, H_q, H_kv, N, L, lens, scoring, sink, window):
     """The one-launch cluster step and the PDL-chained kernels agree on every
     output: codes, norms, scores and the selection bit for bit, attention to
     fp32 / bf16 rounding."""
@@ -580,9 +552,7 @@ def test_one_launch_step_matches_chained(B, H_q, H_kv, N, L, lens, scoring, sink
     k = max(sink + window, min(N // 8, 512))
     res = []
     for no_fused in (False, True):
-        if no_fused:
-            monkeypatch.setenv("SOCKET_NO_FUSED", "1")
-        dec = SocketDecoder(cfg, d["W"], d["K"].clone(), d["V"].clone(), k=k, sink=sink, window=window)
+        dec = SocketDecoder(chained(cfg, no_fused), d["W"], d["K"].clone(), d["V"].clone(), k=k, sink=sink, window=window)
         dec.prefill()
         out, lse = dec.step(d["q"], d["seq_lens"], append=True)
         res.append([t.clone() for t in (dec.codes, dec.vnorm, dec.scores, dec.idx, dec.cnt, out, lse)])

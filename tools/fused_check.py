@@ -1,9 +1,10 @@
 """Small-batch step timing: the one-launch cluster kernel vs the multi-kernel
-path (SOCKET_NO_FUSED=1), CUDA-graph replay, L2 flushed before each step.
+path (socket_cfg.flags = SOCKET_FLAG_CHAINED_STEP), CUDA-graph replay, L2 flushed before each step.
 
     python tools/fused_check.py [--batch 1 2] [--ctx 32768] [--sparsity 10 5]
 """
 import argparse
+import dataclasses
 import json
 import os
 import sys
@@ -53,11 +54,8 @@ def main():
                 res = {"ctx": N, "batch": B, "sparsity": sp, "k": k}
                 outs = {}
                 for mode in ("fused", "multi"):
-                    if mode == "multi":
-                        os.environ["SOCKET_NO_FUSED"] = "1"
-                    else:
-                        os.environ.pop("SOCKET_NO_FUSED", None)
-                    dec = SocketDecoder(cfg, W, K, V, k=k)
+                    cm = dataclasses.replace(cfg, flags=_lib.FLAG_CHAINED_STEP if mode == "multi" else 0)
+                    dec = SocketDecoder(cm, W, K, V, k=k)
                     dec.prefill()
                     dec.capture(q, lens, append=True)
                     res[mode + "_us"] = round(timed(dec.replay, flush), 2)
@@ -65,7 +63,6 @@ def main():
                     torch.cuda.synchronize()
                     outs[mode] = (dec.out.float().clone(), dec.idx.clone(), dec.scores.clone())
                     del dec
-                os.environ.pop("SOCKET_NO_FUSED", None)
                 res["same_idx"] = bool(torch.equal(outs["fused"][1], outs["multi"][1]))
                 res["same_scores"] = bool(torch.equal(outs["fused"][2], outs["multi"][2]))
                 res["max_out_diff"] = float((outs["fused"][0] - outs["multi"][0]).abs().max())
