@@ -480,3 +480,40 @@ def test_sampling_estimator_is_unbiased():
     runs = np.stack([O.sampling_estimator(s, vn, V, N, r.uniform(size=256))[1] for _ in range(400)])
     se = runs.std(axis=0, ddof=1) / np.sqrt(runs.shape[0])
     assert np.all(np.abs(runs.mean(axis=0) - y) < 5 * se + 1e-12)
+
+
+# ---------------------------------------------------------------------------
+# input widening (bf16 bits -> float64)
+# ---------------------------------------------------------------------------
+def test_widen_hand_values():
+    """Exact values of hand-picked bf16 bit patterns: the bf16 format is the top
+    16 bits of an IEEE binary32 (sign, 8 exponent bits, 7 fraction bits)."""
+    cases = {
+        0x0000: 0.0, 0x3F80: 1.0, 0xC000: -2.0, 0x3F81: 1.0 + 2.0 ** -7, 0x4049: 3.140625,
+        0x0001: 2.0 ** -133,                          # smallest subnormal: 2^-126 * 2^-7
+        0x0080: 2.0 ** -126,                          # smallest normal
+        0x7F7F: (2.0 - 2.0 ** -7) * 2.0 ** 127,      # max finite
+        0xFF7F: -(2.0 - 2.0 ** -7) * 2.0 ** 127,
+    }
+    got = O.widen(np.array(list(cases), dtype=np.uint16))
+    assert np.array_equal(got, np.array(list(cases.values())))
+    neg0 = O.widen(np.array([0x8000], dtype=np.uint16))[0]
+    assert neg0 == 0.0 and math.copysign(1.0, neg0) == -1.0
+    inf = O.widen(np.array([0x7F80, 0xFF80], dtype=np.uint16))
+    assert inf[0] == math.inf and inf[1] == -math.inf
+
+
+def test_widen_round_trips_datagen_rounding():
+    """widen inverts datagen's fp32 -> bf16 rounding on values that are already
+    bf16 (the rounding is then exact), and stays within half a bf16 ulp of the
+    fp32 input otherwise (round-to-nearest)."""
+    import datagen
+    r = rng(77)
+    x = r.standard_normal(20000).astype(np.float32) * np.float32(10.0) ** r.integers(-30, 30, 20000).astype(np.float32)
+    bits = datagen.bf16_bits_from_f32(x)
+    w = O.widen(bits)
+    assert np.array_equal(datagen.bf16_bits_from_f32(w.astype(np.float32)), bits)
+    ulp = np.abs(w) * 2.0 ** -8
+    assert np.all(np.abs(w - x.astype(np.float64)) <= ulp * (1 + 1e-12) + 1e-45)
+    # the sign is the top bit, the magnitude the rest
+    assert np.array_equal(np.signbit(w), (bits >> 15).astype(bool))
