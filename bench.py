@@ -301,6 +301,7 @@ class Ctx:
                 os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
                 os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
                 os.environ.setdefault("RANK", "0")
+                os.environ.setdefault("WORLD_SIZE", "1")
             dist.init_process_group("nccl", device_id=self.dev)
             self.pg = True
 
