@@ -15,6 +15,7 @@ constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int kBins = 2048;
 constexpr int kCandCap = 2048;
+constexpr int kMaxCluster = 16;   // CTAs per cluster (non-portable maximum)
 
 #ifdef SK_TRACE
 // phase stamps (clock64 of thread 0 of every CTA), read by tools/trace_topk.py
@@ -264,10 +265,17 @@ __device__ __forceinline__ void topk_core(const TopkArgs& a, uint32_t* keys, Top
     // followed by a descending suffix scan that locates the bin of rank `need`
     if (warp == 0) {
       uint32_t c0 = 0, c1 = 0;                 // coarse bins 63 - 2 lane, 62 - 2 lane
-      for (int r = 0; r < csize; ++r) {
-        const uint32_t* rc = cluster.map_shared_rank(S.coarse, r);
-        c0 += rc[63 - 2 * lane];
-        c1 += rc[62 - 2 * lane];
+      {   // all ranks' loads in flight at once (a DSMEM load is ~200 cycles)
+        uint32_t v0[kMaxCluster], v1[kMaxCluster];
+#pragma unroll
+        for (int r = 0; r < kMaxCluster; ++r) {
+          const uint32_t* rc = cluster.map_shared_rank(S.coarse, r < csize ? r : 0);
+          v0[r] = rc[63 - 2 * lane];
+          v1[r] = rc[62 - 2 * lane];
+        }
+#pragma unroll
+        for (int r = 0; r < kMaxCluster; ++r)
+          if (r < csize) { c0 += v0[r]; c1 += v1[r]; }
       }
       const uint32_t tot = c0 + c1;
       uint32_t inc = tot;
@@ -286,7 +294,13 @@ __device__ __forceinline__ void topk_core(const TopkArgs& a, uint32_t* keys, Top
       // fine bins of cb: lane l holds bin cb*32 + 31 - l (descending)
       const int fb = cb * 32 + 31 - lane;
       uint32_t f = 0;
-      for (int r = 0; r < csize; ++r) f += cluster.map_shared_rank(S.hist, r)[fb];
+      {
+        uint32_t v[kMaxCluster];
+#pragma unroll
+        for (int r = 0; r < kMaxCluster; ++r) v[r] = cluster.map_shared_rank(S.hist, r < csize ? r : 0)[fb];
+#pragma unroll
+        for (int r = 0; r < kMaxCluster; ++r) f += r < csize ? v[r] : 0u;
+      }
       uint32_t finc = f;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -426,8 +440,11 @@ __device__ __forceinline__ void topk_core(const TopkArgs& a, uint32_t* keys, Top
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int bin = 255 - (lane * 8 + q);
-          uint32_t s = 0;
-          for (int c = 0; c < csize; ++c) s += *cluster.map_shared_rank(&hb[bin], c);
+          uint32_t s = 0, v[kMaxCluster];
+#pragma unroll
+          for (int c = 0; c < kMaxCluster; ++c) v[c] = *cluster.map_shared_rank(&hb[bin], c < csize ? c : 0);
+#pragma unroll
+          for (int c = 0; c < kMaxCluster; ++c) s += c < csize ? v[c] : 0u;
           c8[q] = s;
           tot += s;
         }
@@ -516,10 +533,17 @@ __device__ __forceinline__ void topk_emit(const TopkArgs& a, uint32_t* keys, Top
     if (tid == 0) { S.stat[6] = gtot; S.stat[7] = etot; }
     cluster.sync();
     uint32_t gb = 0, eb = 0;
-    for (int r = 0; r < crank; ++r) {
-      const uint32_t* rs = cluster.map_shared_rank(S.stat, r);
-      gb += rs[6];
-      eb += rs[7];
+    {
+      uint32_t vg[kMaxCluster], ve[kMaxCluster];
+#pragma unroll
+      for (int r = 0; r < kMaxCluster; ++r) {
+        const uint32_t* rs = cluster.map_shared_rank(S.stat, r < crank ? r : 0);
+        vg[r] = rs[6];
+        ve[r] = rs[7];
+      }
+#pragma unroll
+      for (int r = 0; r < kMaxCluster; ++r)
+        if (r < crank) { gb += vg[r]; eb += ve[r]; }
     }
     gbase = (int)(gb + gw);
     ebase = (int)(eb + ew);
