@@ -1,8 +1,8 @@
 // Fused small-batch decode step: one launch, one thread-
-// block CLUSTER of CS CTAs (16, or 8 when more rows must be co-resident) per
-// selection row (b, kv head) in KV_SHARED mode, CTA c owning the key slice
-// [c S, (c+1) S), about 100 KB of shared memory per CTA so two clusters of 16
-// can share a GPC (14 co-resident clusters of 16 on 148 SMs):
+// block CLUSTER of CS CTAs (8; 16 when the rows' clusters of 16 are all
+// co-resident) per selection row (b, kv head) in KV_SHARED mode, CTA c owning
+// the key slice [c S, (c+1) S), one CTA per SM (two CTAs per SM were measured
+// to share an SM's shared-memory bandwidth and registers and ran slower):
 //
 //   A. tables (Alg. 2): CTA c projects q on the W rows of tables
 //      [c tpc, (c+1) tpc) (fp64 tensor-core DMMA), turns them into sigma
@@ -47,6 +47,10 @@ static __device__ unsigned long long g_fused_trace[4096 * 8];
 extern "C" int socket_debug_fused_trace(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, g_fused_trace, (size_t)n * sizeof(unsigned long long));
 }
+// this translation unit's copy of the top-k phase stamps (TK_TRACE in topk_dev.cuh)
+extern "C" int socket_debug_fused_topk_trace(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_topk_trace, (size_t)n * sizeof(unsigned long long));
+}
 #else
 #define FU_STAMP(i) \
   do {              \
@@ -84,6 +88,7 @@ struct FusedArgs {
   int tpc;     // tables per CTA
   int gt;      // tables per LUT-build group
   int zoneB;   // bytes of zone B (sigma factors + half tables | keys)
+  int smem;    // dynamic shared memory bytes (zone A + zone B, or the attention ring)
 };
 
 // zone B: sigma factors [NH][8 bits][2][LP] + half tables [NH][2][16][GT], or the keys
@@ -119,7 +124,7 @@ __device__ __forceinline__ void f_load_tile(FTile<LP>& t, const uint8_t* tile_co
 }
 
 template <int NH, int LP>
-__global__ void __launch_bounds__(kFThreads, 2) fused_step_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
   extern __shared__ __align__(1024) char fsm[];
   __shared__ float s_part[NH][kD + 2];          // this CTA's (m, l, o) per head (log2 units)
   __shared__ float s_ks[kD];
@@ -312,28 +317,39 @@ __global__ void __launch_bounds__(kFThreads, 2) fused_step_kernel(FusedArgs a) {
       }
       __syncthreads();
       // LUT entries T(rr) = sum_h lo_h(rr & 15) hi_h(rr >> 4), 4 tables per task
+      // (one float4 per head and half; GT is a multiple of 4 or LP < 4)
       const int ng = (GT + 3) >> 2;
       for (int e = tid; e < 256 * ng; e += kFThreads) {
         const int q4 = e % ng, rr = e / ng;
         const int tl = q4 * 4, l = gl0 + tl;
-        float T[4] = {0.f, 0.f, 0.f, 0.f};
+        float4 T = make_float4(0.f, 0.f, 0.f, 0.f);
         if (rr < R) {
+          if (GT >= 4) {
 #pragma unroll
-          for (int h = 0; h < NH; ++h) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              if (tl + u < GT)
-                T[u] = fmaf(s_half[((h * 2 + 0) * 16 + (rr & 15)) * GT + tl + u],
-                            s_half[((h * 2 + 1) * 16 + (rr >> 4)) * GT + tl + u], T[u]);
+            for (int h = 0; h < NH; ++h) {
+              const float4 lo = *reinterpret_cast<const float4*>(s_half + ((h * 2 + 0) * 16 + (rr & 15)) * GT + tl);
+              const float4 hv = *reinterpret_cast<const float4*>(s_half + ((h * 2 + 1) * 16 + (rr >> 4)) * GT + tl);
+              T.x = fmaf(lo.x, hv.x, T.x);
+              T.y = fmaf(lo.y, hv.y, T.y);
+              T.z = fmaf(lo.z, hv.z, T.z);
+              T.w = fmaf(lo.w, hv.w, T.w);
             }
+          } else {
+            float* tp = &T.x;
+            for (int u = 0; u < GT; ++u)
+#pragma unroll
+              for (int h = 0; h < NH; ++h)
+                tp[u] = fmaf(s_half[((h * 2 + 0) * 16 + (rr & 15)) * GT + u],
+                             s_half[((h * 2 + 1) * 16 + (rr >> 4)) * GT + u], tp[u]);
           }
         }
+        const float tv[4] = {T.x, T.y, T.z, T.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (tl + u >= GT) continue;
-          const float tv = (l + u < L) ? T[u] : 0.f;
-          if (LP >= 32) lut[rr * 64 + l + u] = tv;
-          else for (int cc = l + u; cc < 32; cc += LP) lut[rr * 64 + cc] = tv;   // column c: table c mod LP
+          const float v = (l + u < L) ? tv[u] : 0.f;
+          if (LP >= 32) lut[rr * 64 + l + u] = v;
+          else for (int cc = l + u; cc < 32; cc += LP) lut[rr * 64 + cc] = v;   // column c: table c mod LP
         }
       }
       __syncthreads();
@@ -386,16 +402,22 @@ __global__ void __launch_bounds__(kFThreads, 2) fused_step_kernel(FusedArgs a) {
       nforced += key == 0xFFFFFFFFu;
       if (key != 0u && key != 0xFFFFFFFFu) { kmin = min(kmin, key); kmax = max(kmax, key); }
     };
-    // two tiles per warp in registers: the next one loads while the current one is
-    // looked up (two CTAs per SM share the register file: <= 64 registers)
-    FTile<LP> x0, x1;
+    // four tiles per warp in registers: the next two load while the current two
+    // are looked up
+    FTile<LP> x0, x1, y0, y1;
     int ti = warp;
     if (ti < vt) f_load_tile<LP>(x0, crow + (size_t)(t0 + ti) * 32 * LP, vrow + (t0 + ti) * 32, lane, pol_code);
-    for (; ti < vt; ti += kFWarps) {
-      if (ti + kFWarps < vt)
-        f_load_tile<LP>(x1, crow + (size_t)(t0 + ti + kFWarps) * 32 * LP, vrow + (t0 + ti + kFWarps) * 32, lane, pol_code);
+    if (ti + kFWarps < vt)
+      f_load_tile<LP>(x1, crow + (size_t)(t0 + ti + kFWarps) * 32 * LP, vrow + (t0 + ti + kFWarps) * 32, lane, pol_code);
+    for (; ti < vt; ti += 2 * kFWarps) {
+      if (ti + 2 * kFWarps < vt)
+        f_load_tile<LP>(y0, crow + (size_t)(t0 + ti + 2 * kFWarps) * 32 * LP, vrow + (t0 + ti + 2 * kFWarps) * 32, lane, pol_code);
+      if (ti + 3 * kFWarps < vt)
+        f_load_tile<LP>(y1, crow + (size_t)(t0 + ti + 3 * kFWarps) * 32 * LP, vrow + (t0 + ti + 3 * kFWarps) * 32, lane, pol_code);
       score_tile(x0, ti);
-      x0 = x1;
+      if (ti + kFWarps < vt) score_tile(x1, ti + kFWarps);
+      x0 = y0;
+      x1 = y1;
     }
     // tiles past seq_len: -inf scores, invalid keys
     for (int tz = vt + warp; tz < tiles; tz += kFWarps) {
@@ -433,7 +455,7 @@ __global__ void __launch_bounds__(kFThreads, 2) fused_step_kernel(FusedArgs a) {
   FU_STAMP(6);
   // ===== D. attention over my selected rows + cluster LSE merge =====================
   {
-    const int att_warps = min(kFWarps, (kFZoneA + a.zoneB) / (2 * kTileBytes));   // 2 ring stages each
+    const int att_warps = min(kFWarps, a.smem / (2 * kTileBytes));   // 2 ring stages each
     const int gid = lane >> 2, tig = lane & 3;
     const int h0 = g * NH;
     uint32_t qb[8][2];
@@ -624,7 +646,13 @@ static void* fused_kernel_ptr(int NH, int Lp) {
   return nullptr;
 }
 
-static size_t fused_smem(int NH, int Lp, int S) { return (size_t)kFZoneA + fused_zone_b(NH, Lp, S); }
+// one CTA per SM anyway: the rest of the shared memory deepens the attention ring
+// (13 warps x 2 stages x 8 KB)
+constexpr size_t kFRingBytes = 13 * 2 * kTileBytes;
+static size_t fused_smem(int NH, int Lp, int S) {
+  const size_t z = (size_t)kFZoneA + fused_zone_b(NH, Lp, S);
+  return z > kFRingBytes ? z : kFRingBytes;
+}
 
 // co-resident clusters of CS CTAs of this kernel instance (queried once per
 // device / shape): the whole grid must be one wave, since the CTAs of a cluster
@@ -735,6 +763,7 @@ socket_status launch_fused_step(const socket_cfg& c, const void* q, void* K, voi
   a.gt = fused_gt(NH, Lp);
   a.zoneB = (int)fused_zone_b(NH, Lp, S);
   const size_t sm = fused_smem(NH, Lp, S);
+  a.smem = (int)sm;
   void* fn = fused_kernel_ptr(NH, Lp);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return fail(SOCKET_ECUDA, "fused step: shared memory request rejected");

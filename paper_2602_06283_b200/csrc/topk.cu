@@ -378,7 +378,11 @@ static void topk_geometry(int rows, int n_max_row, int& cs, int& per, bool& gk) 
   // is below one CTA per SM and the slices stay >= 4096 keys (smaller slices cost
   // more in cluster synchronization than they save; tools/tune_step.py, B = 1-16)
   constexpr int kMinSlice = 4096;
+#ifdef SK_TOPK_MIN_CTAS   // experiments only (tools/variant_build.py); not a runtime knob
+  const int min_ctas = SK_TOPK_MIN_CTAS;
+#else
   const int min_ctas = num_sms();
+#endif
   while (cs < 16 && ((size_t)(n_max_row + cs - 1) / cs > kMaxSlice ||
                      (rows * cs < min_ctas && (n_max_row + 2 * cs - 1) / (2 * cs) >= kMinSlice)))
     cs *= 2;

@@ -16,8 +16,10 @@ import torch  # noqa: E402
 
 from trace_topk import build_trace  # noqa: E402
 
-PH = ["stage q/W", "DMMA+sigma+half+append", "LUT to cluster", "cluster sync", "score slice",
+PH = ["stage q/W", "DMMA+sigma+append+push", "cluster sync", "LUT build", "score slice",
       "top-k", "attend + merge"]
+TK = ["stat_sync", "hist", "hist_sync", "ghist_scan", "cand", "cand_sync", "gather_select", "count",
+      "emit", "tail", "final_sync"]
 
 
 def main():
@@ -51,6 +53,16 @@ def main():
     for i in range(7):
         d = t[:, i + 1] - t[:, i]
         print(f"   {PH[i]:24s} median {np.median(d):8.0f}  max {np.max(d):8.0f} cycles")
+    # top-k sub-phases (TK_TRACE stamps 2..13 of topk_core; 0/1 are not stamped here)
+    tb = (ctypes.c_ulonglong * (4096 * 16))()
+    if L.socket_debug_fused_topk_trace(tb, 4096 * 16) == 0:
+        u = np.frombuffer(tb, dtype=np.uint64).reshape(4096, 16).astype(np.int64)
+        u = u[u[:, 2] != 0]
+        for i in range(2, 13):
+            ok = (u[:, i + 1] != 0) & (u[:, i] != 0)
+            if ok.any():
+                d = u[ok, i + 1] - u[ok, i]
+                print(f"     topk {TK[i - 2]:14s} median {np.median(d):8.0f}  max {np.max(d):8.0f} cycles")
 
 
 if __name__ == "__main__":
