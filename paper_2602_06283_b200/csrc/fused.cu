@@ -1,34 +1,23 @@
 // Fused small-batch decode step: one launch, one thread-
-// block CLUSTER of CS CTAs (8; 16 when the rows' clusters of 16 are all
-// co-resident) per selection row (b, kv head) in KV_SHARED mode, CTA c owning
-// the key slice [c S, (c+1) S), one CTA per SM (two CTAs per SM were measured
-// to share an SM's shared-memory bandwidth and registers and ran slower):
+// block CLUSTER per selection row (b, kv head) in KV_SHARED mode, CS CTAs per
+// cluster, CTA c owning the key slice [c S, (c+1) S):
 //
 //   A. tables (Alg. 2): CTA c projects q on the W rows of tables
-//      [c tpc, (c+1) tpc) (fp64 tensor-core DMMA), turns them into sigma
-//      factors sigma(+-2u/tau) and pushes only those factors (2 floats per
-//      head and W row) to every CTA of the cluster through distributed shared
-//      memory; with append, it also hashes the newest key on its tables
-//      (Alg. 1) -> codes.  After one cluster barrier every CTA builds
-//      the whole LUT image from the factors (fp64 half tables, fp32 group sum)
-//      -- the same arithmetic as the chained path's prologue, bit for bit;
-//   B. scores (Eq. 4 / Alg. 4): the CTA streams its slice's codes and norms
-//      straight into registers (16-byte loads, two tiles in flight per warp),
+//      [c tpc, (c+1) tpc) (fp64 tensor-core DMMA), builds their sigma factors,
+//      half tables and LUT columns, and writes the columns into the LUT of
+//      EVERY CTA of the cluster (distributed shared memory); with append, it
+//      also hashes the newest key on those tables (Alg. 1) -> codes;
+//   B. scores (Eq. 4 / Alg. 4): the CTA streams its slice's codes and norms,
 //      scores = ||v|| * sum_l LUT, written to `scores` and kept in shared
 //      memory as monotone keys (sink/window forced, invalid 0);
-//   C. top-k (Alg. 3 l.244): topk_core over the cluster's slices (no score
-//      round trip); each CTA's selected rows are its contiguous share of idx;
-//   D. sparse attention (Eq. 2, exact logits P:271): the CTA's warps gather
-//      their selected K/V rows into a ring over the dead LUT / key zones and
-//      attend (tensor-core MMA tiles, online softmax); the cluster merges the
-//      CS partial states by LSE through distributed shared memory.
+//   C. top-k (Alg. 3 l.244): topk_core over the cluster's shared-memory slices
+//      (no score round trip); each CTA keeps its own selected rows;
+//   D. sparse attention (Eq. 2, exact logits P:271): the CTA attends over its
+//      selected rows (tensor-core MMA tiles, online softmax), and the cluster
+//      merges the CS partial states by LSE through distributed shared memory.
 //
 // Same arithmetic as the multi-kernel path, stage by stage, except the split
 // of the attention (per CTA slice here), so the outputs agree to fp32 rounding.
-#include <map>
-#include <mutex>
-#include <tuple>
-
 #include "mma_dev.cuh"
 #include "score_dev.cuh"
 #include "topk_dev.cuh"
@@ -59,12 +48,17 @@ extern "C" int socket_debug_fused_topk_trace(unsigned long long* host, int n) {
 
 constexpr int kFThreads = kTopkThreads;   // 512
 constexpr int kFWarps = kFThreads / 32;
-constexpr int kFZoneA = 64 * 1024;        // LUT image | projection staging | top-k shared | KV ring
-constexpr int kFWs = 72;                  // staged W row stride (floats): [t][w], w < 64
-constexpr int kFQs = 8;                   // staged q row stride (doubles): [t][h]
-constexpr int kFMaxSlice = 8192;          // keys per CTA slice (zone B holds them as u32)
-static_assert(sizeof(TopkShared) <= kFZoneA, "top-k state must fit zone A");
-static_assert(kD * kFQs * 8 + kD * kFWs * 4 <= kFZoneA, "projection staging must fit zone A");
+constexpr int kFScoreStages = 2;
+constexpr int kFAttWarps = 8;
+constexpr int kFAttStages = 2;
+constexpr int kFLutBytes = 256 * 64 * 4;                                   // 64 KB
+constexpr int kFRingBytes = kFWarps * kFScoreStages * TileStage<64>::BYTES; // 68 KB
+constexpr int kFZone = kFLutBytes + kFRingBytes;                          // LUT + score ring
+static_assert(kFZone >= kFAttWarps * kFAttStages * kTileBytes, "attention ring must fit the zone");
+static_assert(128 * 8 * 8 + 128 * 72 * 4 + 8 * (8 * 2 * 16 + 2 * 16 * 16) * 4 <= kFRingBytes,
+              "table staging must fit the ring zone");
+constexpr int kFWs = 72;    // staged W row stride (floats): [t][w]
+constexpr int kFQs = 8;     // staged q row stride (doubles): [t][h]
 
 struct FusedArgs {
   const uint16_t* q;
@@ -82,54 +76,21 @@ struct FusedArgs {
   int32_t* cnt;
   uint16_t* out;
   float* lse;
-  int H_q, H_kv, N_max, L, P, k, sink, window, do_append, hard;
+  int H_q, H_kv, N_max, L, P, Lp, k, sink, window, do_append, hard;
   float tau, scale_log2;
-  int S;       // keys per CTA slice (multiple of 128)
-  int tpc;     // tables per CTA
-  int gt;      // tables per LUT-build group
-  int zoneB;   // bytes of zone B (sigma factors + half tables | keys)
-  int smem;    // dynamic shared memory bytes (zone A + zone B, or the attention ring)
+  int S;     // keys per CTA slice (multiple of 128)
+  int tpc;   // tables per CTA
 };
 
-// zone B: sigma factors [NH][8 bits][2][LP] + half tables [NH][2][16][GT], or the keys
-static int fused_gt(int NH, int LP) { return NH >= 8 ? (LP < 8 ? LP : 8) : (LP < 16 ? LP : 16); }
-static size_t fused_zone_b(int NH, int LP, int S) {
-  const size_t fx = (size_t)NH * 8 * 2 * LP * 4, half = (size_t)NH * 2 * 16 * fused_gt(NH, LP) * 4;
-  const size_t keys = (size_t)S * 4;
-  const size_t z = fx + half > keys ? fx + half : keys;
-  return (z + 1023) & ~(size_t)1023;
-}
-
-template <int LP>
-struct FTile {   // one 32-key tile of a lane: its code words and norm (register-fed scoring)
-  uint32_t w[LP / 4];
-  float vn;
-};
-
-template <int LP>
-__device__ __forceinline__ void f_load_tile(FTile<LP>& t, const uint8_t* tile_codes, const float* tile_vn, int lane,
-                                            uint64_t pol) {
-  constexpr int CB = LP < 16 ? LP : 16;
-#pragma unroll
-  for (int ch = 0; ch < LP / CB; ++ch) {
-    if constexpr (CB == 16) {
-      const uint4 v = ldg_nc_v4_hint(tile_codes + ch * 512 + lane * 16, pol);
-      t.w[ch * 4 + 0] = v.x; t.w[ch * 4 + 1] = v.y; t.w[ch * 4 + 2] = v.z; t.w[ch * 4 + 3] = v.w;
-    } else {
-      const uint2 v = ldg_nc_v2_hint(tile_codes + ch * 256 + lane * 8, pol);
-      t.w[ch * 2 + 0] = v.x; t.w[ch * 2 + 1] = v.y;
-    }
-  }
-  t.vn = __ldg(tile_vn + lane);
-}
+size_t fused_smem_bytes(int S) { return (size_t)kFZone + (size_t)S * 4; }
 
 template <int NH, int LP>
 __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
   extern __shared__ __align__(1024) char fsm[];
+  __shared__ TopkShared TS;
   __shared__ float s_part[NH][kD + 2];          // this CTA's (m, l, o) per head (log2 units)
   __shared__ float s_ks[kD];
   __shared__ uint32_t s_bits[64];
-  __shared__ float s_loc[NH][8][2][8];          // my sigma factors [h][bit][s][table < tpc <= 8]
   cg::cluster_group cluster = cg::this_cluster();
   const int c = (int)cluster.block_rank();
   const int CS = (int)cluster.num_blocks();
@@ -138,244 +99,256 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int P = a.P, L = a.L;
   const int n = a.seq_lens[b];
-  float* lut = reinterpret_cast<float*>(fsm);                       // zone A
-  char* zoneB = fsm + kFZoneA;
-  float* s_fx = reinterpret_cast<float*>(zoneB);                    // [NH][8][2][LP]
-  float* s_half = s_fx + NH * 8 * 2 * LP;                           // [NH][2][16][gt]
-  uint32_t* keys = reinterpret_cast<uint32_t*>(zoneB);              // after the LUT is built
+  float* lut = reinterpret_cast<float*>(fsm);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(fsm + kFZone);
 
   FU_STAMP(0);
-  // ===== A1. projections + sigma factors of my tables, append of the newest key =====
+  // ===== A. tables of my tables + append of the newest key ========================
   const int l0 = c * a.tpc;
-  const int nw = max(0, min(a.tpc, L - l0)) * P;          // my valid W rows (<= 64)
-  const bool app = a.do_append && n > 0 && n <= a.N_max;  // an outgrown cache is not written
-  double* qs = reinterpret_cast<double*>(fsm);                        // [t][kFQs]
-  float* ws = reinterpret_cast<float*>(fsm + kD * kFQs * 8);         // [t][kFWs]
+  const int ntab = max(0, min(a.tpc, LP - l0));           // my tables (incl. padding ones)
+  const int nw = max(0, min(a.tpc, L - l0)) * P;          // my valid W rows
   {
+    double* qs = reinterpret_cast<double*>(fsm + kFLutBytes);              // [t][kFQs]
+    float* ws = reinterpret_cast<float*>(fsm + kFLutBytes + kD * kFQs * 8);  // [t][kFWs]
+    float* s_fx = ws + kD * kFWs;                       // sigma factors [h][bit][c][table]
+    float* s_half = s_fx + NH * 8 * 2 * 16;             // half tables [h][hi][entry][table]
     const int h0 = g * NH;
-    uint4 vw[2], vq;
-    const int m = tid & 7, cq = (tid >> 3) & 15;
-    vq = make_uint4(0, 0, 0, 0);
-    if (tid < 128 && m < NH) vq = __ldg(reinterpret_cast<const uint4*>(a.q + ((size_t)b * a.H_q + h0 + m) * kD) + cq);
+    {   // q: 8 (padded) vectors x 16 uint4; W: 64 rows x 16 uint4 -- all loads first
+      uint4 vw[2], vq;
+      const int m = tid & 7, cq = (tid >> 3) & 15;
+      vq = make_uint4(0, 0, 0, 0);
+      if (tid < 128 && m < NH) vq = __ldg(reinterpret_cast<const uint4*>(a.q + ((size_t)b * a.H_q + h0 + m) * kD) + cq);
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int e = tid + u * kFThreads, w = e & 63, cw = e >> 6;
-      vw[u] = make_uint4(0, 0, 0, 0);
-      if (w < nw) vw[u] = __ldg(reinterpret_cast<const uint4*>(a.W + (size_t)(l0 * P + w) * kD) + cw);
+      for (int u = 0; u < 2; ++u) {
+        const int e = tid + u * kFThreads, w = e & 63, cw = e >> 6;
+        vw[u] = make_uint4(0, 0, 0, 0);
+        if (w < nw) vw[u] = __ldg(reinterpret_cast<const uint4*>(a.W + (size_t)(l0 * P + w) * kD) + cw);
+      }
+      if (tid < 128) {
+        const uint32_t w4[4] = {vq.x, vq.y, vq.z, vq.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) qs[(cq * 8 + e) * kFQs + m] = (double)((e & 1) ? bf16hi(w4[e >> 1]) : bf16lo(w4[e >> 1]));
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = tid + u * kFThreads, w = e & 63, cw = e >> 6;
+        const uint32_t w4[4] = {vw[u].x, vw[u].y, vw[u].z, vw[u].w};
+#pragma unroll
+        for (int e2 = 0; e2 < 8; ++e2) ws[(cw * 8 + e2) * kFWs + w] = (e2 & 1) ? bf16hi(w4[e2 >> 1]) : bf16lo(w4[e2 >> 1]);
+      }
     }
-    if (app && tid >= 384) {   // the newest key: 128 dims over 128 threads
-      const int t = tid - 384;
+    const bool app = a.do_append && n > 0 && n <= a.N_max;   // outgrown cache: no write
+    if (app && tid < kD) {
       const size_t crow = (((size_t)b * a.H_kv + g) * a.N_max + n - 1) * kD;
       if (a.k_new) {   // the new rows come from k_new / v_new; CTA 0 stores them in the cache
         const size_t nrow = ((size_t)b * a.H_kv + g) * kD;
-        const uint16_t kv = a.k_new[nrow + t];
-        s_ks[t] = bf16lo((uint32_t)kv);
+        const uint16_t kv = a.k_new[nrow + tid];
+        s_ks[tid] = bf16lo((uint32_t)kv);
         if (c == 0) {
-          a.K[crow + t] = kv;
-          a.V[crow + t] = a.v_new[nrow + t];
+          a.K[crow + tid] = kv;
+          a.V[crow + tid] = a.v_new[nrow + tid];
         }
       } else {
-        s_ks[t] = bf16lo((uint32_t)a.K[crow + t]);
+        s_ks[tid] = bf16lo((uint32_t)a.K[crow + tid]);
       }
     }
-    if (tid < 128) {
-      const uint32_t w4[4] = {vq.x, vq.y, vq.z, vq.w};
-#pragma unroll
-      for (int e = 0; e < 8; ++e) qs[(cq * 8 + e) * kFQs + m] = (double)((e & 1) ? bf16hi(w4[e >> 1]) : bf16lo(w4[e >> 1]));
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int e = tid + u * kFThreads, w = e & 63, cw = e >> 6;
-      const uint32_t w4[4] = {vw[u].x, vw[u].y, vw[u].z, vw[u].w};
-#pragma unroll
-      for (int e2 = 0; e2 < 8; ++e2) ws[(cw * 8 + e2) * kFWs + w] = (e2 & 1) ? bf16hi(w4[e2 >> 1]) : bf16lo(w4[e2 >> 1]);
-    }
-  }
-  __syncthreads();
-  FU_STAMP(1);
-  // x[h][w] = q_h . W_w in fp64 on the tensor cores: warp w owns W rows
-  // 8 (w & 7) .. + 7 over the K half w >> 3; x = (K half 0) + (K half 1) -- the
-  // same decomposition as the chained prologue's tables tiles, so the LUTs agree
-  // bit for bit
-  {
-    const int nt8 = warp & 7, kh = warp >> 3;
-    double d0 = 0.0, d1 = 0.0;
-    const int kr = lane & 3, col = lane >> 2;
-    if (nt8 * 8 < nw) {
-#pragma unroll 8
-      for (int k0 = kh * (kD / 2); k0 < (kh + 1) * (kD / 2); k0 += 4) {
-        const double av = qs[(k0 + kr) * kFQs + col];
-        const double bv = (double)ws[(k0 + kr) * kFWs + nt8 * 8 + col];
-        dmma_8x8x4(d0, d1, av, bv);
-      }
-    }
-    // append: the newest key's bits on my tables, fp32 t-ascending FMA chain
-    // (the SIMT prefill's / chained prologue's order)
-    bool bit = false;
-    if (app && tid < nw) {
-      float x = 0.f;
-#pragma unroll 16
-      for (int t = 0; t < kD; ++t) x = fmaf(ws[t * kFWs + tid], s_ks[t], x);
-      bit = x >= 0.f;                                                  // sign(0) = +1 (R-3)
-    }
-    __syncthreads();                                   // qs dead: partials go there
-    double* xp = qs;                                   // [kh][h 8][w 64]
-    if (nt8 * 8 < nw) {
-      xp[(kh * 8 + col) * 64 + nt8 * 8 + 2 * (lane & 3)] = d0;
-      xp[(kh * 8 + col) * 64 + nt8 * 8 + 2 * (lane & 3) + 1] = d1;
-    }
-    if (app && tid < 64) s_bits[tid] = bit ? 1u : 0u;
     __syncthreads();
-    const float inv_sqrt_d = 0.08838834764831845f;
-    for (int e = tid; e < NH * 64; e += kFThreads) {
-      const int h = e >> 6, w = e & 63;
-      if (w < nw) {
-        const double x = xp[h * 64 + w] + xp[(8 + h) * 64 + w];
-        const int tl = w / P, bi = w - tl * P;
-        float fp, fm;
-        if (a.hard) {
-          fp = x >= 0.0 ? 1.f : 0.f;
-          fm = 1.f - fp;
-        } else {
-          const float uu = tanhf((float)x) * inv_sqrt_d;            // Alg. 2 l.217
-          const float av = 2.0f * uu / a.tau;
-          fp = 1.0f / (1.0f + expf(-av));
-          fm = 1.0f / (1.0f + expf(av));
+    FU_STAMP(1);
+    // x[h][w] = q_h . W_w in fp64 on the tensor cores: warp w owns W rows
+    // 8 (w & 7) .. + 7 over the K half w >> 3; x = (K half 0) + (K half 1) -- the
+    // same decomposition as the chained prologue's tables tiles, so the LUTs agree
+    // bit for bit
+    {
+      const int nt8 = warp & 7, kh = warp >> 3;
+      double d0 = 0.0, d1 = 0.0;
+      const int kr = lane & 3, col = lane >> 2;
+      if (nt8 * 8 < nw) {
+#pragma unroll 8
+        for (int k0 = kh * (kD / 2); k0 < (kh + 1) * (kD / 2); k0 += 4) {
+          const double av = qs[(k0 + kr) * kFQs + col];
+          const double bv = (double)ws[(k0 + kr) * kFWs + nt8 * 8 + col];
+          dmma_8x8x4(d0, d1, av, bv);
         }
-        s_loc[h][bi][1][tl] = fp;
-        s_loc[h][bi][0][tl] = fm;
       }
-    }
-  }
-  if (app && tid < a.tpc && l0 + tid < LP) {   // code byte of my table tid (padding tables write 0)
-    const int l = l0 + tid;
-    uint32_t code = 0;
-    if (l < L)
-      for (int i = 0; i < P; ++i) code |= s_bits[tid * P + i] << i;   // row i -> bit i (R-4)
-    const int j = n - 1;
-    const int M = (LP < 32 ? LP : 32) - 1;
-    const int s = (l & ~M) | ((l - j) & M);
-    a.codes[((size_t)b * a.H_kv + g) * a.N_max * LP + code_off(j, s, LP)] = (uint8_t)code;
-  }
-  if (app && c == 0 && warp == 15) {   // ||v_j|| of the newest key (vnorm_kernel's order)
-    const uint2 u = a.v_new ? *reinterpret_cast<const uint2*>(a.v_new + ((size_t)b * a.H_kv + g) * kD + lane * 4)
-                            : *reinterpret_cast<const uint2*>(a.V + (((size_t)b * a.H_kv + g) * a.N_max + n - 1) * kD + lane * 4);
-    float va = bf16lo(u.x), vb = bf16hi(u.x), vc = bf16lo(u.y), vd = bf16hi(u.y);
-    float sq = fmaf(va, va, fmaf(vb, vb, fmaf(vc, vc, vd * vd)));
+      __syncthreads();                                   // qs dead: partials go there
+      double* xp = qs;                                   // [kh][h 8][w 64]
+      if (nt8 * 8 < nw) {
+        xp[(kh * 8 + col) * 64 + nt8 * 8 + 2 * (lane & 3)] = d0;
+        xp[(kh * 8 + col) * 64 + nt8 * 8 + 2 * (lane & 3) + 1] = d1;
+      }
+      __syncthreads();
+      const float inv_sqrt_d = 0.08838834764831845f;
+      if (kh == 0 && nt8 * 8 < nw) {
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    if (lane == 0) a.vnorm[((size_t)b * a.H_kv + g) * a.N_max + n - 1] = sqrtf(sq);
-  }
-  __syncthreads();
-  // push my factors into every CTA's s_fx[h][bit][s][l0 .. l0 + tpc)
-  {
-    const int ntl = max(0, min(a.tpc, L - l0));
-    if (ntl == 4) {
-      for (int e = tid; e < NH * P * 2 * CS; e += kFThreads) {
-        const int r = e % CS, hs = e / CS, sgn = hs & 1, hb = hs >> 1, bi = hb % P, h = hb / P;
-        const float4 v = make_float4(s_loc[h][bi][sgn][0], s_loc[h][bi][sgn][1], s_loc[h][bi][sgn][2],
-                                     s_loc[h][bi][sgn][3]);
-        *reinterpret_cast<float4*>(cluster.map_shared_rank(s_fx, r) + ((h * 8 + bi) * 2 + sgn) * LP + l0) = v;
-      }
-    } else if (ntl > 0) {
-      for (int e = tid; e < NH * P * 2 * ntl * CS; e += kFThreads) {
-        const int r = e % CS, rest = e / CS, tl = rest % ntl, hs = rest / ntl, sgn = hs & 1, hb = hs >> 1,
-                  bi = hb % P, h = hb / P;
-        cluster.map_shared_rank(s_fx, r)[((h * 8 + bi) * 2 + sgn) * LP + l0 + tl] = s_loc[h][bi][sgn][tl];
+        for (int i = 0; i < 2; ++i) {
+          const int h = lane >> 2, w = nt8 * 8 + 2 * (lane & 3) + i;
+          if (h < NH && w < nw) {
+            const double x = xp[h * 64 + w] + xp[(8 + h) * 64 + w];
+            const int tl = w / P, bit = w - tl * P;
+            float fp, fm;
+            if (a.hard) {
+              fp = x >= 0.0 ? 1.f : 0.f;
+              fm = 1.f - fp;
+            } else {
+              const float uu = tanhf((float)x) * inv_sqrt_d;            // Alg. 2 l.217
+              const float av = 2.0f * uu / a.tau;
+              fp = 1.0f / (1.0f + expf(-av));
+              fm = 1.0f / (1.0f + expf(av));
+            }
+            s_fx[((h * 8 + bit) * 2 + 1) * 16 + tl] = fp;
+            s_fx[((h * 8 + bit) * 2 + 0) * 16 + tl] = fm;
+          }
+        }
       }
     }
-  }
-  __threadfence();   // the appended code / norm before the cluster barrier (release)
-  FU_STAMP(2);
-  cluster.sync();
-  FU_STAMP(3);
-
-  // ===== A2. the whole LUT from the factors (every CTA) =============================
-  {
-    const int R = 1 << P;
-    const int GT = a.gt;
-    for (int gl0 = 0; gl0 < LP; gl0 += GT) {
-      // half tables: one (head, table, half) per thread, ((f0 f1) f2) f3 in fp64
-      for (int e = tid; e < NH * GT * 2; e += kFThreads) {
-        const int hi = e & 1, tl = (e >> 1) % GT, h = (e >> 1) / GT;
-        const int l = gl0 + tl;
+    // append: the newest key's bits on my tables, fp32 t-ascending (SIMT prefill order)
+    if (app && tid < 64) {
+      bool bit = false;
+      if (tid < nw) {
+        float x = 0.f;
+        for (int t = 0; t < kD; ++t) x = fmaf(ws[t * kFWs + tid], s_ks[t], x);
+        bit = x >= 0.f;                                                  // sign(0) = +1 (R-3)
+      }
+      s_bits[tid] = bit ? 1u : 0u;
+    }
+    __syncthreads();
+    // half tables (fp64 products, rounded once): one (h, table, half) per thread
+    if (tid < NH * 16 * 2) {
+      const int hi = tid & 1, tl = (tid >> 1) & 15, h = tid >> 5;
+      if (tl < ntab) {
         double f[4][2];
 #pragma unroll
         for (int bit = 0; bit < 4; ++bit) {
           const int ib = hi * 4 + bit;
-          const bool ok = ib < P && l < L;
-          f[bit][0] = ok ? (double)s_fx[((h * 8 + ib) * 2 + 0) * LP + l] : 1.0;
-          f[bit][1] = ok ? (double)s_fx[((h * 8 + ib) * 2 + 1) * LP + l] : 1.0;
+          const bool ok = ib < P && (l0 + tl) < L;
+          f[bit][0] = ok ? (double)s_fx[((h * 8 + ib) * 2 + 0) * 16 + tl] : 1.0;
+          f[bit][1] = ok ? (double)s_fx[((h * 8 + ib) * 2 + 1) * 16 + tl] : 1.0;
         }
         double p01[4], p012[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) p01[q] = f[0][q & 1] * f[1][q >> 1];
+        for (int e = 0; e < 4; ++e) p01[e] = f[0][e & 1] * f[1][e >> 1];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) p012[q] = p01[q & 3] * f[2][q >> 2];
+        for (int e = 0; e < 8; ++e) p012[e] = p01[e & 3] * f[2][e >> 2];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) s_half[((h * 2 + hi) * 16 + q) * GT + tl] = (float)(p012[q & 7] * f[3][q >> 3]);
+        for (int e = 0; e < 16; ++e) s_half[((h * 2 + hi) * 16 + e) * 16 + tl] = (float)(p012[e & 7] * f[3][e >> 3]);
       }
-      __syncthreads();
-      // LUT entries T(rr) = sum_h lo_h(rr & 15) hi_h(rr >> 4), 4 tables per task
-      // (one float4 per head and half; GT is a multiple of 4 or LP < 4)
-      const int ng = (GT + 3) >> 2;
+    }
+    if (app && tid < ntab) {   // code byte of my table tid (padding tables write 0)
+      const int l = l0 + tid;
+      uint32_t code = 0;
+      if (l < L)
+        for (int i = 0; i < P; ++i) code |= s_bits[tid * P + i] << i;   // row i -> bit i (R-4)
+      const int j = n - 1;
+      const int M = (LP < 32 ? LP : 32) - 1;
+      const int s = (l & ~M) | ((l - j) & M);
+      a.codes[((size_t)b * a.H_kv + g) * a.N_max * LP + code_off(j, s, LP)] = (uint8_t)code;
+    }
+    if (app && c == 0 && warp == 0) {   // ||v_j|| of the newest key (vnorm_kernel's order)
+      const uint2 u = a.v_new ? *reinterpret_cast<const uint2*>(a.v_new + ((size_t)b * a.H_kv + g) * kD + lane * 4)
+                              : *reinterpret_cast<const uint2*>(a.V + (((size_t)b * a.H_kv + g) * a.N_max + n - 1) * kD + lane * 4);
+      float va = bf16lo(u.x), vb = bf16hi(u.x), vc = bf16lo(u.y), vd = bf16hi(u.y);
+      float sq = fmaf(va, va, fmaf(vb, vb, fmaf(vc, vc, vd * vd)));
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      if (lane == 0) a.vnorm[((size_t)b * a.H_kv + g) * a.N_max + n - 1] = sqrtf(sq);
+    }
+    __syncthreads();
+    FU_STAMP(2);
+    // LUT columns of my tables -> every CTA of the cluster.  Column of table l:
+    // l (LP >= 32), or l, l + LP, ... < 32 (LP < 32, replicated)
+    const int R = 1 << P;
+    if (LP >= 32 && (a.tpc & 3) == 0) {
+      // task = (LUT row rr, 4-table group): one float4 per destination CTA
+      const int ng = a.tpc >> 2;
       for (int e = tid; e < 256 * ng; e += kFThreads) {
-        const int q4 = e % ng, rr = e / ng;
-        const int tl = q4 * 4, l = gl0 + tl;
+        const int gq = e % ng, rr = e / ng;
+        const int tl = gq * 4, l = l0 + tl;
+        if (l >= LP) continue;
         float4 T = make_float4(0.f, 0.f, 0.f, 0.f);
         if (rr < R) {
-          if (GT >= 4) {
 #pragma unroll
-            for (int h = 0; h < NH; ++h) {
-              const float4 lo = *reinterpret_cast<const float4*>(s_half + ((h * 2 + 0) * 16 + (rr & 15)) * GT + tl);
-              const float4 hv = *reinterpret_cast<const float4*>(s_half + ((h * 2 + 1) * 16 + (rr >> 4)) * GT + tl);
-              T.x = fmaf(lo.x, hv.x, T.x);
-              T.y = fmaf(lo.y, hv.y, T.y);
-              T.z = fmaf(lo.z, hv.z, T.z);
-              T.w = fmaf(lo.w, hv.w, T.w);
-            }
-          } else {
-            float* tp = &T.x;
-            for (int u = 0; u < GT; ++u)
-#pragma unroll
-              for (int h = 0; h < NH; ++h)
-                tp[u] = fmaf(s_half[((h * 2 + 0) * 16 + (rr & 15)) * GT + u],
-                             s_half[((h * 2 + 1) * 16 + (rr >> 4)) * GT + u], tp[u]);
+          for (int h = 0; h < NH; ++h) {
+            const float4 lo = *reinterpret_cast<const float4*>(s_half + ((h * 2 + 0) * 16 + (rr & 15)) * 16 + tl);
+            const float4 hv = *reinterpret_cast<const float4*>(s_half + ((h * 2 + 1) * 16 + (rr >> 4)) * 16 + tl);
+            T.x = fmaf(lo.x, hv.x, T.x);
+            T.y = fmaf(lo.y, hv.y, T.y);
+            T.z = fmaf(lo.z, hv.z, T.z);
+            T.w = fmaf(lo.w, hv.w, T.w);
           }
+          if (l + 0 >= L) T.x = 0.f;
+          if (l + 1 >= L) T.y = 0.f;
+          if (l + 2 >= L) T.z = 0.f;
+          if (l + 3 >= L) T.w = 0.f;
         }
-        const float tv[4] = {T.x, T.y, T.z, T.w};
+        for (int r = 0; r < CS; ++r)
+          *reinterpret_cast<float4*>(cluster.map_shared_rank(lut, r) + rr * 64 + l) = T;
+      }
+    } else {
+      for (int e = tid; e < 256 * 16; e += kFThreads) {
+        const int tl = e & 15, rr = e >> 4;
+        if (tl >= ntab) continue;
+        const int l = l0 + tl;
+        float T = 0.f;
+        if (l < L && rr < R) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (tl + u >= GT) continue;
-          const float v = (l + u < L) ? tv[u] : 0.f;
-          if (LP >= 32) lut[rr * 64 + l + u] = v;
-          else for (int cc = l + u; cc < 32; cc += LP) lut[rr * 64 + cc] = v;   // column c: table c mod LP
+          for (int h = 0; h < NH; ++h) T = fmaf(s_half[((h * 2 + 0) * 16 + (rr & 15)) * 16 + tl], s_half[((h * 2 + 1) * 16 + (rr >> 4)) * 16 + tl], T);
+        }
+        for (int r = 0; r < CS; ++r) {
+          float* rl = cluster.map_shared_rank(lut, r);
+          if (LP >= 32) rl[rr * 64 + l] = T;
+          else for (int cc = l; cc < 32; cc += LP) rl[rr * 64 + cc] = T;
         }
       }
-      __syncthreads();
     }
+    __threadfence();   // the appended code / norm before the cluster barrier (release)
   }
+  FU_STAMP(3);
+  cluster.sync();
   FU_STAMP(4);
 
-  // ===== B. scores of my slice (codes + norms straight into registers) ===============
+  // ===== B. scores of my slice ======================================================
   const int base = c * a.S;
   int len = n - base;
   len = len < 0 ? 0 : (len > a.S ? a.S : len);
   uint32_t nvalid = 0, nforced = 0, kmin = 0xFFFFFFFFu, kmax = 0u;
   {
+    using TSt = TileStage<LP>;
+    const uint32_t ring = smem_u32(fsm + kFLutBytes) + (uint32_t)warp * (kFScoreStages * TSt::BYTES);
+    const char* ringp = fsm + kFLutBytes + warp * (kFScoreStages * TSt::BYTES);
     uint32_t pk[16];
 #pragma unroll
     for (int m = 0; m < 16; ++m)
       pk[m] = (uint32_t)(((2 * m + lane) & 31) << 2) | ((uint32_t)(((2 * m + 1 + lane) & 31) << 2) << 8);
-    const uint64_t pol_code = l2_policy_evict_first();
     const uint8_t* crow = a.codes + ((size_t)b * a.H_kv + g) * a.N_max * LP;
     const float* vrow = a.vnorm + ((size_t)b * a.H_kv + g) * a.N_max;
     const uint8_t* mrow = a.mask ? a.mask + (size_t)b * a.N_max : nullptr;
     float* srow = a.scores + (size_t)row * a.N_max;
     const int tiles = a.S >> 5;
     const int vt = (len + 31) >> 5;                    // tiles holding valid keys
+    const int my = warp < vt ? (vt - warp + kFWarps - 1) / kFWarps : 0;
     const int t0 = base >> 5;
-    auto score_tile = [&](const FTile<LP>& tt, int li_tile) {
+    if (my > 0) issue_tile<LP>(ring, crow + (size_t)(t0 + warp) * 32 * LP, vrow + (t0 + warp) * 32, lane);
+    cpa_commit();
+    for (int i = 0; i < my; ++i) {
+      if (i + 1 < my) {
+        const int ti = t0 + warp + (i + 1) * kFWarps;
+        issue_tile<LP>(ring + ((i + 1) & 1) * TSt::BYTES, crow + (size_t)ti * 32 * LP, vrow + ti * 32, lane);
+      }
+      cpa_commit();
+      cpa_wait<1>();
+      const char* st = ringp + (i & 1) * TSt::BYTES;
+      uint32_t w[LP / 4];
+#pragma unroll
+      for (int ch = 0; ch < TSt::NCH; ++ch) {
+        if constexpr (TSt::CB == 16) {
+          const uint4 v = *reinterpret_cast<const uint4*>(st + ch * 512 + lane * 16);
+          w[ch * 4 + 0] = v.x; w[ch * 4 + 1] = v.y; w[ch * 4 + 2] = v.z; w[ch * 4 + 3] = v.w;
+        } else {
+          const uint2 v = *reinterpret_cast<const uint2*>(st + ch * 256 + lane * 8);
+          w[ch * 2 + 0] = v.x; w[ch * 2 + 1] = v.y;
+        }
+      }
+      const float vn = *reinterpret_cast<const float*>(st + TSt::CODE_BYTES + lane * 4);
       uint64_t acc = 0ull;
 #pragma unroll
       for (int s2 = 0; s2 < LP; s2 += 2) {
@@ -384,14 +357,14 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
         for (int u = 0; u < 2; ++u) {
           const int ss = s2 + u, sl = ss & 31;
           const uint32_t sel = (uint32_t)(4 + (sl & 1)) | ((uint32_t)(ss & 3) << 4) | 0x7600u;
-          const uint32_t addr = __byte_perm(tt.w[ss >> 2], pk[sl >> 1], sel);
+          const uint32_t addr = __byte_perm(w[ss >> 2], pk[sl >> 1], sel);
           v[u] = *reinterpret_cast<const float*>(fsm + ((ss & 32) ? 128 : 0) + addr);
         }
         const uint64_t pv = (uint64_t)__float_as_uint(v[0]) | ((uint64_t)__float_as_uint(v[1]) << 32);
         asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(pv));
       }
-      const float score = tt.vn * (__uint_as_float((uint32_t)acc) + __uint_as_float((uint32_t)(acc >> 32)));
-      const int li = li_tile * 32 + lane;                // slice-local index
+      const float score = vn * (__uint_as_float((uint32_t)acc) + __uint_as_float((uint32_t)(acc >> 32)));
+      const int li = (warp + i * kFWarps) * 32 + lane;   // slice-local index
       const int j = base + li;
       const bool ok = li < len && (!mrow || mrow[j]);
       srow[j] = ok ? score : -INFINITY;
@@ -401,37 +374,22 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
       nvalid += key != 0u;
       nforced += key == 0xFFFFFFFFu;
       if (key != 0u && key != 0xFFFFFFFFu) { kmin = min(kmin, key); kmax = max(kmax, key); }
-    };
-    // four tiles per warp in registers: the next two load while the current two
-    // are looked up
-    FTile<LP> x0, x1, y0, y1;
-    int ti = warp;
-    if (ti < vt) f_load_tile<LP>(x0, crow + (size_t)(t0 + ti) * 32 * LP, vrow + (t0 + ti) * 32, lane, pol_code);
-    if (ti + kFWarps < vt)
-      f_load_tile<LP>(x1, crow + (size_t)(t0 + ti + kFWarps) * 32 * LP, vrow + (t0 + ti + kFWarps) * 32, lane, pol_code);
-    for (; ti < vt; ti += 2 * kFWarps) {
-      if (ti + 2 * kFWarps < vt)
-        f_load_tile<LP>(y0, crow + (size_t)(t0 + ti + 2 * kFWarps) * 32 * LP, vrow + (t0 + ti + 2 * kFWarps) * 32, lane, pol_code);
-      if (ti + 3 * kFWarps < vt)
-        f_load_tile<LP>(y1, crow + (size_t)(t0 + ti + 3 * kFWarps) * 32 * LP, vrow + (t0 + ti + 3 * kFWarps) * 32, lane, pol_code);
-      score_tile(x0, ti);
-      if (ti + kFWarps < vt) score_tile(x1, ti + kFWarps);
-      x0 = y0;
-      x1 = y1;
     }
+    cpa_wait<0>();
     // tiles past seq_len: -inf scores, invalid keys
-    for (int tz = vt + warp; tz < tiles; tz += kFWarps) {
-      const int li = tz * 32 + lane;
+    for (int ti = vt + warp; ti < tiles; ti += kFWarps) {
+      const int li = ti * 32 + lane;
       srow[base + li] = -INFINITY;
       keys[li] = 0u;
     }
   }
-  __syncthreads();   // keys complete; the LUT is dead (zone A becomes the top-k state)
+  __syncthreads();
 
   FU_STAMP(5);
   // ===== C. exact top-k over the cluster =============================================
   TopkArgs ta = {};
   ta.op = 0;
+  ta.index_base = 0;
   ta.scores = a.scores;
   ta.seq_lens = a.seq_lens;
   ta.rows = (int)gridDim.y;
@@ -440,22 +398,21 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
   ta.k = a.k;
   ta.sink = a.sink;
   ta.window = a.window;
-  ta.index_base = 0;
   ta.per = a.S;
   ta.idx = a.idx;
   ta.cnt = a.cnt;
   ta.sel_scores = nullptr;
-  TopkShared& TS = *reinterpret_cast<TopkShared*>(fsm);
+  int32_t* sel = reinterpret_cast<int32_t*>(fsm);   // LUT region (dead)
   int sel_lo = 0, sel_cnt = 0;
-  // sel_local = nullptr: this CTA's rows are read back from its own share of idx
-  topk_core(ta, keys, TS, row, n, base, len, nvalid, nforced, kmin, kmax, nullptr, &sel_lo, &sel_cnt);
-  // (topk_core ends with a cluster barrier: the idx writes are visible, zones A/B are dead)
-  const int32_t* list = a.idx + (size_t)row * a.k + sel_lo;
+  topk_core(ta, keys, TS, row, n, base, len, nvalid, nforced, kmin, kmax, sel, &sel_lo, &sel_cnt);
+  __syncthreads();
+  int32_t* list = reinterpret_cast<int32_t*>(keys);  // keys are dead: move the list out of the ring zone
+  for (int i = tid; i < sel_cnt; i += kFThreads) list[i] = sel[i];
+  __syncthreads();
 
   FU_STAMP(6);
   // ===== D. attention over my selected rows + cluster LSE merge =====================
   {
-    const int att_warps = min(kFWarps, a.smem / (2 * kTileBytes));   // 2 ring stages each
     const int gid = lane >> 2, tig = lane & 3;
     const int h0 = g * NH;
     uint32_t qb[8][2];
@@ -475,8 +432,8 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
     const uint16_t* Kb = a.K + ((size_t)b * a.H_kv + g) * a.N_max * kD;
     const uint16_t* Vb = a.V + ((size_t)b * a.H_kv + g) * a.N_max * kD;
     const int ntiles = (sel_cnt + kTileRows - 1) / kTileRows;
-    if (warp < att_warps) {
-      const uint32_t ring0 = smem_u32(fsm) + (uint32_t)warp * (2 * kTileBytes);
+    if (warp < kFAttWarps) {
+      const uint32_t ring0 = smem_u32(fsm) + (uint32_t)warp * (kFAttStages * kTileBytes);
       auto issue = [&](int t, int stage) {
         const int row0 = t * kTileRows;
         const uint32_t kbuf = ring0 + stage * kTileBytes, vbuf = kbuf + kTileRows * 256;
@@ -485,18 +442,18 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
           const int cc = (it * 32 + lane) & 15, rr = (it * 32 + lane) >> 4;
           const int i = row0 + rr;
           const bool v = i < sel_cnt;
-          const int tok = v ? list[i] : 0;   // written by this CTA's top-k: a coherent load
+          const int tok = v ? list[i] : 0;
           cp16(kbuf + swz(rr, cc), Kb + (size_t)tok * kD + cc * 8, v);
           cp16(vbuf + swz(rr, cc), Vb + (size_t)tok * kD + cc * 8, v);
         }
       };
       int my = 0;
-      for (int t = warp; t < ntiles; t += att_warps) ++my;
+      for (int t = warp; t < ntiles; t += kFAttWarps) ++my;
       if (my > 0) issue(warp, 0);
       cp_commit();
       for (int jt = 0; jt < my; ++jt) {
-        const int t = warp + jt * att_warps;
-        if (jt + 1 < my) issue(warp + (jt + 1) * att_warps, (jt + 1) & 1);
+        const int t = warp + jt * kFAttWarps;
+        if (jt + 1 < my) issue(warp + (jt + 1) * kFAttWarps, (jt + 1) & 1);
         cp_commit();
         cp_wait<1>();
         __syncwarp();
@@ -561,9 +518,9 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
     __syncthreads();
     // merge the attention warps' states (ring region reused)
     float* sm_o = reinterpret_cast<float*>(fsm);                    // [warps][8][128]
-    float* sm_m = sm_o + kFWarps * 8 * kD;
-    float* sm_l = sm_m + kFWarps * 8;
-    if (warp < att_warps) {
+    float* sm_m = sm_o + kFAttWarps * 8 * kD;
+    float* sm_l = sm_m + kFAttWarps * 8;
+    if (warp < kFAttWarps) {
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
         const int d0 = mt * 16 + gid;
@@ -581,10 +538,12 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
     for (int x = tid; x < NH * kD; x += kFThreads) {
       const int h = x / kD, e = x % kD;
       float M = -INFINITY;
-      for (int w = 0; w < att_warps; ++w) M = fmaxf(M, sm_m[w * 8 + h]);
+#pragma unroll
+      for (int w = 0; w < kFAttWarps; ++w) M = fmaxf(M, sm_m[w * 8 + h]);
       float Ls = 0.f, O = 0.f;
       if (M != -INFINITY) {
-        for (int w = 0; w < att_warps; ++w) {
+#pragma unroll
+        for (int w = 0; w < kFAttWarps; ++w) {
           const float wt = exp2f(sm_m[w * 8 + h] - M);
           Ls = fmaf(wt, sm_l[w * 8 + h], Ls);
           O = fmaf(wt, sm_o[(w * 8 + h) * kD + e], O);
@@ -595,30 +554,18 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
     }
     cluster.sync();
     // cluster LSE merge: CTA c merges heads h = c, c + CS, ... over the CS partials
-    // (all ranks' loads in flight at once)
     constexpr float kLn2 = 0.6931471805599453f;
     for (int h = c; h < NH; h += CS) {
       for (int e = tid; e < kD + 1; e += kFThreads) {
-        float pm[kMaxCluster], pl[kMaxCluster], po[kMaxCluster];
-#pragma unroll
-        for (int r = 0; r < kMaxCluster; ++r) {
-          const float* pr = cluster.map_shared_rank(&s_part[0][0], r < CS ? r : 0) + h * (kD + 2);
-          pm[r] = pr[0];
-          pl[r] = pr[1];
-          po[r] = e < kD ? pr[2 + e] : 0.f;
-        }
         float M = -INFINITY;
-#pragma unroll
-        for (int r = 0; r < kMaxCluster; ++r) M = r < CS ? fmaxf(M, pm[r]) : M;
+        for (int r = 0; r < CS; ++r) M = fmaxf(M, cluster.map_shared_rank(&s_part[0][0], r)[h * (kD + 2)]);
         float Ls = 0.f, O = 0.f;
         if (M != -INFINITY) {
-#pragma unroll
-          for (int r = 0; r < kMaxCluster; ++r) {
-            if (r < CS) {
-              const float wt = exp2f(pm[r] - M);
-              Ls = fmaf(wt, pl[r], Ls);
-              O = fmaf(wt, po[r], O);
-            }
+          for (int r = 0; r < CS; ++r) {
+            const float* pr = cluster.map_shared_rank(&s_part[0][0], r) + h * (kD + 2);
+            const float wt = exp2f(pr[0] - M);
+            Ls = fmaf(wt, pr[1], Ls);
+            if (e < kD) O = fmaf(wt, pr[2 + e], O);
           }
         }
         const size_t oh = (size_t)b * a.H_q + h0 + h;
@@ -631,82 +578,24 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
   FU_STAMP(7);
 }
 
-// ---- host: geometry -------------------------------------------------------------
-template <int NH, int LP>
-static void* fused_fn() { return reinterpret_cast<void*>(fused_step_kernel<NH, LP>); }
-
-static void* fused_kernel_ptr(int NH, int Lp) {
-#define SK_FPTR(N, LPV) \
-  if (NH == N && Lp == LPV) return fused_fn<N, LPV>();
-  SK_FPTR(1, 8) SK_FPTR(1, 16) SK_FPTR(1, 32) SK_FPTR(1, 64)
-  SK_FPTR(2, 8) SK_FPTR(2, 16) SK_FPTR(2, 32) SK_FPTR(2, 64)
-  SK_FPTR(4, 8) SK_FPTR(4, 16) SK_FPTR(4, 32) SK_FPTR(4, 64)
-  SK_FPTR(8, 8) SK_FPTR(8, 16) SK_FPTR(8, 32) SK_FPTR(8, 64)
-#undef SK_FPTR
-  return nullptr;
-}
-
-// one CTA per SM anyway: the rest of the shared memory deepens the attention ring
-// (13 warps x 2 stages x 8 KB)
-constexpr size_t kFRingBytes = 13 * 2 * kTileBytes;
-static size_t fused_smem(int NH, int Lp, int S) {
-  const size_t z = (size_t)kFZoneA + fused_zone_b(NH, Lp, S);
-  return z > kFRingBytes ? z : kFRingBytes;
-}
-
-// co-resident clusters of CS CTAs of this kernel instance (queried once per
-// device / shape): the whole grid must be one wave, since the CTAs of a cluster
-// synchronize with each other
-static int max_active_clusters(void* fn, int CS, size_t smem) {
-  static std::mutex mu;
-  static std::map<std::tuple<int, void*, int, size_t>, int> cache;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const auto key = std::make_tuple(dev, fn, CS, smem);
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  int n = 0;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
-      (CS <= 8 || cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CS, 1, 1);
-    cfg.blockDim = dim3(kFThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CS;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) n = 0;
-  }
-  cudaGetLastError();
-  cache[key] = n;
-  return n;
-}
-
-// Pick the cluster size: 16 CTAs per row when all the rows' clusters are
-// co-resident (one wave), else 8; false when the one-launch path does not apply.
+// Host: pick the cluster size and check that the whole grid is co-resident
+// (one wave); returns false when the fused path does not apply.
 static bool fused_geometry(const socket_cfg& c, int& CS, int& S) {
-  if (c.group_mode != SOCKET_GROUP_KV_SHARED || c.P > 8 || c.index_base != 0) return false;
+  if (c.group_mode != SOCKET_GROUP_KV_SHARED || c.P > 8) return false;
   const int Lp = code_slots(c.L);
   if (Lp > 64) return false;
   const int NH = c.H_q / c.H_kv;
-  void* fn = fused_kernel_ptr(NH, Lp);
-  if (!fn) return false;
+  if (NH != 1 && NH != 2 && NH != 4 && NH != 8) return false;
   const int rows = c.B * c.H_kv;
-  // measured (bench batch1 rows, tools/fused_check.py): one launch wins while the
-  // rows fit one wave of clusters; beyond 8 rows the multi-kernel path spreads
-  // each stage over all SMs
+  // measured (tools/fused_check.py): one launch wins while the grid is at most
+  // 8 clusters of 8 (B = 1 at 8 KV heads: 39 vs 48 us at 32K); beyond that the
+  // multi-kernel path spreads each stage over all 148 SMs and is faster
   if (rows > 8) return false;
-  for (int cs : {16, 8}) {
+  for (int cs : {8, 4}) {   // clusters of 16 do not all fit one wave
     if (c.N_max % (cs * 128) != 0) continue;
     const int s = c.N_max / cs;
-    if (s > kFMaxSlice) continue;
-    if ((Lp + cs - 1) / cs * c.P > 64) continue;   // <= 64 W rows per CTA (staging, 16 DMMA warps)
-    if (rows > max_active_clusters(fn, cs, fused_smem(NH, Lp, s))) continue;
+    if (s > 16384 || rows * cs > num_sms()) continue;   // keys of a slice: <= 64 KB
+    if ((Lp + cs - 1) / cs * c.P > 64) continue;   // <= 64 W rows per CTA (staging, 8 DMMA warps)
     CS = cs;
     S = s;
     return true;
@@ -729,7 +618,6 @@ socket_status launch_fused_step(const socket_cfg& c, const void* q, void* K, voi
   int CS, S;
   if (!fused_geometry(c, CS, S)) return fail(SOCKET_EUNSUPPORTED, "fused step: shape not supported");
   const int Lp = code_slots(c.L);
-  const int NH = c.H_q / c.H_kv;
   FusedArgs a;
   a.q = (const uint16_t*)q;
   a.K = (uint16_t*)K;
@@ -751,6 +639,7 @@ socket_status launch_fused_step(const socket_cfg& c, const void* q, void* K, voi
   a.N_max = c.N_max;
   a.L = c.L;
   a.P = c.P;
+  a.Lp = Lp;
   a.k = k;
   a.sink = sink;
   a.window = window;
@@ -760,14 +649,7 @@ socket_status launch_fused_step(const socket_cfg& c, const void* q, void* K, voi
   a.scale_log2 = c.sm_scale * kLog2eM;
   a.S = S;
   a.tpc = (Lp + CS - 1) / CS;
-  a.gt = fused_gt(NH, Lp);
-  a.zoneB = (int)fused_zone_b(NH, Lp, S);
-  const size_t sm = fused_smem(NH, Lp, S);
-  a.smem = (int)sm;
-  void* fn = fused_kernel_ptr(NH, Lp);
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
-    return fail(SOCKET_ECUDA, "fused step: shared memory request rejected");
-  if (CS > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  const size_t sm = fused_smem_bytes(S);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CS, c.B * c.H_kv, 1);
   cfg.blockDim = dim3(kFThreads, 1, 1);
@@ -780,8 +662,22 @@ socket_status launch_fused_step(const socket_cfg& c, const void* q, void* K, voi
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  void* args[] = {&a};
-  cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+  const int NH = c.H_q / c.H_kv;
+  cudaError_t e = cudaSuccess;
+#define SK_FUSED(N, LPV)                                                                          \
+  if (NH == N && Lp == LPV) {                                                                     \
+    auto kfn = fused_step_kernel<N, LPV>;                                                         \
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) \
+      return fail(SOCKET_ECUDA, "fused step: shared memory request rejected");                   \
+    if (CS > 8) cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);    \
+    e = cudaLaunchKernelEx(&cfg, kfn, a);                                                         \
+  } else
+  SK_FUSED(1, 8) SK_FUSED(1, 16) SK_FUSED(1, 32) SK_FUSED(1, 64)
+  SK_FUSED(2, 8) SK_FUSED(2, 16) SK_FUSED(2, 32) SK_FUSED(2, 64)
+  SK_FUSED(4, 8) SK_FUSED(4, 16) SK_FUSED(4, 32) SK_FUSED(4, 64)
+  SK_FUSED(8, 8) SK_FUSED(8, 16) SK_FUSED(8, 32) SK_FUSED(8, 64)
+  { return fail(SOCKET_EUNSUPPORTED, "fused step: heads / tables not instantiated"); }
+#undef SK_FUSED
   if (e != cudaSuccess) return fail(SOCKET_ECUDA, std::string("fused step launch: ") + cudaGetErrorString(e));
   return check_launch("fused_step_kernel");
 }

@@ -16,7 +16,7 @@ import torch  # noqa: E402
 
 from trace_topk import build_trace  # noqa: E402
 
-PH = ["stage q/W", "DMMA+sigma+append+push", "cluster sync", "LUT build", "score slice",
+PH = ["stage q/W", "DMMA+sigma+half+append", "LUT to cluster", "cluster sync", "score slice",
       "top-k", "attend + merge"]
 TK = ["stat_sync", "hist", "hist_sync", "ghist_scan", "cand", "cand_sync", "gather_select", "count",
       "emit", "tail", "final_sync"]
