@@ -594,7 +594,9 @@ static bool fused_geometry(const socket_cfg& c, int& CS, int& S) {
   for (int cs : {8, 4}) {   // clusters of 16 do not all fit one wave
     if (c.N_max % (cs * 128) != 0) continue;
     const int s = c.N_max / cs;
-    if (s > 16384 || rows * cs > num_sms()) continue;   // keys of a slice: <= 64 KB
+    // keys of a slice <= 32 KB: with the LUT + score ring (132 KB) and the static
+    // top-k state (34 KB) the CTA uses ~200 KB of shared memory
+    if (s > 8192 || rows * cs > num_sms()) continue;
     if ((Lp + cs - 1) / cs * c.P > 64) continue;   // <= 64 W rows per CTA (staging, 8 DMMA warps)
     CS = cs;
     S = s;
