@@ -140,14 +140,25 @@ enum {
  *      + ((j >> 5) * (Lp / CB) + s / CB) * (32 * CB) + (j & 31) * CB + (s % CB)
  * Rotating each key's slots by j mod 32 makes the 32 lanes of a warp (lane =
  * key j mod 32) look up 32 different tables at every step, i.e. 32 different
- * shared-memory banks.  socket_pack_codes /
- * socket_unpack_codes convert from / to the plain [B][H_kv][L][N_max] uint8
- * layout.
+ * shared-memory banks.
+ *
+ * Wide codes (P = 9..16, NEXT-2): the same slots and rotation with Lp =
+ * max(32, socket_code_slots(L)), tightly packed -- Lp * P bits per key (640
+ * bits for the 600 useful at L = 60, P = 10).  Per (b, h) region, 32-key tiles;
+ * per tile and 32-slot group g (G = Lp / 32), the group's 32 slot codes form
+ * one 32P-bit string, slot s at bits [s P, s P + P) LSB first, stored as P
+ * uint32 words interleaved across the tile's keys:
+ *   uint32 index of word w of group g of key j = (((j >> 5) * G + g) * P + w) * 32 + (j & 31)
+ * (in units of uint32 from the start of the (b, h) region, which is
+ * N_max * Lp * P / 8 bytes).
+ * socket_pack_codes / socket_unpack_codes convert from / to the plain
+ * [B][H_kv][L][N_max] layout (uint8 for P <= 8, uint16 for P > 8).
  * ------------------------------------------------------------------------ */
 
-/* Slots per key of the code layout (see above); 0 if L < 1. */
+/* Slots per key of the byte-code layout (see above); 0 if L < 1. */
 int32_t socket_code_slots(int32_t L);
-/* Bytes of the codes buffer for cfg: B*H_kv*N_max*socket_code_slots(L). */
+/* Bytes of the codes buffer for cfg: B*H_kv*N_max*socket_code_slots(L) for
+ * P <= 8, B*H_kv*N_max*Lp*P/8 (packed) for P > 8. */
 size_t socket_codes_bytes(const socket_cfg* cfg);
 
 /* Workspace requirement of an entry point (op = SOCKET_OP_*), for budget k. */

@@ -84,7 +84,7 @@ int32_t socket_code_slots(int32_t L) { return code_slots(L); }
 
 size_t socket_codes_bytes(const socket_cfg* c) {
   if (!c) return 0;
-  return (size_t)c->B * c->H_kv * c->N_max * code_slots(c->L) * code_elem_bytes(c->P);
+  return (size_t)c->B * c->H_kv * c->N_max * code_bytes_per_key(c->L, c->P);
 }
 
 size_t socket_workspace_bytes(const socket_cfg* c, int32_t op, int32_t k) {

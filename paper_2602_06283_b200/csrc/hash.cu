@@ -46,6 +46,27 @@ hash_keys_simt_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict
     cs[lane][l] = (CT)code;
   }
   __syncthreads();
+  if (P > 8) {
+    // packed wide codes: thread = (key, group, word) gathers the slots overlapping
+    // word w of the group's 32P-bit string (internal.cuh, packed_word)
+    const int G = Lp >> 5;
+    uint32_t* cw = reinterpret_cast<uint32_t*>(codes) + (size_t)bh * N_max * Lp * P / 32;
+    for (int i = threadIdx.x; i < 32 * G * P; i += kHashThreads) {
+      const int key = i & 31, gw = i >> 5, g = gw / P, w = gw % P;
+      const int j = j0 + key;
+      if (j < n_begin || j >= n_end) continue;
+      uint32_t word = 0;
+      const int s_lo = (32 * w) / P, s_hi = min(31, (32 * w + 31) / P);
+      for (int s = s_lo; s <= s_hi; ++s) {
+        const int t = g * 32 + ((s + j) & 31);
+        const uint32_t code = t < L ? (uint32_t)cs[key][t] : 0u;
+        const int bp = s * P - 32 * w;          // slot's first bit relative to the word
+        word |= bp >= 0 ? (code << bp) : (code >> -bp);
+      }
+      cw[packed_word(j, g, w, G, P)] = word;
+    }
+    return;
+  }
   // write: thread = (key, chunk); CB contiguous code elements per (key, chunk)
   const int CB = Lp < 16 ? Lp : 16;
   const int nch = Lp / CB;
@@ -64,7 +85,7 @@ hash_keys_simt_kernel(const uint16_t* __restrict__ K, const uint16_t* __restrict
       }
     }
     CT* dst = cb + code_off(j, ch * CB, Lp);
-    const int nbytes = CB * (int)sizeof(CT);   // 8, 16 or 32
+    const int nbytes = CB * (int)sizeof(CT);   // 8 or 16
     for (int o = 0; o < nbytes; o += 8)
       *reinterpret_cast<uint2*>(reinterpret_cast<char*>(dst) + o) =
           *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(buf) + o);
@@ -146,9 +167,53 @@ __global__ void pack_codes_kernel(const CT* __restrict__ plain, CT* __restrict__
   }
 }
 
+// plain [bh][L][N_max] int16 <-> packed wide layout (P > 8)
+//   pack:   one thread per (bh, j, group, word): the slots overlapping the word
+//   unpack: one thread per (bh, j, slot): the slot's P bits from one or two words
+__global__ void pack_wide_kernel(const uint16_t* __restrict__ plain, uint32_t* __restrict__ codes, int N_max,
+                                 int L, int Lp, int P, long long total) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int G = Lp >> 5;
+  const int w = (int)(i % P);
+  const long long r1 = i / P;
+  const int g = (int)(r1 % G);
+  const long long r2 = r1 / G;
+  const int j = (int)(r2 % N_max);
+  const long long bh = r2 / N_max;
+  uint32_t word = 0;
+  const int s_lo = (32 * w) / P, s_hi = min(31, (32 * w + 31) / P);
+  for (int s = s_lo; s <= s_hi; ++s) {
+    const int t = g * 32 + ((s + j) & 31);
+    const uint32_t code = t < L ? (uint32_t)plain[(bh * L + t) * N_max + j] : 0u;
+    const int bp = s * P - 32 * w;
+    word |= bp >= 0 ? (code << bp) : (code >> -bp);
+  }
+  codes[bh * (long long)N_max * Lp * P / 32 + packed_word(j, g, w, G, P)] = word;
+}
+
+__global__ void unpack_wide_kernel(uint16_t* __restrict__ plain, const uint32_t* __restrict__ codes, int N_max,
+                                   int L, int Lp, int P, long long total) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int G = Lp >> 5;
+  const int slot = (int)(i % Lp);
+  const long long r = i / Lp;
+  const int j = (int)(r % N_max);
+  const long long bh = r / N_max;
+  const int g = slot >> 5, s = slot & 31;
+  const int t = g * 32 + ((s + j) & 31);
+  if (t >= L) return;
+  const uint32_t* cw = codes + bh * (long long)N_max * Lp * P / 32;
+  const int bp = s * P, w = bp >> 5, sh = bp & 31;
+  uint64_t v = cw[packed_word(j, g, w, G, P)];
+  if (sh + P > 32) v |= (uint64_t)cw[packed_word(j, g, w + 1, G, P)] << 32;
+  plain[(bh * L + t) * N_max + j] = (uint16_t)((v >> sh) & ((1u << P) - 1u));
+}
+
 socket_status launch_hash_keys_simt(const socket_cfg& c, const void* K, const void* W,
                                     uint8_t* codes, int n_begin, int n_count, cudaStream_t st) {
-  const int Lp = code_slots(c.L);
+  const int Lp = code_slots_p(c.L, c.P);
   const int t0 = n_begin >> 5, t1 = (n_begin + n_count - 1) >> 5;
   dim3 grid(t1 - t0 + 1, c.B * c.H_kv);
   if (c.P > 8)
@@ -204,16 +269,24 @@ socket_status launch_hash_keys(const socket_cfg& c, const void* K, const void* V
 
 socket_status launch_pack_codes(const socket_cfg& c, const uint8_t* plain, uint8_t* codes,
                                 bool unpack, cudaStream_t st) {
-  const int Lp = code_slots(c.L);
+  const int Lp = code_slots_p(c.L, c.P);
   const long long total = (long long)c.B * c.H_kv * c.N_max * Lp;
   if (total == 0) return SOCKET_OK;
   const int threads = 256;
   const unsigned blocks = (unsigned)((total + threads - 1) / threads);
-  if (c.P > 8)
-    pack_codes_kernel<uint16_t><<<blocks, threads, 0, st>>>(
-        reinterpret_cast<const uint16_t*>(plain), reinterpret_cast<uint16_t*>(codes), c.N_max, c.L,
-        Lp, total, unpack);
-  else
+  if (c.P > 8) {
+    if (unpack) {
+      unpack_wide_kernel<<<blocks, threads, 0, st>>>(reinterpret_cast<uint16_t*>(const_cast<uint8_t*>(plain)),
+                                                     reinterpret_cast<const uint32_t*>(codes), c.N_max, c.L,
+                                                     Lp, c.P, total);
+    } else {
+      const long long words = (long long)c.B * c.H_kv * c.N_max * (Lp / 32) * c.P;
+      pack_wide_kernel<<<(unsigned)((words + threads - 1) / threads), threads, 0, st>>>(
+          reinterpret_cast<const uint16_t*>(plain), reinterpret_cast<uint32_t*>(codes), c.N_max, c.L, Lp,
+          c.P, words);
+    }
+    return check_launch("pack_wide_kernel");
+  } else
     pack_codes_kernel<uint8_t><<<blocks, threads, 0, st>>>(plain, codes, c.N_max, c.L, Lp, total,
                                                             unpack);
   return check_launch("pack_codes_kernel");

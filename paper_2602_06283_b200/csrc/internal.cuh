@@ -41,7 +41,17 @@ inline size_t lut_bytes_per_row(int L) {
 // P > 8 ("wide" codes, NEXT-2): one uint16 per (key, table); the score kernel's
 // LUT holds per query head the two factor half-tables A(lo), B(hi) of the
 // exact product form p(r) = A(r mod 2^Pl) B(r >> Pl), Pl = P / 2.
-inline int code_elem_bytes(int P) { return P > 8 ? 2 : 1; }
+// Code slots of the stored layout for (L, P): byte codes (P <= 8) use
+// code_slots(L); packed wide codes (P > 8) need whole 32-slot groups.
+inline int code_slots_p(int L, int P) {
+  const int lp = code_slots(L);
+  return (P > 8 && lp < 32) ? 32 : lp;
+}
+// Stored code bytes per key: Lp bytes (P <= 8) or Lp * P bits, tightly packed (P > 8)
+inline size_t code_bytes_per_key(int L, int P) {
+  const int lp = code_slots_p(L, P);
+  return P > 8 ? (size_t)lp * P / 8 : (size_t)lp;
+}
 inline int wide_lo_bits(int P) { return P / 2; }
 inline int wide_entries(int P) { return 1 << (P - P / 2); }   // rows per half-table image
 inline int heads_per_row(const socket_cfg& c) {
@@ -161,6 +171,11 @@ __device__ __forceinline__ uint2 ldg_nc_v2_hint(const void* p, uint64_t pol) {
                : "l"(p), "l"(pol));
   return r;
 }
+__device__ __forceinline__ uint32_t ldg_nc_u32_hint(const void* p, uint64_t pol) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ void st_f32_hint(float* p, float v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
 }
@@ -177,6 +192,15 @@ __device__ __forceinline__ uint2 ldg_nc_v2(const void* p) {
 __device__ __forceinline__ int local_len(int seq_len, long long index_base, int N_max) {
   const long long n = (long long)seq_len - index_base;
   return n < 0 ? 0 : (n > N_max ? N_max : (int)n);
+}
+
+// Packed wide codes (P > 8, NEXT-2): per (b, kv head) region, 32-key tiles;
+// per tile and 32-slot group g (G = Lp / 32 groups), the group's 32 P-bit slot
+// codes form one 32P-bit string (slot s at bits [sP, sP + P), LSB first), kept
+// as P u32 words, word-interleaved across the tile's 32 keys.  u32 index of
+// word w of group g of key j:
+__device__ __forceinline__ size_t packed_word(int j, int g, int w, int G, int P) {
+  return ((size_t)((j >> 5) * G + g) * P + w) * 32 + (j & 31);
 }
 
 // monotone map fp32 -> u32 (larger float <=> larger key)

@@ -57,7 +57,7 @@ socket_status launch_prologue(const socket_cfg& c, ProArgs a, bool tables, cudaS
   a.N_max = c.N_max;
   a.L = c.L;
   a.P = c.P;
-  a.Lp = code_slots(c.L);
+  a.Lp = code_slots_p(c.L, c.P);
   a.tau = c.tau;
   a.hard = c.scoring == SOCKET_SCORING_HARD;
   a.tpt = c.P > 8 ? 64 / c.P : kTT;
@@ -132,7 +132,7 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, vo
                                  const void* k_new, const void* v_new, int k, int sink, int window,
                                  float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
                                  void* ws, size_t ws_bytes, cudaStream_t st) {
-  const int Lp = code_slots(c.L);
+  const int Lp = code_slots_p(c.L, c.P);
   if (Lp > 64) return fail(SOCKET_EUNSUPPORTED, "decode step: L > 64 not supported");
   const int H_sel = num_sel_rows(c);
   const int NH = c.group_mode == SOCKET_GROUP_PER_QHEAD ? 1 : c.H_q / c.H_kv;

@@ -449,9 +449,24 @@ __device__ __forceinline__ void append_tile(const ProArgs& a, int at, int wt, ch
       const int Lp = a.Lp;
       const int M = (Lp < 32 ? Lp : 32) - 1;
       const int s = (l & ~M) | ((l - j) & M);
-      const size_t o = (size_t)kbh[m] * a.N_max * Lp + code_off(j, s, Lp);
-      if (P > 8) reinterpret_cast<uint16_t*>(a.codes)[o] = (uint16_t)code;
-      else a.codes[o] = (uint8_t)code;
+      if (P > 8) {
+        // packed wide codes: the slot's P bits in one or two words; other tiles'
+        // CTAs write other slots of the same words, so clear and set only mine
+        // with atomics (disjoint bit sets: the order does not matter)
+        const int G = Lp >> 5, g = s >> 5, bp = (s & 31) * P, w = bp >> 5, sh = bp & 31;
+        uint32_t* cw = reinterpret_cast<uint32_t*>(a.codes) + (size_t)kbh[m] * a.N_max * Lp * P / 32;
+        const uint32_t fm = (1u << P) - 1u;
+        uint32_t* w0 = cw + packed_word(j, g, w, G, P);
+        atomicAnd(w0, ~(fm << sh));
+        atomicOr(w0, code << sh);
+        if (sh + P > 32) {
+          uint32_t* w1 = cw + packed_word(j, g, w + 1, G, P);
+          atomicAnd(w1, ~(fm >> (32 - sh)));
+          atomicOr(w1, code >> (32 - sh));
+        }
+      } else {
+        a.codes[(size_t)kbh[m] * a.N_max * Lp + code_off(j, s, Lp)] = (uint8_t)code;
+      }
     }
   }
   if (a.V && wt == 0 && tid < 256) {   // ||v_j||: warp w handles keys 4w .. 4w+3

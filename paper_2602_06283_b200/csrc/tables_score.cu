@@ -34,38 +34,55 @@ constexpr int kScoreThreads = 512;            // 16 warps, one CTA per SM (persi
 constexpr int kScoreWarps = kScoreThreads / 32;
 
 // ----------------------------------------------------------------------------
-// wide-code score kernel (P > 8, NEXT-2): codes are uint16, the LUT image holds
-// per head the factor half-tables A_h (low Pl bits) and B_h (high P - Pl bits);
-//   w_hat(j) = sum_s sum_h A_h[l(s)](lo) * B_h[l(s)](hi)   (fp32 fma, s then h ascending)
-// One CTA = (selection row, 256-tile chunk); lane = key, same bank-rotated
-// column c(s, lane) = (s & 32) | ((s + lane) & 31) as the byte-code kernel.
+// wide-code score kernels (P > 8, NEXT-2).  Codes are tightly packed: per key
+// and 32-slot group, one 32P-bit string (P u32 words, word-interleaved across
+// the tile's keys; internal.cuh packed_word) -- 600 useful of 640 stored bits
+// per key at the RULER setting L = 60, P = 10.  The LUT image holds per head
+// the factor half-tables A_h (low Pl bits) and B_h (high P - Pl bits) of the
+// exact product form p_h(r) = A_h(r mod 2^Pl) B_h(r >> Pl).
 // ----------------------------------------------------------------------------
 constexpr int kWideThreads = 512;
 constexpr int kWideTilesPerCta = 256;
 
-template <int NH>
+// the P-bit code of slot sl of a group string w[0..P), placed at bit `dst`
+// (sl, P, dst compile-time after unrolling: one funnel shift, or a shift)
+template <int P>
+__device__ __forceinline__ uint32_t slot_bits(const uint32_t (&w)[P], int sl, int dst) {
+  const int r = sl * P - dst;
+  if (r < 0) return w[0] << (-r);
+  const int i = r >> 5, sh = r & 31;
+  const uint32_t hi = (i + 1 < P) ? w[i + 1 < P ? i + 1 : P - 1] : 0u;
+  return sh == 0 ? w[i] : __funnelshift_r(w[i], hi, sh);
+}
+
+// P = 11..16 (and any group size): every slot and head adds A_h[lo] * B_h[hi]
+//   w_hat(j) = sum_s sum_h A_h[l(s)](lo) * B_h[l(s)](hi)   (fp32 fma, s then h ascending)
+// One CTA = (selection row, 256-tile chunk); lane = key, bank-rotated column
+// c(s, lane) = (s & 32) | ((s + lane) & 31) as the byte-code kernel.
+template <int NH, int P>
 __global__ void __launch_bounds__(kWideThreads, 1)
-score_wide_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ codes,
+score_wide_kernel(const float* __restrict__ lut_g, const uint32_t* __restrict__ codes,
                   const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
                   const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
-                  int G_sel, int N_max, int Lp, int P, int E, int row_floats, long long index_base) {
+                  int G_sel, int N_max, int Lp, int E, int row_floats, long long index_base) {
   extern __shared__ __align__(16) float wlut[];
+  constexpr int Pl = P / 2;
+  constexpr uint32_t lomask = (1u << Pl) - 1u, fmask = (1u << P) - 1u;
   const int row = blockIdx.y;
   const int b = row / H_sel, r = row % H_sel, g = r / G_sel;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t pol_code = l2_policy_evict_first();
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const float4* src = reinterpret_cast<const float4*>(lut_g + (size_t)row * row_floats);
   for (int i = threadIdx.x; i < row_floats / 4; i += kWideThreads)
     reinterpret_cast<float4*>(wlut)[i] = src[i];
   __syncthreads();
   const int n = local_len(seq_lens[b], index_base, N_max);
-  const int Pl = P / 2;
-  const uint32_t lomask = (1u << Pl) - 1u;
-  const int CB = Lp < 16 ? Lp : 16;
+  const int G = Lp >> 5;
   const int tiles = N_max >> 5;
   const int t0 = blockIdx.x * kWideTilesPerCta;
   const int t1 = min(t0 + kWideTilesPerCta, tiles);
-  const uint16_t* crow = codes + ((size_t)b * H_kv + g) * N_max * Lp;
+  const uint32_t* crow = codes + ((size_t)b * H_kv + g) * (size_t)N_max * Lp * P / 32;
   const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
   const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
   float* srow = scores + (size_t)row * N_max;
@@ -76,18 +93,14 @@ score_wide_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ 
       continue;
     }
     float acc = 0.f;
-    for (int ch = 0; ch < Lp / CB; ++ch) {
-      const uint16_t* cp = crow + code_off(j, ch * CB, Lp);
-      uint4 w[2];
-      w[0] = ldg_nc_v4(cp);
-      w[1] = CB == 16 ? ldg_nc_v4(cp + 8) : make_uint4(0, 0, 0, 0);
-      const uint32_t* wd = reinterpret_cast<const uint32_t*>(w);
+    for (int gi = 0; gi < G; ++gi) {
+      uint32_t w[P];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        if (e >= CB) break;
-        const int sidx = ch * CB + e;
-        const uint32_t code = (e & 1) ? (wd[e >> 1] >> 16) : (wd[e >> 1] & 0xFFFFu);
-        const int col = (sidx & 32) | ((sidx + lane) & 31);
+      for (int wd = 0; wd < P; ++wd) w[wd] = ldg_nc_u32_hint(crow + packed_word(j, gi, wd, G, P), pol_code);
+#pragma unroll
+      for (int sl = 0; sl < 32; ++sl) {
+        const uint32_t code = slot_bits<P>(w, sl, 0) & fmask;
+        const int col = gi * 32 + ((sl + lane) & 31);
         const int lo = (int)(code & lomask), hi = (int)(code >> Pl);
 #pragma unroll
         for (int h = 0; h < NH; ++h)
@@ -99,21 +112,24 @@ score_wide_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ 
   }
 }
 
-// Wide codes with P <= 10 and Lp in {32, 64}: per 32-slot group (= 32 tables,
-// the rotation group), the group-summed tables T_l(r) = sum_h A_h,l(r mod 2^Pl)
+// Wide codes with P <= 10: per 32-slot group (= 32 tables, the rotation
+// group), the group-summed tables T_l(r) = sum_h A_h,l(r mod 2^Pl)
 // B_h,l(r >> Pl) are materialized in shared memory ([2^P][32] fp32, <= 128 KB)
 // from the half-table image, so a lookup is one conflict-free LDS as in the
 // byte-code kernel; the CTA sweeps its keys once per group, keeping the first
-// group's partial sums in shared memory.
-template <int NH>
+// group's partial sums in `scores` (read back by the same thread).  A lookup's
+// byte offset is a funnel shift of the packed words that lands the code at
+// bit 7 (row stride 128 B) and one LOP3 with the lane's column offset.
+template <int NH, int P>
 __global__ void __launch_bounds__(kWideThreads, 1)
-score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__ codes,
+score_wide2_kernel(const float* __restrict__ lut_g, const uint32_t* __restrict__ codes,
                    const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
                    const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
-                   int G_sel, int N_max, int Lp, int P, int E, int row_floats, long long total_tiles,
+                   int G_sel, int N_max, int Lp, int E, int row_floats, long long total_tiles,
                    long long index_base) {
   extern __shared__ __align__(16) float w2[];
-  const int R = 1 << P, Pl = P / 2, RL = 1 << Pl;
+  constexpr int R = 1 << P, Pl = P / 2, RL = 1 << Pl;
+  constexpr uint32_t amask = (uint32_t)(R - 1) << 7;
   float* tab = w2;                          // [R][32]
   const char* tabc = reinterpret_cast<const char*>(w2);
   float* ast = tab + R * 32;                // [NH][RL][32] staged A half-tables of the group
@@ -134,7 +150,7 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
     t = seg_end;
     const int b = row / H_sel, r = row % H_sel, g = r / G_sel;
     const int n = local_len(seq_lens[b], index_base, N_max);
-    const uint16_t* crow = codes + ((size_t)b * H_kv + g) * N_max * Lp;
+    const uint32_t* crow = codes + ((size_t)b * H_kv + g) * (size_t)N_max * Lp * P / 32;
     const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
     const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
     float* srow = scores + (size_t)row * N_max;
@@ -161,13 +177,12 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
         }
       }
       __syncthreads();
-      // sweep: lane = key, slots gi*32 .. gi*32 + 31 (two 16-element chunks); the
-      // first group's partial sum is parked in `scores` (the same thread reads it back)
+      // sweep: lane = key, slots gi*32 .. gi*32 + 31
       constexpr int kU = 2;                   // tiles per batch per warp
       constexpr int kStep = kU * (kWideThreads / 32);
       const bool last = gi + 1 == groups;
       struct Batch {
-        uint4 w[kU][4];
+        uint32_t w[kU][P];
         float prev[kU], vn[kU];               // parked partial, ||v_j|| (loaded with the codes)
       };
       auto load = [&](Batch& B, int ti0) {
@@ -178,12 +193,8 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
           B.prev[u] = 0.f;
           B.vn[u] = 0.f;
           if (ti < vt1) {
-            const uint16_t* cp = crow + code_off(j, gi * 32, Lp);
-            const uint16_t* cp2 = crow + code_off(j, gi * 32 + 16, Lp);
-            B.w[u][0] = ldg_nc_v4_hint(cp, pol_code);
-            B.w[u][1] = ldg_nc_v4_hint(cp + 8, pol_code);
-            B.w[u][2] = ldg_nc_v4_hint(cp2, pol_code);
-            B.w[u][3] = ldg_nc_v4_hint(cp2 + 8, pol_code);
+#pragma unroll
+            for (int wd = 0; wd < P; ++wd) B.w[u][wd] = ldg_nc_u32_hint(crow + packed_word(j, gi, wd, groups, P), pol_code);
             if (gi > 0) B.prev[u] = srow[j];
             if (last) B.vn[u] = __ldg(vrow + j);
           }
@@ -195,15 +206,11 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
           const int ti = ti0 + u * (kWideThreads / 32);
           if (ti >= vt1) break;
           const int j = ti * 32 + lane;
-          const uint32_t* wd = reinterpret_cast<const uint32_t*>(B.w[u]);
-          // byte offset code * 128 + 4 ((sl + lane) & 31), codes < 2^10: the two
-          // codes of a word are shifted in place and OR-ed with the column offset
           uint64_t acc = 0ull;
 #pragma unroll
           for (int sl = 0; sl < 32; sl += 2) {
-            const uint32_t wv = wd[sl >> 1];
-            const uint32_t a0 = ((wv << 7) & 0x1FF80u) | ((lane4 + 4u * sl) & 124u);
-            const uint32_t a1 = ((wv >> 9) & 0x1FF80u) | ((lane4 + 4u * sl + 4u) & 124u);
+            const uint32_t a0 = (slot_bits<P>(B.w[u], sl, 7) & amask) | ((lane4 + 4u * sl) & 124u);
+            const uint32_t a1 = (slot_bits<P>(B.w[u], sl + 1, 7) & amask) | ((lane4 + 4u * sl + 4u) & 124u);
             const float v0 = *reinterpret_cast<const float*>(tabc + a0);
             const float v1 = *reinterpret_cast<const float*>(tabc + a1);
             const uint64_t pv = (uint64_t)__float_as_uint(v0) | ((uint64_t)__float_as_uint(v1) << 32);
@@ -239,7 +246,7 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint16_t* __restrict__
 static socket_status launch_score_wide(const socket_cfg& c, const float* lut, const uint8_t* codes,
                                        const float* vnorm, const int32_t* seq_lens,
                                        const uint8_t* mask, float* scores, cudaStream_t st) {
-  const int Lp = code_slots(c.L);
+  const int Lp = code_slots_p(c.L, c.P);
   if (Lp > 64) return fail(SOCKET_EUNSUPPORTED, "score: P > 8 with more than 64 tables");
   const size_t bytes = lut_row_bytes(c);
   if (bytes > kWideLutMax)
@@ -251,39 +258,42 @@ static socket_status launch_score_wide(const socket_cfg& c, const float* lut, co
   if (grid.x == 0 || grid.y == 0) return SOCKET_OK;
   const int E = wide_entries(c.P);
   const int row_floats = (int)(bytes / sizeof(float));
-  if (c.P <= 10 && Lp >= 32 && true) {
+  const uint32_t* cw = reinterpret_cast<const uint32_t*>(codes);
+  if (c.P <= 10) {
     // group-summed tables per 32-slot group (one LDS per lookup)
     const int R = 1 << c.P, RL = 1 << (c.P / 2);
     const size_t sm2 = ((size_t)R * 32 + (size_t)NH * RL * 32) * sizeof(float);
     const long long total_tiles = (long long)c.B * H_sel * (c.N_max / 32);
     const unsigned pgrid = (unsigned)(total_tiles < num_sms() ? total_tiles : num_sms());
-#define SK_WIDE2(N)                                                                          \
-  case N:                                                                                    \
-    cudaFuncSetAttribute(score_wide2_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2); \
-    score_wide2_kernel<N><<<pgrid, kWideThreads, sm2, st>>>(                                 \
-        lut, reinterpret_cast<const uint16_t*>(codes), vnorm, seq_lens, mask, scores, H_sel, c.H_kv, \
-        G_sel, c.N_max, Lp, c.P, E, row_floats, total_tiles, c.index_base);                  \
-    return check_launch("score_wide2_kernel");
-    switch (NH) {
-      SK_WIDE2(1) SK_WIDE2(2) SK_WIDE2(4) SK_WIDE2(8)
-      default: break;
-    }
+#define SK_WIDE2(N, PV)                                                                        \
+  if (NH == N && c.P == PV) {                                                                  \
+    cudaFuncSetAttribute(score_wide2_kernel<N, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2); \
+    score_wide2_kernel<N, PV><<<pgrid, kWideThreads, sm2, st>>>(                               \
+        lut, cw, vnorm, seq_lens, mask, scores, H_sel, c.H_kv, G_sel, c.N_max, Lp, E, row_floats, \
+        total_tiles, c.index_base);                                                            \
+    return check_launch("score_wide2_kernel");                                                 \
+  }
+    SK_WIDE2(1, 9) SK_WIDE2(2, 9) SK_WIDE2(4, 9) SK_WIDE2(8, 9)
+    SK_WIDE2(1, 10) SK_WIDE2(2, 10) SK_WIDE2(4, 10) SK_WIDE2(8, 10)
 #undef SK_WIDE2
+    return fail(SOCKET_EUNSUPPORTED, "score: heads per selection row must be 1, 2, 4 or 8");
   }
-#define SK_WIDE(N)                                                                             \
-  case N:                                                                                      \
-    cudaFuncSetAttribute(score_wide_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); \
-    score_wide_kernel<N><<<grid, kWideThreads, bytes, st>>>(                                   \
-        lut, reinterpret_cast<const uint16_t*>(codes), vnorm, seq_lens, mask, scores, H_sel, c.H_kv, \
-        G_sel, c.N_max, Lp, c.P, E, row_floats, c.index_base);                                 \
-    break;
-  switch (NH) {
-    SK_WIDE(1) SK_WIDE(2) SK_WIDE(4) SK_WIDE(8)
-    default:
-      return fail(SOCKET_EUNSUPPORTED, "score: heads per selection row must be 1, 2, 4 or 8");
+#define SK_WIDE(N, PV)                                                                         \
+  if (NH == N && c.P == PV) {                                                                  \
+    cudaFuncSetAttribute(score_wide_kernel<N, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); \
+    score_wide_kernel<N, PV><<<grid, kWideThreads, bytes, st>>>(                               \
+        lut, cw, vnorm, seq_lens, mask, scores, H_sel, c.H_kv, G_sel, c.N_max, Lp, E, row_floats, \
+        c.index_base);                                                                         \
+    return check_launch("score_wide_kernel");                                                  \
   }
+  SK_WIDE(1, 11) SK_WIDE(2, 11) SK_WIDE(4, 11) SK_WIDE(8, 11)
+  SK_WIDE(1, 12) SK_WIDE(2, 12) SK_WIDE(4, 12) SK_WIDE(8, 12)
+  SK_WIDE(1, 13) SK_WIDE(2, 13) SK_WIDE(4, 13) SK_WIDE(8, 13)
+  SK_WIDE(1, 14) SK_WIDE(2, 14) SK_WIDE(4, 14) SK_WIDE(8, 14)
+  SK_WIDE(1, 15) SK_WIDE(2, 15) SK_WIDE(4, 15) SK_WIDE(8, 15)
+  SK_WIDE(1, 16) SK_WIDE(2, 16) SK_WIDE(4, 16) SK_WIDE(8, 16)
 #undef SK_WIDE
-  return check_launch("score_wide_kernel");
+  return fail(SOCKET_EUNSUPPORTED, "score: heads per selection row must be 1, 2, 4 or 8");
 }
 
 // ----------------------------------------------------------------------------
@@ -408,7 +418,7 @@ socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint
                                const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
                                float* scores, cudaStream_t st, bool pdl) {
   if (c.P > 8) return launch_score_wide(c, lut, codes, vnorm, seq_lens, mask, scores, st);
-  const int Lp = code_slots(c.L);
+  const int Lp = code_slots_p(c.L, c.P);
   const int H_sel = num_sel_rows(c);
   const int G_sel = c.group_mode == SOCKET_GROUP_PER_QHEAD ? c.H_q / c.H_kv : 1;
   const long long total_tiles = (long long)c.B * H_sel * (c.N_max / 32);
