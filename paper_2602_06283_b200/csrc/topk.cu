@@ -255,6 +255,9 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
   extern __shared__ __align__(16) uint32_t skeys[];          // [per], per % 128 == 0
   __shared__ TopkShared S;
   TK_TRACE(0);
+  // cluster barrier phase 1 of 2: every CTA must be running before topk_core
+  // pushes into its shared memory (waited for after the slice load)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: scores of the predecessor
   TK_TRACE(1);
   cg::cluster_group cluster = cg::this_cluster();
@@ -342,6 +345,7 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
   kmin += 1u;   // back from key - 1 (no regular key: 0xFFFFFFFF + 1 = 0, fixed below)
   if (kmin == 0u) kmin = 0xFFFFFFFFu;
   if (GK) __syncthreads();   // global slices: written and re-read by other threads
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // every CTA of the cluster runs
   switch (a.op) {
     case 0:
       topk_core(a, keys, S, row, n, base, len, nvalid, nforced, kmin, kmax, nullptr, nullptr, nullptr);

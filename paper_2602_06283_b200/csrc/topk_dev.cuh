@@ -108,6 +108,10 @@ struct __align__(16) TopkShared {
   uint32_t acc[2];               // lower ranks' candidates > T / == T
   alignas(16) uint32_t stat[8];  // nvalid, nforced, kmin, kmax, ncand, above, gt, eq (read remotely)
   uint32_t dec[4];
+  // written by the other CTAs (pushed before a cluster barrier, never read remotely):
+  uint4 sall[kMaxCluster];       // every rank's (nvalid, nforced, kmin, kmax)
+  uint2 call[kMaxCluster];       // every rank's (#candidates, #keys above the target bin)
+  uint32_t gall[kCandCap];       // every rank's candidates, rank r at [r * cap, r * cap + count)
 };
 
 __device__ __forceinline__ void topk_emit(const TopkArgs& a, uint32_t* keys, TopkShared& S, int row, int base,
@@ -200,13 +204,18 @@ __device__ __forceinline__ void topk_core(const TopkArgs& a, uint32_t* keys, Top
     atomicMin(&S.stat[2], kmin);
     atomicMax(&S.stat[3], kmax);
   }
+  __syncthreads();
+  // push my statistics to every rank (remote stores complete at the barrier;
+  // the caller has made sure every CTA of the cluster is running)
+  if (tid < csize)
+    *cluster.map_shared_rank(&S.sall[crank], tid) = *reinterpret_cast<const uint4*>(S.stat);
   TK_TRACE(2);
   cluster.sync();
-  // ---- 1. cluster totals: lane r of warp 0 reads rank r's statistics ----------
+  // ---- 1. cluster totals from the pushed statistics (local reads) --------------
   if (warp == 0) {
     uint32_t v0 = 0, v1 = 0, v2 = 0xFFFFFFFFu, v3 = 0;
     if (lane < csize) {
-      const uint4 rs = *reinterpret_cast<const uint4*>(cluster.map_shared_rank(S.stat, lane));
+      const uint4 rs = S.sall[lane];
       v0 = rs.x; v1 = rs.y; v2 = rs.z; v3 = rs.w;
     }
 #pragma unroll
@@ -339,16 +348,29 @@ __device__ __forceinline__ void topk_core(const TopkArgs& a, uint32_t* keys, Top
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) ab += __shfl_xor_sync(kFull, ab, o);
       if (lane == 0) { S.wab[warp] = ab; atomicAdd(&S.stat[5], ab); }
+      __syncthreads();
+      // push (count, above) and -- when they fit my share of the buffer -- my
+      // candidates to every rank, so that after the barrier all reads are local
+      const int cap = kCandCap / csize;
+      {
+        const uint32_t nloc = S.stat[4], abv = S.stat[5];
+        const int npush = 1 + (nloc <= (uint32_t)cap ? (int)nloc : 0);
+        for (int e = tid; e < csize * npush; e += kTopkThreads) {
+          const int r = e % csize, i = e / csize;
+          if (i == 0) *cluster.map_shared_rank(&S.call[crank], r) = make_uint2(nloc, abv);
+          else cluster.map_shared_rank(S.gall, r)[crank * cap + i - 1] = S.cand[i - 1];
+        }
+      }
       TK_TRACE(7);
       cluster.sync();
       TK_TRACE(8);
-      // gather every rank's candidates (rank-major) and above-bin counts
+      // every rank's candidate count and above-bin count (local), rank-major offsets
       if (warp == 0) {
         uint32_t nc = 0, rab = 0;
         if (lane < csize) {
-          const uint32_t* rs = cluster.map_shared_rank(S.stat, lane);
-          nc = rs[4];
-          rab = rs[5];
+          const uint2 rs = S.call[lane];
+          nc = rs.x;
+          rab = rs.y;
         }
         uint32_t inc = nc;
 #pragma unroll
@@ -358,12 +380,16 @@ __device__ __forceinline__ void topk_core(const TopkArgs& a, uint32_t* keys, Top
         }
         if (lane < csize) { S.roff[lane + 1] = inc; S.rab[lane] = rab; }
         if (lane == 0) S.roff[0] = 0;
+        const unsigned over = __ballot_sync(kFull, lane < csize && nc > (uint32_t)cap);
+        if (lane == 0) S.dec[3] = over;
       }
       __syncthreads();
+      const bool pushed = S.dec[3] == 0u;   // else some rank had more than `cap`: read remotely
       for (int i = tid; i < (int)C; i += kTopkThreads) {
         int r = 0;
         while (r + 1 < csize && S.roff[r + 1] <= (uint32_t)i) ++r;
-        S.gcand[i] = cluster.map_shared_rank(S.cand, r)[i - (int)S.roff[r]];
+        S.gcand[i] = pushed ? S.gall[r * cap + i - (int)S.roff[r]]
+                            : cluster.map_shared_rank(S.cand, r)[i - (int)S.roff[r]];
       }
       __syncthreads();
       // T = the need2-th largest candidate, above = candidates > T

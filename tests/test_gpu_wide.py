@@ -52,7 +52,7 @@ def check_codes(got, ref, margin, P):
 def test_wide_codes_prefill_and_append(L, P, N):
     cfg, c, W, d = make(2, 2, 2, N, L, P, seed=L + P)
     codes = ops.alloc_codes(cfg, DEV)
-    assert codes.numel() == 2 * 2 * N * cfg.code_slots * 2
+    assert codes.numel() == 2 * 2 * N * max(32, cfg.code_slots) * P // 8   # packed: Lp * P bits per key
     vn = torch.zeros((2, 2, N), dtype=torch.float32, device=DEV)
     ops.hash_keys(cfg, d["K"], d["W"], codes, V=d["V"], vnorm=vn)
     ref, margin = O.hash_keys(O.widen(c["K"]), O.widen(W))
