@@ -71,13 +71,15 @@ def point(ctx, batch, L, P, sparsity, flush, cache, mode=None, H_q=32, H_kv=8):
     qq = q.view(batch, H_q, 1, 128)
     t_sdpa = timed(lambda: torch.nn.functional.scaled_dot_product_attention(qq, K, V, scale=cfg.scale,
                                                                              enable_gqa=True), flush)
-    score_bytes = batch * H_kv * ctx * (L * ((P + 7) // 8) + 4) + batch * cfg.H_sel * ctx * 4
+    code_bytes = ops.codes_bytes(cfg) // (batch * H_kv * ctx)      # stored bytes per key (packed for P > 8)
+    score_bytes = batch * H_kv * ctx * (code_bytes + 4) + batch * cfg.H_sel * ctx * 4
     dec_bytes = batch * cfg.H_sel * k * 516 + batch * H_q * 512
     best_dense = min(t_dense, t_sdpa)
     return {
         "ctx": ctx, "batch": batch, "H_q": H_q, "H_kv": H_kv,
         "selection": "per_qhead" if cfg.group_mode == PER_QHEAD else "kv_shared",
-        "fused_step": dec.fused, "L": L, "P": P, "bits_per_token": L * P, "sparsity": sparsity, "k": k,
+        "launches": ops.decode_step_launches(cfg), "L": L, "P": P, "bits_per_token": L * P,
+        "stored_bits_per_token": code_bytes * 8, "sparsity": sparsity, "k": k,
         "step_ms": round(t_step, 4), "tokens_per_s": round(batch / (t_step * 1e-3), 1),
         "dense_ms": round(best_dense, 4), "dense_impl": "ours" if t_dense <= t_sdpa else "torch_sdpa",
         "speedup_vs_dense": round(best_dense / t_step, 3),
