@@ -348,8 +348,7 @@ __global__ void __launch_bounds__(kTopkThreads, 2) topk_cluster_kernel(TopkArgs 
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // every CTA of the cluster runs
   switch (a.op) {
     case 0:
-      if (!topk_fast(a, keys, S, row, n_glob, n, base, len, nvalid, nforced))
-        topk_core(a, keys, S, row, n, base, len, nvalid, nforced, kmin, kmax, nullptr, nullptr, nullptr);
+      topk_core(a, keys, S, row, n, base, len, nvalid, nforced, kmin, kmax, nullptr, nullptr, nullptr);
       break;
     case 1:
       topk_digest(a, keys, S, row, len, nvalid, nforced, kmin, kmax, shards);

@@ -116,8 +116,7 @@ struct __align__(16) TopkShared {
 
 __device__ __forceinline__ void topk_emit(const TopkArgs& a, uint32_t* keys, TopkShared& S, int row, int base,
                                           int len, uint32_t T, uint32_t quota, uint32_t k_out, bool counted,
-                                          int32_t* sel_local, int* sel_lo, int* sel_cnt, int ext_gb = -1,
-                                          int ext_eb = -1);
+                                          int32_t* sel_local, int* sel_lo, int* sel_cnt);
 
 // Local exact select over a small candidate array: the `need`-th largest key
 // (1-based) and how many candidates are strictly greater.
@@ -515,8 +514,7 @@ __device__ __forceinline__ void topk_core(const TopkArgs& a, uint32_t* keys, Top
 // (written to cnt by CTA 0).  Ends with a cluster barrier.
 __device__ __forceinline__ void topk_emit(const TopkArgs& a, uint32_t* keys, TopkShared& S, int row, int base,
                                           int len, uint32_t T, uint32_t quota, uint32_t k_out, bool counted,
-                                          int32_t* sel_local, int* sel_lo, int* sel_cnt, int ext_gb,
-                                          int ext_eb) {
+                                          int32_t* sel_local, int* sel_lo, int* sel_cnt) {
   constexpr unsigned kFull = 0xffffffffu;
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
@@ -558,13 +556,10 @@ __device__ __forceinline__ void topk_emit(const TopkArgs& a, uint32_t* keys, Top
       gw += w < warp ? xg : 0u; ew += w < warp ? xe : 0u;
       gtot += xg; etot += xe;
     }
+    if (tid == 0) { S.stat[6] = gtot; S.stat[7] = etot; }
+    cluster.sync();
     uint32_t gb = 0, eb = 0;
-    if (ext_gb >= 0) {       // lower ranks' counts given by the caller: no barrier
-      gb = (uint32_t)ext_gb;
-      eb = (uint32_t)ext_eb;
-    } else {
-      if (tid == 0) { S.stat[6] = gtot; S.stat[7] = etot; }
-      cluster.sync();
+    {
       uint32_t vg[kMaxCluster], ve[kMaxCluster];
 #pragma unroll
       for (int r = 0; r < kMaxCluster; ++r) {
@@ -647,205 +642,7 @@ __device__ __forceinline__ void topk_emit(const TopkArgs& a, uint32_t* keys, Top
     if (tid == 0) a.cnt[row] = (int)k_out;
   }
   TK_TRACE(13);
-  if (ext_gb < 0) cluster.sync();   // keep shared memory alive until every CTA finished remote reads
-}
-
-
-// ---------------------------------------------------------------------------
-// Fast path of the row select (op 0): one cluster barrier instead of four.
-// Every CTA reads the same strided sample of the whole row from `scores`
-// (<= kSample keys) and derives the same key bracket [lo, hi) around the
-// expected threshold (sample quantiles +- a few standard deviations); a pass
-// over its slice counts the keys >= hi (forced included) and collects the
-// bracket's keys; (#valid, #forced, #above, #candidates) and the candidates are
-// pushed to every rank before the one barrier.  If the bracket holds the
-// threshold (#above < k_eff <= #above + #candidates) and no CTA overflowed its
-// candidate share, T and the tie quota follow from the candidates exactly and
-// each CTA's emit offsets from the pushed counts (no further barrier).
-// Otherwise returns false and the caller runs topk_core (exact, any input).
-// ---------------------------------------------------------------------------
-constexpr int kSample = 2 * kCandCap;   // sample keys (S.cidx + S.gcand)
-
-__device__ __forceinline__ bool topk_fast(const TopkArgs& a, uint32_t* keys, TopkShared& S, int row, int n_glob,
-                                          int n, int base, int len, uint32_t nvalid, uint32_t nforced) {
-  constexpr unsigned kFull = 0xffffffffu;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int crank = (int)cluster.block_rank();
-  const int csize = (int)cluster.num_blocks();
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (n <= 0) return false;
-  // ---- 1. the sample (same in every CTA) and its 2048-bin histogram ------------
-  uint32_t* samp = S.cidx;                       // kSample keys (cidx and gcand are adjacent)
-  const int stride = (n + kSample - 1) / kSample;
-  const int ns = (n + stride - 1) / stride;
-  const float* srow = a.scores + (size_t)row * a.N_max;
-  uint32_t smin = 0xFFFFFFFFu, smax = 0u, sreg = 0;
-  for (int i = tid; i < ns; i += kTopkThreads) {
-    const int j = i * stride;
-    const uint32_t key = make_key(srow[j], j, n_glob, a.index_base, a.sink, a.window);
-    samp[i] = key;
-    if (key != 0u && key != 0xFFFFFFFFu) { smin = min(smin, key); smax = max(smax, key); ++sreg; }
-  }
-  if (tid < kBins / 4) reinterpret_cast<uint4*>(S.hist)[tid] = make_uint4(0, 0, 0, 0);
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    smin = min(smin, __shfl_xor_sync(kFull, smin, o));
-    smax = max(smax, __shfl_xor_sync(kFull, smax, o));
-    sreg += __shfl_xor_sync(kFull, sreg, o);
-  }
-  if (tid < 4) S.dec[tid] = tid == 0 ? 0xFFFFFFFFu : 0u;
-  __syncthreads();
-  if (lane == 0) { atomicMin(&S.dec[0], smin); atomicMax(&S.dec[1], smax); atomicAdd(&S.dec[2], sreg); }
-  __syncthreads();
-  const uint32_t gmin = S.dec[0], gmax = S.dec[1], nreg = S.dec[2];
-  if (nreg < 64u) return false;                  // too few regular keys to bracket
-  const uint32_t span = gmax - gmin;
-  const int sh = span < (uint32_t)kBins ? 0 : (32 - __clz(span)) - 11;
-  for (int i = tid; i < ns; i += kTopkThreads) {
-    const uint32_t key = samp[i];
-    if (key != 0u && key != 0xFFFFFFFFu) atomicAdd(&S.hist[(key - gmin) >> sh], 1u);
-  }
-  __syncthreads();
-  // target rank among the regular sample keys: k (less the forced keys, which
-  // are all above) in proportion; bracket = +- (3 sigma + 8) sample ranks
-  const float f_forced = fminf((float)(a.sink + a.window), (float)a.k);
-  const float t_s = fmaxf(1.f, ((float)a.k - f_forced) / (float)stride);
-  const float dlt = 3.f * sqrtf(t_s) + 8.f;
-  const uint32_t r_hi = (uint32_t)fmaxf(0.f, t_s - dlt);           // 0: hi above every sampled key
-  const uint32_t r_lo = (uint32_t)fminf((float)nreg, t_s + dlt);
-  if (warp == 0) {
-    // bins lane*64 .. lane*64+63 per lane, descending suffix over the bins
-    uint32_t tot = 0;
-    for (int q = 0; q < 64; ++q) tot += S.hist[lane * 64 + q];
-    uint32_t inc = tot;                                              // inclusive suffix (lanes >= lane)
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_down_sync(kFull, inc, o);
-      if (lane + o < 32) inc += y;
-    }
-    // bin b_x holding sample rank x (1-based, descending): suffix(b_x) >= x > suffix(b_x + 1)
-    uint32_t run = inc - tot;                                        // keys in bins above my range
-    int b_hi = -1, b_lo = -1;
-    for (int q = 63; q >= 0; --q) {
-      const uint32_t h = S.hist[lane * 64 + q];
-      if (r_hi >= 1 && run < r_hi && run + h >= r_hi) b_hi = lane * 64 + q;
-      if (run < r_lo && run + h >= r_lo) b_lo = lane * 64 + q;
-      run += h;
-    }
-    const unsigned mh = __ballot_sync(kFull, b_hi >= 0), ml = __ballot_sync(kFull, b_lo >= 0);
-    const int bh = mh ? __shfl_sync(kFull, b_hi, __ffs(mh) - 1) : -1;
-    const int bl = ml ? __shfl_sync(kFull, b_lo, __ffs(ml) - 1) : -1;
-    if (lane == 0) {
-      // hi: first edge above bin bh (sample keys >= hi number < r_hi); r_hi = 0:
-      // above every regular key (only forced keys are >= hi)
-      const unsigned long long hi64 = bh < 0 ? 0xFFFFFFFFull
-                                             : (unsigned long long)gmin + ((unsigned long long)(bh + 1) << sh);
-      S.dec[0] = (uint32_t)min(hi64, 0xFFFFFFFFull);
-      S.dec[1] = bl < 0 ? 1u : gmin + ((uint32_t)bl << sh);        // lo: lower edge of bin bl
-    }
-  }
-  __syncthreads();
-  const uint32_t hi = S.dec[0], lo = min(S.dec[1], hi);
-  // ---- 2. my slice: keys >= hi, the bracket's keys, counts -----------------------
-  const int cap = kCandCap / csize;
-  if (tid < 8) S.stat[tid] = 0u;
-  __syncthreads();
-  const int len128 = (len + 127) & ~127;
-  uint32_t above = 0;
-  for (int i = tid * 4; i < len128; i += kTopkThreads * 4) {
-    const uint4 kv = *reinterpret_cast<const uint4*>(keys + i);
-    const uint32_t k4[4] = {kv.x, kv.y, kv.z, kv.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t key = k4[e];
-      above += key >= hi ? 1u : 0u;                 // hi >= 1: invalid keys never count
-      if (key != 0u && key >= lo && key < hi) {
-        const uint32_t sl = atomicAdd(&S.stat[4], 1u);
-        if (sl < (uint32_t)cap) S.cand[sl] = key;
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    above += __shfl_xor_sync(kFull, above, o);
-    nvalid += __shfl_xor_sync(kFull, nvalid, o);
-    nforced += __shfl_xor_sync(kFull, nforced, o);
-  }
-  if (lane == 0) { atomicAdd(&S.stat[0], nvalid); atomicAdd(&S.stat[1], nforced); atomicAdd(&S.stat[5], above); }
-  __syncthreads();
-  const uint32_t ncand = S.stat[4];
-  {   // push (nvalid, nforced, above, ncand) and the candidates (if they fit) to every rank
-    const uint4 mine = make_uint4(S.stat[0], S.stat[1], S.stat[5], ncand);
-    const int npush = 1 + (ncand <= (uint32_t)cap ? (int)ncand : 0);
-    for (int e = tid; e < csize * npush; e += kTopkThreads) {
-      const int r = e % csize, i = e / csize;
-      if (i == 0) *cluster.map_shared_rank(&S.sall[crank], r) = mine;
-      else cluster.map_shared_rank(S.gall, r)[crank * cap + i - 1] = S.cand[i - 1];
-    }
-  }
-  cluster.sync();
-  // ---- 3. totals, threshold, quota (identical in every CTA) ----------------------
-  uint32_t tvalid = 0, tforced = 0, A = 0, C = 0;
-  bool over = false;
-  for (int r = 0; r < csize; ++r) {
-    const uint4 v = S.sall[r];
-    tvalid += v.x; tforced += v.y; A += v.z; C += v.w;
-    over |= v.w > (uint32_t)cap;
-  }
-  const uint32_t k_eff = min((uint32_t)a.k, tvalid);
-  uint32_t T, quota;
-  int ext_gb = 0, ext_eb = 0;
-  if (k_eff == tvalid) {                          // everything valid is selected
-    T = 0u;
-    quota = 0u;
-    for (int r = 0; r < crank; ++r) ext_gb += (int)S.sall[r].x;
-  } else if (k_eff <= tforced) {                  // forced keys only (all tie at the max key)
-    T = 0xFFFFFFFFu;
-    quota = k_eff;
-    for (int r = 0; r < crank; ++r) ext_eb += (int)S.sall[r].y;
-  } else {
-    if (over || A >= k_eff || A + C < k_eff) {    // bracket missed: the exact slow path
-      cluster.sync();                             // (after everyone read the pushed counts)
-      return false;
-    }
-    // compact the candidates rank-major into gcand (the sample is dead) and select
-    uint32_t* gc = S.gcand;
-    uint32_t off = 0;
-    for (int r = 0; r < csize; ++r) {
-      const uint32_t c = S.sall[r].w;
-      for (uint32_t i = tid; i < c; i += kTopkThreads) gc[off + i] = S.gall[r * cap + i];
-      off += c;
-    }
-    __syncthreads();
-    const uint32_t need = k_eff - A;
-    uint32_t ab;
-    local_select(gc, (int)C, need, S, tid, warp, lane, T, ab);
-    quota = need - ab;
-    // lower ranks' keys > T and == T
-    uint32_t gbv = 0, ebv = 0;
-    off = 0;
-    for (int r = 0; r < csize; ++r) {
-      const uint32_t c = S.sall[r].w;
-      if (r < crank) {
-        for (uint32_t i = tid; i < c; i += kTopkThreads) { gbv += gc[off + i] > T; ebv += gc[off + i] == T; }
-      }
-      off += c;
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      gbv += __shfl_xor_sync(kFull, gbv, o);
-      ebv += __shfl_xor_sync(kFull, ebv, o);
-    }
-    if (tid < 2) S.acc[tid] = 0u;
-    __syncthreads();
-    if (lane == 0 && (gbv | ebv)) { atomicAdd(&S.acc[0], gbv); atomicAdd(&S.acc[1], ebv); }
-    __syncthreads();
-    ext_gb = (int)S.acc[0];
-    ext_eb = (int)S.acc[1];
-    for (int r = 0; r < crank; ++r) ext_gb += (int)S.sall[r].z;   // their keys >= hi are all > T
-  }
-  topk_emit(a, keys, S, row, base, len, T, quota, k_eff, false, nullptr, nullptr, nullptr, ext_gb, ext_eb);
-  return true;
+  cluster.sync();   // keep shared memory alive until every CTA finished remote reads
 }
 
 }  // namespace sk
