@@ -112,6 +112,76 @@ score_wide_kernel(const float* __restrict__ lut_g, const uint32_t* __restrict__ 
   }
 }
 
+// Large half-table images (KV_SHARED at P >= 13: the row's image [NH][2][E][64]
+// exceeds shared memory): the same arithmetic tiled over (32-slot group g, head
+// chunk of NHC heads), i.e. sub-images [NHC][2][E][32] of <= 128 KB, one pass
+// over the CTA's keys per tile; a key's partial sum is parked in `scores`
+// between passes (the same thread owns the key in every pass) and the last
+// pass multiplies by ||v_j|| and applies the mask.
+template <int NHC, int P>
+__global__ void __launch_bounds__(kWideThreads, 1)
+score_wide_tiled_kernel(const float* __restrict__ lut_g, const uint32_t* __restrict__ codes,
+                        const float* __restrict__ vnorm, const int32_t* __restrict__ seq_lens,
+                        const uint8_t* __restrict__ mask, float* __restrict__ scores, int H_sel, int H_kv,
+                        int G_sel, int N_max, int Lp, int NH, int E, int row_floats, long long index_base) {
+  extern __shared__ __align__(16) float wsub[];   // [NHC][2][E][32]
+  constexpr int Pl = P / 2;
+  constexpr uint32_t lomask = (1u << Pl) - 1u, fmask = (1u << P) - 1u;
+  const int row = blockIdx.y;
+  const int b = row / H_sel, r = row % H_sel, g = r / G_sel;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t pol_code = l2_policy_evict_first();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int n = local_len(seq_lens[b], index_base, N_max);
+  const int G = Lp >> 5;
+  const int tiles = N_max >> 5;
+  const int t0 = blockIdx.x * kWideTilesPerCta;
+  const int t1 = min(t0 + kWideTilesPerCta, tiles);
+  const uint32_t* crow = codes + ((size_t)b * H_kv + g) * (size_t)N_max * Lp * P / 32;
+  const float* vrow = vnorm + ((size_t)b * H_kv + g) * N_max;
+  const uint8_t* mrow = mask ? mask + (size_t)b * N_max : nullptr;
+  float* srow = scores + (size_t)row * N_max;
+  const float* img = lut_g + (size_t)row * row_floats;
+  const int nchunks = NH / NHC;
+  const int npass = G * nchunks;
+  for (int pass = 0; pass < npass; ++pass) {
+    const int gi = pass / nchunks, hc = pass % nchunks;
+    __syncthreads();                                    // previous pass done with wsub
+    for (int e = threadIdx.x; e < NHC * 2 * E * 32; e += kWideThreads) {
+      const int col = e & 31, ent = (e >> 5) % E, half = (e / (32 * E)) & 1, h = e / (64 * E);
+      wsub[e] = img[(((hc * NHC + h) * 2 + half) * E + ent) * 64 + gi * 32 + col];
+    }
+    __syncthreads();
+    const bool first = pass == 0, last = pass + 1 == npass;
+    for (int ti = t0 + warp; ti < t1; ti += kWideThreads / 32) {
+      const int j = ti * 32 + lane;
+      if (ti * 32 >= n) {                               // whole tile past seq_len
+        if (last) srow[j] = -INFINITY;
+        continue;
+      }
+      uint32_t w[P];
+#pragma unroll
+      for (int wd = 0; wd < P; ++wd) w[wd] = ldg_nc_u32_hint(crow + packed_word(j, gi, wd, G, P), pol_code);
+      float acc = first ? 0.f : srow[j];
+#pragma unroll
+      for (int sl = 0; sl < 32; ++sl) {
+        const uint32_t code = slot_bits<P>(w, sl, 0) & fmask;
+        const int col = (sl + lane) & 31;
+        const int lo = (int)(code & lomask), hi = (int)(code >> Pl);
+#pragma unroll
+        for (int h = 0; h < NHC; ++h)
+          acc = fmaf(wsub[((h * 2) * E + lo) * 32 + col], wsub[((h * 2 + 1) * E + hi) * 32 + col], acc);
+      }
+      if (!last) {
+        srow[j] = acc;
+      } else {
+        const bool ok = j < n && (!mrow || mrow[j]);
+        srow[j] = ok ? vrow[j] * acc : -INFINITY;
+      }
+    }
+  }
+}
+
 // Wide codes with P <= 10: per 32-slot group (= 32 tables, the rotation
 // group), the group-summed tables T_l(r) = sum_h A_h,l(r mod 2^Pl)
 // B_h,l(r >> Pl) are materialized in shared memory ([2^P][32] fp32, <= 128 KB)
@@ -249,8 +319,6 @@ static socket_status launch_score_wide(const socket_cfg& c, const float* lut, co
   const int Lp = code_slots_p(c.L, c.P);
   if (Lp > 64) return fail(SOCKET_EUNSUPPORTED, "score: P > 8 with more than 64 tables");
   const size_t bytes = lut_row_bytes(c);
-  if (bytes > kWideLutMax)
-    return fail(SOCKET_EUNSUPPORTED, "score: P > 8 half-tables of this group size exceed shared memory");
   const int NH = heads_per_row(c);
   const int H_sel = num_sel_rows(c);
   const int G_sel = c.group_mode == SOCKET_GROUP_PER_QHEAD ? c.H_q / c.H_kv : 1;
@@ -277,6 +345,29 @@ static socket_status launch_score_wide(const socket_cfg& c, const float* lut, co
     SK_WIDE2(1, 10) SK_WIDE2(2, 10) SK_WIDE2(4, 10) SK_WIDE2(8, 10)
 #undef SK_WIDE2
     return fail(SOCKET_EUNSUPPORTED, "score: heads per selection row must be 1, 2, 4 or 8");
+  }
+  if (bytes > kWideLutMax) {
+    // tiled over (32-slot group, head chunk): the largest chunk whose sub-image fits
+    int nhc = NH > 4 ? 4 : NH;
+    while (nhc > 1 && (size_t)nhc * 2 * E * 32 * sizeof(float) > kWideLutMax) nhc >>= 1;
+    const size_t sub = (size_t)nhc * 2 * E * 32 * sizeof(float);
+    if (sub > kWideLutMax) return fail(SOCKET_EUNSUPPORTED, "score: P > 8 half-table tile exceeds shared memory");
+#define SK_WIDET(N, PV)                                                                        \
+  if (nhc == N && c.P == PV) {                                                                 \
+    cudaFuncSetAttribute(score_wide_tiled_kernel<N, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub); \
+    score_wide_tiled_kernel<N, PV><<<grid, kWideThreads, sub, st>>>(                           \
+        lut, cw, vnorm, seq_lens, mask, scores, H_sel, c.H_kv, G_sel, c.N_max, Lp, NH, E, row_floats, \
+        c.index_base);                                                                         \
+    return check_launch("score_wide_tiled_kernel");                                            \
+  }
+    SK_WIDET(1, 13) SK_WIDET(2, 13) SK_WIDET(4, 13)
+    SK_WIDET(1, 14) SK_WIDET(2, 14) SK_WIDET(4, 14)
+    SK_WIDET(1, 15) SK_WIDET(2, 15) SK_WIDET(4, 15)
+    SK_WIDET(1, 16) SK_WIDET(2, 16) SK_WIDET(4, 16)
+    SK_WIDET(1, 11) SK_WIDET(2, 11) SK_WIDET(4, 11)
+    SK_WIDET(1, 12) SK_WIDET(2, 12) SK_WIDET(4, 12)
+#undef SK_WIDET
+    return fail(SOCKET_EUNSUPPORTED, "score: wide-code tile shape not instantiated");
   }
 #define SK_WIDE(N, PV)                                                                         \
   if (NH == N && c.P == PV) {                                                                  \

@@ -91,7 +91,11 @@ def test_wide_tables(P, L, mode, tau):
 
 @pytest.mark.parametrize("P,L,mode,lens", [(10, 60, KV_SHARED, [4096, 3000]), (12, 60, PER_QHEAD, [2048, 17]),
                                            (16, 16, PER_QHEAD, [4096, 4096]), (11, 8, KV_SHARED, [100, 4096]),
-                                           (9, 33, PER_QHEAD, [4096, 1000]), (10, 20, KV_SHARED, [0, 4095])])
+                                           (9, 33, PER_QHEAD, [4096, 1000]), (10, 20, KV_SHARED, [0, 4095]),
+                                           # KV_SHARED half-table images beyond shared memory: tiled
+                                           # over (32-slot group, head chunk) with parked partials
+                                           (16, 16, KV_SHARED, [4096, 2000]), (13, 60, KV_SHARED, [4096, 4096]),
+                                           (14, 40, KV_SHARED, [3000, 4096])])
 def test_wide_scores(P, L, mode, lens):
     N = 4096
     cfg, c, W, d = make(2, 8, 2, N, L, P, seed=P * L, mode=mode, lens=lens)
@@ -112,22 +116,13 @@ def test_wide_scores(P, L, mode, lens):
                 assert np.max(rel_err(got[b, r][fin], s[fin])) <= 1e-5
 
 
-def test_wide_unsupported_group_size():
-    # P = 16 with 4 heads per selection row: 4 x 2 x 256 x 64 x 4 B = 512 KB of half-tables
-    cfg, c, W, d = make(1, 8, 2, 256, 16, 16, seed=1, mode=KV_SHARED)
-    codes = ops.alloc_codes(cfg, DEV)
-    vn = torch.ones((1, 2, 256), dtype=torch.float32, device=DEV)
-    with pytest.raises(SocketError) as e:
-        ops.score(cfg, d["q"], d["W"], codes, vn, d["seq_lens"])
-    assert e.value.status == 2
-
-
-@pytest.mark.parametrize("mode", [KV_SHARED, PER_QHEAD])
-def test_wide_decode_step_end_to_end(mode):
-    """RULER-setting step (L = 60, P = 10, 600 bits/token) through SocketDecoder
+@pytest.mark.parametrize("mode,L,P", [(KV_SHARED, 60, 10), (PER_QHEAD, 60, 10), (KV_SHARED, 16, 16)])
+def test_wide_decode_step_end_to_end(mode, L, P):
+    """RULER-setting step (L = 60, P = 10, 600 bits/token) and P = 16 with a
+    group-summed selection (tiled half-tables) through SocketDecoder
     (socket_decode_step): scores, top-k and attention vs the oracle."""
     H_q, H_kv, N, k = 8, 2, 4096, 512
-    cfg, c, W, d = make(1, H_q, H_kv, N, 60, 10, seed=41, mode=mode)
+    cfg, c, W, d = make(1, H_q, H_kv, N, L, P, seed=41, mode=mode)
     dec = SocketDecoder(cfg, d["W"], d["K"], d["V"], k=k)
     assert dec.fused           # socket_decode_step: PDL-chained kernels with the wide score
     dec.prefill()
