@@ -103,6 +103,10 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
   uint32_t* keys = reinterpret_cast<uint32_t*>(fsm + kFZone);
 
   FU_STAMP(0);
+  // cluster barrier phase 1 of 2: every CTA of the cluster must be running before
+  // the LUT columns are pushed into its shared memory (waited for just before
+  // the push, so the table work below hides it)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   // ===== A. tables of my tables + append of the newest key ========================
   const int l0 = c * a.tpc;
   const int ntab = max(0, min(a.tpc, LP - l0));           // my tables (incl. padding ones)
@@ -256,6 +260,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
     FU_STAMP(2);
     // LUT columns of my tables -> every CTA of the cluster.  Column of table l:
     // l (LP >= 32), or l, l + LP, ... < 32 (LP < 32, replicated)
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // every CTA is running
     const int R = 1 << P;
     if (LP >= 32 && (a.tpc & 3) == 0) {
       // task = (LUT row rr, 4-table group): one float4 per destination CTA
