@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
       bool bit = false;
       if (tid < nw) {
         float x = 0.f;
+#pragma unroll 16
         for (int t = 0; t < kD; ++t) x = fmaf(ws[t * kFWs + tid], s_ks[t], x);
         bit = x >= 0.f;                                                  // sign(0) = +1 (R-3)
       }
