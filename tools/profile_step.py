@@ -25,11 +25,13 @@ ap.add_argument("--mode", default="kv_shared")
 ap.add_argument("--dense", action="store_true")
 ap.add_argument("--unfused", action="store_true", help="also run the stage-by-stage step")
 ap.add_argument("--hard", action="store_true", help="hard-LSH tables (Eq. 3)")
+ap.add_argument("--chained", action="store_true", help="never the one-launch kernel (SOCKET_FLAG_CHAINED_STEP)")
 a = ap.parse_args()
 B, N, L = a.batch, a.ctx, a.tables
 k = int(round(N / a.sparsity))
 cfg = Config(B=B, H_q=32, H_kv=8, N_max=N, L=L, P=a.bits, tau=0.5,
-             group_mode=KV_SHARED if a.mode == "kv_shared" else PER_QHEAD, scoring=int(a.hard))
+             group_mode=KV_SHARED if a.mode == "kv_shared" else PER_QHEAD, scoring=int(a.hard),
+             flags=int(a.chained))
 q, K, V = datagen.torch_make_cache(B, 32, 8, N, 128, seed=1)
 W = torch.from_numpy(datagen.make_projections(4242, L, a.bits, 128).view("int16")).cuda().view(torch.bfloat16)
 lens = torch.full((B,), N, dtype=torch.int32, device="cuda")
