@@ -55,10 +55,8 @@ constexpr int kFLutBytes = 256 * 64 * 4;                                   // 64
 constexpr int kFRingBytes = kFWarps * kFScoreStages * TileStage<64>::BYTES; // 68 KB
 constexpr int kFZone = kFLutBytes + kFRingBytes;                          // LUT + score ring
 static_assert(kFZone >= kFAttWarps * kFAttStages * kTileBytes, "attention ring must fit the zone");
-static_assert(128 * 8 * 8 + 128 * 72 * 4 + 8 * (8 * 2 * 8 + 2 * 16 * 8) * 4 <= kFLutBytes &&
-                  128 * 8 * 8 + 128 * 72 * 4 + 4 * (8 * 2 * 16 + 2 * 16 * 16) * 4 <= kFLutBytes,
-              "table staging must fit the LUT region");
-static_assert(8 * 2 * 16 * 64 * 4 <= kFRingBytes, "the gathered half tables must fit the ring region");
+static_assert(128 * 8 * 8 + 128 * 72 * 4 + 8 * (8 * 2 * 16 + 2 * 16 * 16) * 4 <= kFRingBytes,
+              "table staging must fit the ring zone");
 constexpr int kFWs = 72;    // staged W row stride (floats): [t][w]
 constexpr int kFQs = 8;     // staged q row stride (doubles): [t][h]
 
@@ -103,7 +101,6 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
   const int n = a.seq_lens[b];
   float* lut = reinterpret_cast<float*>(fsm);
   uint32_t* keys = reinterpret_cast<uint32_t*>(fsm + kFZone);
-  constexpr int TSW = NH >= 8 ? 8 : 16;          // table stride of the sigma factors / my half tables
 
   FU_STAMP(0);
   // cluster barrier phase 1 of 2: every CTA of the cluster must be running before
@@ -114,15 +111,11 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
   const int l0 = c * a.tpc;
   const int ntab = max(0, min(a.tpc, LP - l0));           // my tables (incl. padding ones)
   const int nw = max(0, min(a.tpc, L - l0)) * P;          // my valid W rows
-  // every CTA's half tables, pushed by their owners: [h][hi][entry][table < 64]
-  // (score-ring region, dead until scoring)
-  float* s_half_all = reinterpret_cast<float*>(fsm + kFLutBytes);
   {
-    // projection staging in the LUT region (the LUT is built after the barrier)
-    double* qs = reinterpret_cast<double*>(fsm);                              // [t][kFQs]
-    float* ws = reinterpret_cast<float*>(fsm + kD * kFQs * 8);               // [t][kFWs]
+    double* qs = reinterpret_cast<double*>(fsm + kFLutBytes);              // [t][kFQs]
+    float* ws = reinterpret_cast<float*>(fsm + kFLutBytes + kD * kFQs * 8);  // [t][kFWs]
     float* s_fx = ws + kD * kFWs;                       // sigma factors [h][bit][c][table]
-    float* s_half = s_fx + NH * 8 * 2 * TSW;             // my half tables [h][hi][entry][table]
+    float* s_half = s_fx + NH * 8 * 2 * 16;             // half tables [h][hi][entry][table]
     const int h0 = g * NH;
     {   // q: 8 (padded) vectors x 16 uint4; W: 64 rows x 16 uint4 -- all loads first
       uint4 vw[2], vq;
@@ -206,8 +199,8 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
               fp = 1.0f / (1.0f + expf(-av));
               fm = 1.0f / (1.0f + expf(av));
             }
-            s_fx[((h * 8 + bit) * 2 + 1) * TSW + tl] = fp;
-            s_fx[((h * 8 + bit) * 2 + 0) * TSW + tl] = fm;
+            s_fx[((h * 8 + bit) * 2 + 1) * 16 + tl] = fp;
+            s_fx[((h * 8 + bit) * 2 + 0) * 16 + tl] = fm;
           }
         }
       }
@@ -225,16 +218,16 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
     }
     __syncthreads();
     // half tables (fp64 products, rounded once): one (h, table, half) per thread
-    if (tid < NH * TSW * 2) {
-      const int hi = tid & 1, tl = (tid >> 1) % TSW, h = (tid >> 1) / TSW;
+    if (tid < NH * 16 * 2) {
+      const int hi = tid & 1, tl = (tid >> 1) & 15, h = tid >> 5;
       if (tl < ntab) {
         double f[4][2];
 #pragma unroll
         for (int bit = 0; bit < 4; ++bit) {
           const int ib = hi * 4 + bit;
           const bool ok = ib < P && (l0 + tl) < L;
-          f[bit][0] = ok ? (double)s_fx[((h * 8 + ib) * 2 + 0) * TSW + tl] : 1.0;
-          f[bit][1] = ok ? (double)s_fx[((h * 8 + ib) * 2 + 1) * TSW + tl] : 1.0;
+          f[bit][0] = ok ? (double)s_fx[((h * 8 + ib) * 2 + 0) * 16 + tl] : 1.0;
+          f[bit][1] = ok ? (double)s_fx[((h * 8 + ib) * 2 + 1) * 16 + tl] : 1.0;
         }
         double p01[4], p012[8];
 #pragma unroll
@@ -242,7 +235,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) p012[e] = p01[e & 3] * f[2][e >> 2];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) s_half[((h * 2 + hi) * 16 + e) * TSW + tl] = (float)(p012[e & 7] * f[3][e >> 3]);
+        for (int e = 0; e < 16; ++e) s_half[((h * 2 + hi) * 16 + e) * 16 + tl] = (float)(p012[e & 7] * f[3][e >> 3]);
       }
     }
     if (app && tid < ntab) {   // code byte of my table tid (padding tables write 0)
@@ -266,62 +259,57 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_step_kernel(FusedArgs a) {
     }
     __syncthreads();
     FU_STAMP(2);
-    // my half tables -> every CTA of the cluster (2 x 16 entries per head and
-    // table: 8x fewer bytes than the LUT columns they expand to)
+    // LUT columns of my tables -> every CTA of the cluster.  Column of table l:
+    // l (LP >= 32), or l, l + LP, ... < 32 (LP < 32, replicated)
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // every CTA is running
-    if ((a.tpc & 3) == 0 && ntab == a.tpc) {
-      const int nq = a.tpc >> 2;                        // float4 per (h, hi, entry)
-      for (int e = tid; e < NH * 2 * 16 * nq * CS; e += kFThreads) {
-        const int r = e % CS, rest = e / CS, q4 = rest % nq, hhe = rest / nq;   // hhe = (h*2+hi)*16 + entry
-        const float4 v = *reinterpret_cast<const float4*>(s_half + hhe * TSW + q4 * 4);
-        *reinterpret_cast<float4*>(cluster.map_shared_rank(s_half_all, r) + hhe * 64 + l0 + q4 * 4) = v;
+    const int R = 1 << P;
+    if (LP >= 32 && (a.tpc & 3) == 0) {
+      // task = (LUT row rr, 4-table group): one float4 per destination CTA
+      const int ng = a.tpc >> 2;
+      for (int e = tid; e < 256 * ng; e += kFThreads) {
+        const int gq = e % ng, rr = e / ng;
+        const int tl = gq * 4, l = l0 + tl;
+        if (l >= LP) continue;
+        float4 T = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (rr < R) {
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            const float4 lo = *reinterpret_cast<const float4*>(s_half + ((h * 2 + 0) * 16 + (rr & 15)) * 16 + tl);
+            const float4 hv = *reinterpret_cast<const float4*>(s_half + ((h * 2 + 1) * 16 + (rr >> 4)) * 16 + tl);
+            T.x = fmaf(lo.x, hv.x, T.x);
+            T.y = fmaf(lo.y, hv.y, T.y);
+            T.z = fmaf(lo.z, hv.z, T.z);
+            T.w = fmaf(lo.w, hv.w, T.w);
+          }
+          if (l + 0 >= L) T.x = 0.f;
+          if (l + 1 >= L) T.y = 0.f;
+          if (l + 2 >= L) T.z = 0.f;
+          if (l + 3 >= L) T.w = 0.f;
+        }
+        for (int r = 0; r < CS; ++r)
+          *reinterpret_cast<float4*>(cluster.map_shared_rank(lut, r) + rr * 64 + l) = T;
       }
-    } else if (ntab > 0) {
-      for (int e = tid; e < NH * 2 * 16 * ntab * CS; e += kFThreads) {
-        const int r = e % CS, rest = e / CS, tl = rest % ntab, hhe = rest / ntab;
-        cluster.map_shared_rank(s_half_all, r)[hhe * 64 + l0 + tl] = s_half[hhe * TSW + tl];
+    } else {
+      for (int e = tid; e < 256 * 16; e += kFThreads) {
+        const int tl = e & 15, rr = e >> 4;
+        if (tl >= ntab) continue;
+        const int l = l0 + tl;
+        float T = 0.f;
+        if (l < L && rr < R) {
+#pragma unroll
+          for (int h = 0; h < NH; ++h) T = fmaf(s_half[((h * 2 + 0) * 16 + (rr & 15)) * 16 + tl], s_half[((h * 2 + 1) * 16 + (rr >> 4)) * 16 + tl], T);
+        }
+        for (int r = 0; r < CS; ++r) {
+          float* rl = cluster.map_shared_rank(lut, r);
+          if (LP >= 32) rl[rr * 64 + l] = T;
+          else for (int cc = l; cc < 32; cc += LP) rl[rr * 64 + cc] = T;
+        }
       }
     }
     __threadfence();   // the appended code / norm before the cluster barrier (release)
   }
   FU_STAMP(3);
   cluster.sync();
-  // the whole LUT image from the gathered half tables: T(rr) = sum_h lo_h(rr & 15)
-  // hi_h(rr >> 4), fp32 fma with h ascending (the chained prologue's arithmetic);
-  // column of table l: l (LP >= 32), or l, l + LP, ... < 32 (LP < 32, replicated)
-  {
-    const int R = 1 << P;
-    constexpr int NQ = (LP + 3) / 4;
-    for (int e = tid; e < 256 * NQ; e += kFThreads) {
-      const int q4 = e % NQ, rr = e / NQ, l = q4 * 4;
-      float4 T = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (rr < R) {
-#pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          const float4 lo = *reinterpret_cast<const float4*>(s_half_all + ((h * 2 + 0) * 16 + (rr & 15)) * 64 + l);
-          const float4 hv = *reinterpret_cast<const float4*>(s_half_all + ((h * 2 + 1) * 16 + (rr >> 4)) * 64 + l);
-          T.x = fmaf(lo.x, hv.x, T.x);
-          T.y = fmaf(lo.y, hv.y, T.y);
-          T.z = fmaf(lo.z, hv.z, T.z);
-          T.w = fmaf(lo.w, hv.w, T.w);
-        }
-        if (l + 0 >= L) T.x = 0.f;
-        if (l + 1 >= L) T.y = 0.f;
-        if (l + 2 >= L) T.z = 0.f;
-        if (l + 3 >= L) T.w = 0.f;
-      }
-      if (LP >= 32) {
-        *reinterpret_cast<float4*>(lut + rr * 64 + l) = T;
-      } else {
-        const float tv[4] = {T.x, T.y, T.z, T.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (l + u < LP)
-            for (int cc = l + u; cc < 32; cc += LP) lut[rr * 64 + cc] = tv[u];
-      }
-    }
-  }
-  __syncthreads();
   FU_STAMP(4);
 
   // ===== B. scores of my slice ======================================================
@@ -616,7 +604,6 @@ static bool fused_geometry(const socket_cfg& c, int& CS, int& S) {
     // top-k state (34 KB) the CTA uses ~200 KB of shared memory
     if (s > 8192 || rows * cs > num_sms()) continue;
     if ((Lp + cs - 1) / cs * c.P > 64) continue;   // <= 64 W rows per CTA (staging, 8 DMMA warps)
-    if ((Lp + cs - 1) / cs > (NH >= 8 ? 8 : 16)) continue;   // tables per CTA <= the staging stride
     CS = cs;
     S = s;
     return true;
