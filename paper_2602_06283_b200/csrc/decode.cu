@@ -87,7 +87,11 @@ static void decode_geometry(const socket_cfg& c, int k, bool dense, int& units, 
   // ~0.86 of one wave at 2 CTAs per SM (256 CTAs on 148 SMs): a single wave of
   // balanced splits was the fastest geometry in tools/tune_step.py sweeps
   // (B 4-16, 5x-10x, 32K)
+#ifdef SK_DECODE_TARGET_PCT   // experiments only (tools/variant_build.py)
+  const int target = num_sms() * SK_DECODE_TARGET_PCT / 100;
+#else
   const int target = num_sms() * 173 / 100;
+#endif
   pick_splits(units, dense ? c.N_max : k, kMmaGran, kMmaMaxRps, target, n_splits, rps);
 }
 

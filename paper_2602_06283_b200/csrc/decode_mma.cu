@@ -16,10 +16,13 @@
 
 namespace sk {
 
-constexpr int kMmaWarps = 4;
+#ifndef SK_DECODE_WARPS
+#define SK_DECODE_WARPS 4   // experiments only (tools/variant_build.py)
+#endif
+constexpr int kMmaWarps = SK_DECODE_WARPS;
 constexpr int kMmaThreads = kMmaWarps * 32;
 #ifndef SK_DECODE_STAGES
-#define SK_DECODE_STAGES 3
+#define SK_DECODE_STAGES 3   // experiments only (tools/variant_build.py)
 #endif
 constexpr int kMmaStages = SK_DECODE_STAGES;   // cp.async ring depth (tiles per warp)
 constexpr int kMmaRing = kMmaWarps * kMmaStages * kTileBytes;   // 96 KB
