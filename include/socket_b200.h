@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define SOCKET_ABI_VERSION 3
+#define SOCKET_ABI_VERSION 4
 
 typedef enum {
   SOCKET_OK = 0,
@@ -86,7 +86,8 @@ typedef struct {
   int32_t N_max;      /* token capacity = row stride of K/V/vnorm/scores; %32 == 0 */
   int32_t L;          /* hash tables, >= 1 (Alg. 1 "#tables L")                    */
   int32_t P;          /* hyperplanes per table, 1..16 (Alg. 1 "#hyperplanes P");    *
-                       * P <= 8: one code byte per table, P = 9..16: one uint16   */
+                       * P <= 8: one code byte per table slot; P = 9..16: P-bit  *
+                       * codes tightly packed (socket_codes_bytes)              */
   float tau;          /* temperature > 0 (Alg. 2)                                  */
   float sm_scale;     /* softmax scale on q.k (reading R-2; usually 1/sqrt(d))     */
   int32_t group_mode; /* socket_group_mode                                         */
@@ -101,9 +102,13 @@ typedef struct {
 
 /* socket_cfg.flags */
 enum {
-  /* socket_decode_step: never use the one-launch cluster kernel, always the
+  /* socket_decode_step: never use the one-launch kernel, always the
    * PDL-chained kernels (both give bit-identical codes, scores and selections) */
-  SOCKET_FLAG_CHAINED_STEP = 1
+  SOCKET_FLAG_CHAINED_STEP = 1,
+  /* socket_decode_step: use the one-launch row-spread kernel whenever the shape
+   * allows it (KV_SHARED, P <= 8, L <= 64, 2 B H_kv <= #SMs), not only for the
+   * small grids where it is the default */
+  SOCKET_FLAG_ONE_LAUNCH = 2
 };
 
 /* ------------------------------------------------------------------------ *
@@ -232,14 +237,20 @@ socket_status socket_score_lut(const socket_cfg* cfg, const void* lut, const uin
  *     otherwise the caller has written row j already;
  *   then scores (Eq. 4 / Alg. 4, written to `scores`), TopK with sink/window
  *   (idx, cnt as socket_topk) and sparse attention (out, lse as
- *   socket_sparse_decode).  Up to 8 selection rows (KV_SHARED, P <= 8) run as
- *   one cluster launch; otherwise 4 launches chained with programmatic
- *   dependent launch.  Requires L <= 64.
+ *   socket_sparse_decode).  Up to 16 selection rows (KV_SHARED, P <= 8, and
+ *   every selection row spread over >= 2 SMs) run as ONE cooperative launch
+ *   over all SMs (the row-spread kernel; SOCKET_FLAG_ONE_LAUNCH: whenever the
+ *   shape allows); otherwise 4 launches chained with programmatic dependent
+ *   launch.  Requires L <= 64.
  *   q, k_new and v_new may be device pointers or pinned, UVA-mapped host
  *   pointers (cudaHostAlloc / cudaHostRegister); out may be either too.  On the
  *   chained path host-resident inputs are first pulled into the workspace by
  *   one copy kernel (a 5th launch); the one-launch kernel reads them in place.
- *   ws: socket_workspace_bytes(cfg, SOCKET_OP_DECODE_STEP, k). */
+ *   ws: socket_workspace_bytes(cfg, SOCKET_OP_DECODE_STEP, k) bytes, ZERO-FILLED
+ *   before its first use with a given cfg (e.g. one cudaMemsetAsync after
+ *   allocation): it holds the one-launch kernel's row barrier counters, which
+ *   every step leaves at zero again.  (A workspace whose counters are not zero
+ *   makes the kernel trap after 2 s instead of hanging.) */
 socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, void* V,
                                  const void* W, uint8_t* codes, float* vnorm,
                                  const int32_t* seq_lens, const uint8_t* mask,
@@ -249,7 +260,7 @@ socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, 
                                  void* ws, size_t ws_bytes, void* stream);
 
 /* Number of kernel launches socket_decode_step issues for cfg with device
- * inputs: 1 (the one-launch cluster kernel, small batches) or 4 (PDL-chained
+ * inputs: 1 (the one-launch row-spread kernel, small batches) or 4 (PDL-chained
  * kernels; 5 when q / k_new / v_new are host-resident); 0 if cfg is invalid. */
 int32_t socket_decode_step_launches(const socket_cfg* cfg);
 

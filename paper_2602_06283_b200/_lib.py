@@ -16,6 +16,7 @@ SOCKET_OK, SOCKET_EINVAL, SOCKET_EUNSUPPORTED, SOCKET_ECUDA, SOCKET_EWORKSPACE =
 GROUP_KV_SHARED, GROUP_PER_QHEAD = 0, 1
 OP_HASH, OP_TABLES, OP_SCORE, OP_TOPK, OP_SPARSE_DECODE, OP_DENSE_DECODE, OP_RESOLVE, OP_DECODE_STEP = range(8)
 FLAG_CHAINED_STEP = 1
+FLAG_ONE_LAUNCH = 2
 MAX_SHARDS = 64
 TOPK_STATE_WORDS = 8
 TOPK_MSG_WORDS = 8 + 2048

@@ -7,7 +7,7 @@
 
 namespace sk {
 
-bool fused_step_applies(const socket_cfg& c);
+bool one_launch_step(const socket_cfg& c);
 
 static thread_local std::string g_last_error;
 
@@ -53,7 +53,7 @@ static socket_status validate(const socket_cfg* c) {
     return fail(SOCKET_EINVAL, "unknown group_mode");
   if (c->scoring != SOCKET_SCORING_SOFT && c->scoring != SOCKET_SCORING_HARD)
     return fail(SOCKET_EINVAL, "unknown scoring");
-  if (c->flags & ~SOCKET_FLAG_CHAINED_STEP) return fail(SOCKET_EINVAL, "unknown flags");
+  if (c->flags & ~(SOCKET_FLAG_CHAINED_STEP | SOCKET_FLAG_ONE_LAUNCH)) return fail(SOCKET_EINVAL, "unknown flags");
   if (c->index_base < 0) return fail(SOCKET_EINVAL, "index_base must be >= 0");
   return SOCKET_OK;
 }
@@ -226,7 +226,7 @@ socket_status socket_decode_step(const socket_cfg* cfg, const void* q, void* K, 
 
 int32_t socket_decode_step_launches(const socket_cfg* cfg) {
   if (validate(cfg) != SOCKET_OK) return 0;
-  return fused_step_applies(*cfg) ? 1 : 4;
+  return one_launch_step(*cfg) ? 1 : 4;
 }
 
 static socket_status check_topk_args(int32_t k, int32_t sink, int32_t window) {

@@ -1,5 +1,5 @@
 // mma.sync / ldmatrix / movmatrix / cp.async helpers of the tensor-core split
-// decode, shared by decode_mma.cu and the fused step (fused.cu).
+// decode, shared by decode_mma.cu and the one-launch step (spread.cu).
 #pragma once
 #include "internal.cuh"
 

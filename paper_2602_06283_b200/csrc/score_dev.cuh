@@ -1,5 +1,5 @@
 // cp.async / mbarrier / bulk-copy helpers and the score kernel's tile staging,
-// shared by the score kernels (tables_score.cu) and the fused step (fused.cu).
+// shared by the score kernels (tables_score.cu) and the one-launch step (spread.cu).
 #pragma once
 #include "step_dev.cuh"
 

@@ -27,13 +27,6 @@ extern "C" int socket_debug_prologue_trace(unsigned long long* host, int n) {
 }
 #endif
 
-bool fused_step_applies(const socket_cfg& c);
-socket_status launch_fused_step(const socket_cfg& c, const void* q, void* K, void* V,
-                                const void* W, uint8_t* codes, float* vnorm, const int32_t* seq_lens,
-                                const uint8_t* mask, int do_append, const void* k_new,
-                                const void* v_new, int k, int sink, int window,
-                                float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
-                                cudaStream_t st);
 socket_status launch_score_pdl(const socket_cfg& c, const float* lut, const uint8_t* codes,
                                const float* vnorm, const int32_t* seq_lens, const uint8_t* mask,
                                float* scores, cudaStream_t st, bool pdl);
@@ -45,6 +38,25 @@ socket_status launch_decode_pdl(const socket_cfg& c, const void* q, const void* 
                                 float* lse, void* ws, size_t ws_bytes, cudaStream_t st, bool pdl,
                                 int** tickets_out, int* n_units);
 size_t decode_workspace_bytes(const socket_cfg& c, int k, bool dense);
+bool spread_geometry(const socket_cfg& c, int& C, int& S);
+size_t spread_workspace_bytes(const socket_cfg& c);
+socket_status launch_spread_step(const socket_cfg& c, const void* q, void* K, void* V,
+                                 const void* W, uint8_t* codes, float* vnorm, const int32_t* seq_lens,
+                                 const uint8_t* mask, int do_append, const void* k_new,
+                                 const void* v_new, int k, int sink, int window,
+                                 float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
+                                 void* ws, cudaStream_t st);
+
+// one-launch row-spread step (spread.cu): by default up to 16 selection rows
+// (measured crossover with the chained kernels, DESIGN 4.5b: -21..24% at B = 2,
+// equal at B = 4); SOCKET_FLAG_ONE_LAUNCH whenever the shape allows
+constexpr int kSpreadMaxRows = 16;
+bool one_launch_step(const socket_cfg& c) {
+  if (c.flags & SOCKET_FLAG_CHAINED_STEP) return false;
+  int C, S;
+  if (!spread_geometry(c, C, S)) return false;
+  return (c.flags & SOCKET_FLAG_ONE_LAUNCH) || (long long)c.B * c.H_kv <= kSpreadMaxRows;
+}
 
 socket_status launch_prologue(const socket_cfg& c, ProArgs a, bool tables, cudaStream_t st) {
   const int NH = c.group_mode == SOCKET_GROUP_PER_QHEAD ? 1 : c.H_q / c.H_kv;
@@ -92,7 +104,9 @@ socket_status launch_prologue(const socket_cfg& c, ProArgs a, bool tables, cudaS
 // kernel pulls them into the workspace before the prologue -- 16-B loads, all in
 // flight at once, so the PCIe reads overlap (a DMA copy of the same 192 KB took
 // ~16 us in tools/e2e_probe3.py).
-static size_t stage_bytes(const socket_cfg& c) {
+size_t stage_bytes(const socket_cfg& c);
+static size_t chained_ws_bytes(const socket_cfg& c, int k);
+size_t stage_bytes(const socket_cfg& c) {
   return (((size_t)c.B * c.H_q * kD + 2 * (size_t)c.B * c.H_kv * kD) * 2 + 255) & ~(size_t)255;
 }
 
@@ -116,14 +130,19 @@ static bool host_resident(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
-size_t decode_step_workspace_bytes(const socket_cfg& c, int k) {
+static size_t chained_ws_bytes(const socket_cfg& c, int k) {
   const size_t lut = ((size_t)c.B * num_sel_rows(c) * lut_row_bytes(c) + 255) & ~(size_t)255;
   return lut + ((decode_workspace_bytes(c, k, false) + 255) & ~(size_t)255) + stage_bytes(c) +
-         topk_workspace_bytes(c);
+         ((topk_workspace_bytes(c) + 255) & ~(size_t)255);
+}
+// [chained-path regions | row-spread control region]; the latter must be zero
+// before the first step (every step leaves it zero) and no other path writes it
+size_t decode_step_workspace_bytes(const socket_cfg& c, int k) {
+  return chained_ws_bytes(c, k) + spread_workspace_bytes(c);
 }
 
 bool decode_step_stages_inputs(const socket_cfg& c, const void* q, const void* k_new, const void* v_new) {
-  return !fused_step_applies(c) && (host_resident(q) || host_resident(k_new) || host_resident(v_new));
+  return !one_launch_step(c) && (host_resident(q) || host_resident(k_new) || host_resident(v_new));
 }
 
 socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, void* V,
@@ -141,10 +160,11 @@ socket_status launch_decode_step(const socket_cfg& c, const void* q, void* K, vo
   const size_t lut_bytes = ((size_t)c.B * H_sel * lut_row_bytes(c) + 255) & ~(size_t)255;
   if (ws_bytes < decode_step_workspace_bytes(c, k))
     return fail(SOCKET_EWORKSPACE, "decode step: workspace too small");
-  // small batch (one cluster per selection row fits one wave): one fused launch
-  if (fused_step_applies(c))
-    return launch_fused_step(c, q, K, V, W, codes, vnorm, seq_lens, mask, do_append, k_new, v_new, k,
-                             sink, window, scores, idx, cnt, out, lse, st);
+  // small batch: one launch over all SMs
+  if (one_launch_step(c))
+    return launch_spread_step(c, q, K, V, W, codes, vnorm, seq_lens, mask, do_append, k_new, v_new, k,
+                              sink, window, scores, idx, cnt, out, lse,
+                              static_cast<char*>(ws) + chained_ws_bytes(c, k), st);
   float* lut = static_cast<float*>(ws);
   void* dws = static_cast<char*>(ws) + lut_bytes;
   const size_t dws_bytes = (decode_workspace_bytes(c, k, false) + 255) & ~(size_t)255;

@@ -1,6 +1,6 @@
 // Device side of the exact cluster top-k (Alg. 3 l.244, PAPER.md; sink/window
-// P:686), shared by topk_cluster_kernel (topk.cu) and the fused small-batch
-// decode step (fused.cu).  Not part of the ABI.
+// P:686), used by topk_cluster_kernel and the sequence-shard protocol kernels
+// (topk.cu).  Not part of the ABI.
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdlib>

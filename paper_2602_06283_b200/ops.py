@@ -34,7 +34,7 @@ class Config:
     group_mode: int = KV_SHARED
     d: int = 128
     scoring: int = 0       # SOCKET_SCORING_SOFT (Eq. 4); 1 = hard LSH collision counts (Eq. 3)
-    flags: int = 0         # SOCKET_FLAG_* (1 = chained decode step, never the one-launch kernel)
+    flags: int = 0         # SOCKET_FLAG_* (1 = chained decode step; 2 = one-launch step whenever it applies)
     index_base: int = 0    # global position of local key 0 (sequence shards)
 
     def c(self) -> SocketCfg:
@@ -88,8 +88,10 @@ def workspace_bytes(cfg: Config, op: int, k: int = 1) -> int:
 
 
 def workspace(cfg: Config, op: int, k: int, device) -> torch.Tensor:
+    """Zero-filled: the decode step's row-spread control words must start at zero
+    (include/socket_b200.h, socket_decode_step)."""
     n = max(16, workspace_bytes(cfg, op, k))
-    return torch.empty(n, dtype=torch.uint8, device=device)
+    return torch.zeros(n, dtype=torch.uint8, device=device)
 
 
 def codes_bytes(cfg: Config) -> int:

@@ -42,7 +42,7 @@ def test_library_is_sm100a(L):
 
 
 def test_version_and_slots(L):
-    assert L.socket_version() == 3
+    assert L.socket_version() == 4
     assert [L.socket_code_slots(x) for x in (0, 1, 8, 9, 16, 17, 32, 33, 60, 64, 65, 128)] == \
         [0, 8, 8, 16, 16, 32, 32, 64, 64, 64, 96, 128]
 

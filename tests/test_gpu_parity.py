@@ -22,6 +22,7 @@ pytestmark = pytest.mark.gpu
 
 ops = pytest.importorskip("paper_2602_06283_b200.ops")
 from paper_2602_06283_b200 import Config, KV_SHARED, PER_QHEAD, SocketDecoder  # noqa: E402
+from paper_2602_06283_b200 import _lib  # noqa: E402
 
 DEV = "cuda"
 
@@ -535,28 +536,41 @@ def test_host_step_graph_matches_device_step(B):
     assert torch.equal(out_h, ob.cpu())
 
 
+def one_vs_chained(cfg, d, k, sink=0, window=0):
+    """(codes, vnorm, scores, idx, cnt, out, lse) of one appended step through the
+    one-launch row-spread kernel (SOCKET_FLAG_ONE_LAUNCH) and through the
+    PDL-chained kernels."""
+    import dataclasses
+    res = []
+    for flags in (_lib.FLAG_ONE_LAUNCH, _lib.FLAG_CHAINED_STEP):
+        cf = dataclasses.replace(cfg, flags=flags)
+        assert ops.decode_step_launches(cf) == (1 if flags == _lib.FLAG_ONE_LAUNCH else 4)
+        dec = SocketDecoder(cf, d["W"], d["K"].clone(), d["V"].clone(), k=k, sink=sink, window=window)
+        dec.prefill()
+        out, lse = dec.step(d["q"], d["seq_lens"], append=True)
+        res.append([t.clone() for t in (dec.codes, dec.vnorm, dec.scores, dec.idx, dec.cnt, out, lse)])
+    return res
+
+
 @pytest.mark.parametrize("B,H_q,H_kv,N,L,lens,scoring,sink,window", [
     (1, 1, 1, 4096, 16, [4096], 0, 0, 0),          # configs[0], NH = 1, Lp = 16 (replicated LUT columns)
     (1, 8, 1, 2048, 8, [1000], 0, 0, 0),           # NH = 8, Lp = 8
     (2, 8, 2, 1024, 33, [1024, 0], 0, 2, 8),       # empty sequence, sink/window, Lp = 64
     (1, 4, 2, 8192, 60, [8190], 1, 0, 0),          # hard-LSH tables, n not a multiple of 32
     (4, 8, 2, 2048, 60, [2048, 1, 700, 2047], 0, 0, 4),
+    (2, 32, 8, 4096, 60, [4096, 3001], 0, 0, 0),   # 16 rows (the default one-launch grid), 9 CTAs per row
+    (4, 32, 8, 2048, 60, [2048, 77, 2000, 1500], 0, 64, 128),   # 32 rows, 4 CTAs per row
+    (1, 32, 8, 16384, 60, [16384], 0, 0, 0),       # 18 CTAs per row (B = 1 production geometry)
 ])
 def test_one_launch_step_matches_chained(B, H_q, H_kv, N, L, lens, scoring, sink, window):
-    """The one-launch cluster step and the PDL-chained kernels agree on every
+    """The one-launch row-spread step and the PDL-chained kernels agree on every
     output: codes, norms, scores and the selection bit for bit, attention to
     fp32 / bf16 rounding."""
     import dataclasses
     cfg, c, W, d = make(B, H_q, H_kv, N, L, 8, seed=61 + L, seq_lens=lens)
     cfg = dataclasses.replace(cfg, scoring=scoring)
     k = max(sink + window, min(N // 8, 512))
-    res = []
-    for no_fused in (False, True):
-        dec = SocketDecoder(chained(cfg, no_fused), d["W"], d["K"].clone(), d["V"].clone(), k=k, sink=sink, window=window)
-        dec.prefill()
-        out, lse = dec.step(d["q"], d["seq_lens"], append=True)
-        res.append([t.clone() for t in (dec.codes, dec.vnorm, dec.scores, dec.idx, dec.cnt, out, lse)])
-    a, b = res
+    a, b = one_vs_chained(cfg, d, k, sink, window)
     for x, y in zip(a[:5], b[:5]):
         assert torch.equal(x, y)
     assert (a[5].float() - b[5].float()).abs().max().item() <= 2e-3
@@ -565,3 +579,35 @@ def test_one_launch_step_matches_chained(B, H_q, H_kv, N, L, lens, scoring, sink
     # the attention weights are rounded to bf16 per tile relative to the running
     # max, which depends on the split: lse agrees within the 1e-3 bar of DESIGN 5
     assert ((a[6][fin] - b[6][fin]).abs() <= 1e-3).all()
+
+
+@pytest.mark.parametrize("case", ["all_tie", "forced_only", "all_valid", "hard_ties"])
+def test_one_launch_selection_modes(case):
+    """The one-launch kernel's top-k branches against the chained kernels and the
+    oracle's TopK on the same fp32 scores: every key tied (refinement levels down
+    to a one-value bin, ties to the smaller index), only forced sink / window keys
+    (k_eff <= #forced), k >= #valid (everything), and hard-LSH collision counts."""
+    import dataclasses
+    B, H_q, H_kv, N = 1, 8, 2, 8192
+    cfg, c, W, d = make(B, H_q, H_kv, N, 60, 8, seed=97)
+    k, sink, window = 1000, 0, 0
+    if case == "all_tie":
+        d["W"] = torch.zeros_like(d["W"])                  # every code 255, uniform tables
+        d["V"] = d["V"][:, :, :1].expand_as(d["V"]).contiguous()   # every norm equal
+    elif case == "forced_only":
+        k, sink, window = 96, 48, 48
+    elif case == "all_valid":
+        d["seq_lens"] = torch.tensor([900], dtype=torch.int32, device=DEV)
+    elif case == "hard_ties":
+        cfg = dataclasses.replace(cfg, scoring=1)
+    a, b = one_vs_chained(cfg, d, k, sink, window)
+    for x, y in zip(a[:5], b[:5]):
+        assert torch.equal(x, y)
+    assert (a[5].float() - b[5].float()).abs().max().item() <= 2e-3
+    n = int(d["seq_lens"][0])
+    for r in range(H_kv):
+        s = a[2][0, r].double().cpu().numpy()
+        ref = O.topk_select(s, k, n, sink=sink, window=window)
+        assert a[3][0, r, :a[4][0, r]].cpu().numpy().tolist() == list(ref)
+    if case == "all_tie":
+        assert a[3][0, 0, :k].cpu().numpy().tolist() == list(range(k))

@@ -109,8 +109,8 @@ def run(B, N, k, L=60, P=8, flags=0, seed=0, lens=None):
 def test_one_launch_step_b1_production(N, sparsity):
     k = int(round(N / sparsity))
     dec, cfg, q, K, V, Wb = run(1, N, k, seed=N, lens=[N - 5])
-    # one launch (8-CTA clusters) up to 8192-key slices; 128K runs the chained kernels
-    assert ops.decode_step_launches(cfg) == (1 if N <= 65536 else 4)
+    # one launch: the row-spread kernel (18 CTAs per row, 1824 .. 7296-key slices)
+    assert ops.decode_step_launches(cfg) == 1
     check_rows(dec, cfg, q, K, V, Wb, N, k, [(0, 0), (0, 5), (0, 7)])
 
 
