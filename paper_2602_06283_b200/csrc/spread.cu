@@ -31,7 +31,8 @@
 // Selection, scores and codes are the same as the multi-kernel path's (same
 // arithmetic, exact top-k); outputs agree to fp32 rounding (the attention is
 // split per CTA slice).  The workspace's row control words must be zero before
-// the first launch; every launch leaves them zero.
+// the first launch; every launch leaves them zero.  The final LSE merge is
+// spread over the row's CTAs after a 4th row barrier (CTA order, deterministic).
 #include <algorithm>
 
 #include "mma_dev.cuh"
@@ -40,16 +41,16 @@
 namespace sk {
 
 #ifdef SK_TRACE
-static __device__ unsigned long long g_spread_trace[4096 * 24];
+static __device__ unsigned long long g_spread_trace[4096 * 32];
 #define SP_STAMP(i)                                                                       \
   do {                                                                                    \
     if (threadIdx.x == 0) {                                                               \
       const int cta = blockIdx.y * gridDim.x + blockIdx.x;                                \
-      if (cta < 4096) g_spread_trace[cta * 24 + (i)] = clock64();                         \
-      if ((i) == 0 && cta < 4096) {                                                       \
+      if (cta < 4096) g_spread_trace[cta * 32 + (i)] = clock64();                         \
+      if (((i) == 0 || (i) == 10) && cta < 4096) {                                        \
         unsigned long long gt;                                                            \
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));                            \
-        g_spread_trace[cta * 24 + 23] = gt;                                               \
+        g_spread_trace[cta * 32 + ((i) == 0 ? 23 : 24)] = gt;                             \
       }                                                                                   \
     }                                                                                     \
   } while (0)
@@ -937,7 +938,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) spread_step_kernel(SpreadArgs a
     __syncthreads();
     SP_STAMP(19);
 #ifdef SK_TRACE
-    if (tid == 0) g_spread_trace[(blockIdx.y * gridDim.x + blockIdx.x) * 24 + 21] = Ct;
+    if (tid == 0) g_spread_trace[(blockIdx.y * gridDim.x + blockIdx.x) * 32 + 21] = Ct;
 #endif
     if (list) {
       // T = the nd-th largest candidate: rank counting (small) or a 4-digit radix
@@ -1210,63 +1211,58 @@ __global__ void __launch_bounds__(kSpThreads, 1) spread_step_kernel(SpreadArgs a
       __stcg(mypart + x, val);
     }
   }
-  // ---- the last CTA of the row merges the C partials -------------------------------
-  __syncthreads();
+  // ---- LSE merge of the row's C partials, spread over the CTAs -------------------------
+  // after a row barrier CTA c merges output elements [c per, (c + 1) per) of the
+  // row's NH (kD + 1) (o and lse), each over the C partials in CTA order
+  // (deterministic); the exit ticket's last CTA resets the row's counters
   SP_STAMP(13);
-  if (tid == 0) {
-    __threadfence();
-    s_dec[0] = atomicAdd(bar + 1, 1u);
-    __threadfence();
-  }
-  __syncthreads();
+  sp_arrive(bar);
+  sp_wait(bar, (++nb) * C);
   SP_STAMP(14);
-  if (s_dec[0] == (uint32_t)(C - 1)) {   // (thread 0's atomic was preceded by its fence)
-    const int tot = C * NH * (kD + 2);
-    const bool staged = (size_t)tot * 4 <= (size_t)a.zone;
-    float* pc = reinterpret_cast<float*>(smem);                   // [C][NH][kD + 2] (zone is dead)
-    if (staged) {   // 8 loads in flight per thread
-      const float2* g2 = reinterpret_cast<const float2*>(gpart);
-      float2* p2 = reinterpret_cast<float2*>(pc);
-      for (int x0 = 0; x0 < tot / 2; x0 += 8 * kSpThreads) {
-        float2 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int x = x0 + u * kSpThreads + tid;
-          if (x < tot / 2) v[u] = __ldcg(g2 + x);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int x = x0 + u * kSpThreads + tid;
-          if (x < tot / 2) p2[x] = v[u];
-        }
-      }
-    } else {   // only the maxima, compactly: pc[r * NH + h]
-      for (int x = tid; x < C * NH; x += kSpThreads) pc[x] = __ldcg(gpart + (size_t)x * (kD + 2));
-    }
-    __syncthreads();
-    SP_STAMP(22);
-    const float* src = staged ? pc : gpart;
+  {
     constexpr float kLn2 = 0.6931471805599453f;
-    for (int x = tid; x < NH * (kD + 1); x += kSpThreads) {
+    const int tot_el = NH * (kD + 1);
+    const int per = (tot_el + C - 1) / C;
+    for (int x = c * per + tid; x < min(tot_el, (c + 1) * per); x += kSpThreads) {
       const int h = x / (kD + 1), e = x % (kD + 1);
+      const float* ph = gpart + (size_t)h * (kD + 2);
+      constexpr int kB = 8;   // partials in flight per thread
       float M = -INFINITY;
-      const int mstride = staged ? kD + 2 : 1;
-      for (int r = 0; r < C; ++r) M = fmaxf(M, pc[(r * NH + h) * mstride]);
+      for (int r0 = 0; r0 < C; r0 += kB) {
+        float mv[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) mv[u] = r0 + u < C ? __ldcg(ph + (size_t)(r0 + u) * NH * (kD + 2)) : -INFINITY;
+#pragma unroll
+        for (int u = 0; u < kB; ++u) M = fmaxf(M, mv[u]);
+      }
       float Ls = 0.f, O = 0.f;
       if (M != -INFINITY) {
-#pragma unroll 4
-        for (int r = 0; r < C; ++r) {
-          const float* pr = src + (size_t)(r * NH + h) * (kD + 2);
-          const float wt = exp2f(pc[(r * NH + h) * mstride] - M);
-          Ls = fmaf(wt, staged ? pr[1] : __ldcg(pr + 1), Ls);
-          if (e < kD) O = fmaf(wt, staged ? pr[2 + e] : __ldcg(pr + 2 + e), O);
+        for (int r0 = 0; r0 < C; r0 += kB) {
+          float mv[kB], lv[kB], ov[kB];
+#pragma unroll
+          for (int u = 0; u < kB; ++u) {
+            const float* pr = ph + (size_t)(r0 + u) * NH * (kD + 2);
+            const bool v = r0 + u < C;
+            mv[u] = v ? __ldcg(pr) : -INFINITY;
+            lv[u] = v ? __ldcg(pr + 1) : 0.f;
+            ov[u] = v && e < kD ? __ldcg(pr + 2 + e) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < kB; ++u) {
+            const float wt = mv[u] == -INFINITY ? 0.f : exp2f(mv[u] - M);
+            Ls = fmaf(wt, lv[u], Ls);
+            O = fmaf(wt, ov[u], O);
+          }
         }
       }
       const size_t oh = (size_t)b * a.H_q + h0 + h;
       if (e < kD) a.out[oh * kD + e] = (uint16_t)f2bf_bits(Ls > 0.f ? O / Ls : 0.f);
       else if (a.lse) a.lse[oh] = Ls > 0.f ? (M + log2f(Ls)) * kLn2 : -INFINITY;
     }
-    if (tid == 0) { bar[0] = 0u; bar[1] = 0u; }   // every CTA of the row is past its last barrier
+  }
+  __syncthreads();
+  if (tid == 0) {   // exit ticket: every CTA of the row is past its last barrier wait
+    if (atomicAdd(bar + 1, 1u) == (uint32_t)(C - 1)) { bar[0] = 0u; bar[1] = 0u; }
   }
   SP_STAMP(10);
 }
@@ -1363,7 +1359,7 @@ socket_status launch_spread_step(const socket_cfg& c, const void* q, void* K, vo
   attr[0].id = cudaLaunchAttributeCooperative;   // every CTA co-resident (row barriers)
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1;   // (measured: no launch-latency cost over a plain launch)
   cudaError_t e = cudaSuccess;
 #define SK_SPREAD(N, LPV)                                                                         \
   if (NH == N && Lp == LPV) {                                                                     \

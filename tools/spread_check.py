@@ -83,7 +83,10 @@ def main():
     ap.add_argument("--modes", default="spread,chained")
     ap.add_argument("--edge", action="store_true", help="ragged / sink-window / hard cases first")
     ap.add_argument("--noflush", action="store_true", help="no L2 flush between timed replays")
+    ap.add_argument("--lib", default=None, help="an experiment build (tools/variant_build.py)")
     a = ap.parse_args()
+    if a.lib:
+        _lib.LIB_PATH = a.lib
     flush = torch.empty(256 << 20 if not a.noflush else 16, dtype=torch.uint8, device="cuda")
     modes = a.modes.split(",")
     if a.edge:

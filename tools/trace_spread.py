@@ -41,15 +41,24 @@ def main():
             dec = SocketDecoder(cfg, W, K, V, k=int(round(N / a.sparsity)))
             dec.prefill()
             flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-            for _ in range(3):
+            dec.capture(q, lens, append=True)
+            ev = []
+            for _ in range(5):
                 flush.zero_()
-                dec.step(q, lens, append=True)
-            torch.cuda.synchronize()
-            buf = (ctypes.c_ulonglong * (4096 * 24))()
-            assert L.socket_debug_spread_trace(buf, 4096 * 24) == 0
-            t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 24).astype(np.int64)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                dec.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                ev.append(e0.elapsed_time(e1) * 1e3)
+            buf = (ctypes.c_ulonglong * (4096 * 32))()
+            assert L.socket_debug_spread_trace(buf, 4096 * 32) == 0
+            t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 32).astype(np.int64)
             t = t[t[:, 0] != 0]
             gt = t[:, 23]
+            ge = t[:, 24]
+            print(f"   last replay: CUDA events {ev[-1]:.1f} us, in-kernel span (first CTA start -> last CTA end, "
+                  f"globaltimer) {(ge.max() - gt.min()) / 1e3:.1f} us")
             print(f"B={B} N={N}: {len(t)} CTAs, start skew (globaltimer) {(gt.max() - gt.min()) / 1e3:.2f} us; "
                   f"total cycles median {np.median(t[:, 10] - t[:, 0]):.0f} max {np.max(t[:, 10] - t[:, 0]):.0f}")
             ct = t[:, 21]
