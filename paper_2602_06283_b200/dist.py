@@ -42,6 +42,7 @@ from dataclasses import replace
 import torch
 import torch.distributed as dist
 
+from . import _lib
 from .ops import Config
 
 MAX_WINDOW_ROUNDS = 3     # 2048-bin histograms take any 32-bit bracket to one key value
@@ -117,6 +118,9 @@ class SeqShard:
         self.cnt = torch.empty((cfg.B, cfg.H_sel), dtype=torch.int32, device=dev)
         self.part = torch.empty((cfg.B, cfg.H_q, cfg.d + 2), dtype=torch.float32, device=dev)
         self.state = None
+        # window message buffer, zero-filled once: the kernel writes only the
+        # header and the wc entries the resolve reads; the tail is all-gathered too
+        self.msg = torch.zeros((cfg.B, cfg.H_sel, _lib.TOPK_MSG_WORDS), dtype=torch.int32, device=dev)
 
     def prefill(self, n_tokens=None):
         n = self.cfg.N_max if n_tokens is None else n_tokens
@@ -134,7 +138,7 @@ class SeqShard:
 
     def window_msg(self, seq_lens):
         return self.ops.topk_window(self.cfg, self.scores, seq_lens, self.state, sink=self.sink,
-                                    window=self.window)
+                                    window=self.window, msg=self.msg)
 
     def resolve(self, all_msgs):
         self.ops.topk_resolve(self.cfg, all_msgs, self.rank, self.state)

@@ -7,8 +7,9 @@ Covers: the tcgen05 prefill hash and the CUDA-core hash, code pack/unpack,
 query tables (plain + LUT), the byte-code and wide-code score kernels, top-k
 (cluster select, sink/window, ties), the sequence-shard protocol (digest,
 bracket, window, resolve, emit), sparse / dense decode, the LSE combine, the
-sampling decode, and socket_decode_step on both the one-launch cluster kernel
-and the PDL-chained kernels (device and pinned-host inputs).
+sampling decode, and socket_decode_step on both the one-launch row-spread
+kernel (incl. all-tied keys, forced-only selection, 4 CTAs per row) and the
+PDL-chained kernels (device and pinned-host inputs).
 """
 import dataclasses
 import os
@@ -75,6 +76,20 @@ def main():
         kn = torch.randn((B, Hkv, 128), device=dev).to(torch.bfloat16)
         dec.step(q.cpu().pin_memory(), lens, append=True, k_new=kn.cpu().pin_memory(),
                  v_new=kn.cpu().pin_memory())
+    # one-launch row-spread kernel: every key tied (refinement levels, one-value bin),
+    # forced-only selection, and 32 rows (4 CTAs per row, SOCKET_FLAG_ONE_LAUNCH)
+    Vt = V[:, :, :1].expand_as(V).contiguous()
+    dec = SocketDecoder(cfg, torch.zeros_like(W), K.clone(), Vt, k=k)
+    dec.prefill()
+    dec.step(q, lens, append=True)
+    dec = SocketDecoder(cfg, W, K.clone(), V.clone(), k=8, sink=4, window=4)
+    dec.prefill()
+    dec.step(q, lens, append=True)
+    c4 = datagen.make_case(4, 32, 8, 1024, 128, seed=5, seq_lens=[1024, 77, 1000, 512])
+    c4cfg = Config(B=4, H_q=32, H_kv=8, N_max=1024, L=L, P=8, flags=2)
+    dec = SocketDecoder(c4cfg, W, bits(c4["K"]), bits(c4["V"]), k=100, sink=3, window=5)
+    dec.prefill()
+    dec.step(bits(c4["q"]), torch.from_numpy(c4["seq_lens"]).to(dev), append=True)
     # sequence-shard protocol on 4 virtual shards (ties)
     vs = VirtualShards(cfg, W, K, V, k, 4, sink=1, window=2)
     vs.prefill()
