@@ -105,7 +105,8 @@ hash_keys_tc2_kernel(const __grid_constant__ CUtensorMap tmK, const uint16_t* __
   constexpr int NSLOT = 512 / MMA_N;               // TMEM chunk slots
   constexpr uint32_t W_BYTES = NC * kTcK * 2;
   constexpr uint32_t A_BYTES = kTcM * kTcK * 2;    // 32 KB
-  constexpr uint32_t STG_BYTES = kTcM * LP;
+  constexpr int RS = LP / 4 + 1;                   // staging row stride (u32 words, odd: conflict-free)
+  constexpr uint32_t STG_BYTES = kTcM * RS * 4;
   constexpr int CB = LP < 16 ? LP : 16;
   constexpr int NCH = LP / CB;
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MMA_N >> 3) << 17) |
@@ -113,7 +114,7 @@ hash_keys_tc2_kernel(const __grid_constant__ CUtensorMap tmK, const uint16_t* __
   extern __shared__ __align__(1024) char smem[];
   char* sW = smem;
   char* sA = smem + W_BYTES;                       // 2 stages
-  uint8_t* stage = reinterpret_cast<uint8_t*>(smem + W_BYTES + 2 * A_BYTES);   // 2 x STG_BYTES
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smem + W_BYTES + 2 * A_BYTES);   // 2 x [kTcM][RS] words
   __shared__ uint64_t full_A[2], empty_A[2], full_T[NSLOT], empty_T[NSLOT];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -202,8 +203,7 @@ hash_keys_tc2_kernel(const __grid_constant__ CUtensorMap tmK, const uint16_t* __
     int it = 0, c = 0;
     for (long long t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       const int bh = (int)(t / tiles_in_range), tile = t_lo + (int)(t % tiles_in_range);
-      const int j = tile * kTcM + r;
-      uint8_t* stg = stage + (it & 1) * STG_BYTES;
+      uint32_t* stg = stage + (it & 1) * (STG_BYTES / 4);
       for (int h = 0; h < NCHK; ++h, ++c) {
         const int slot = c % NSLOT, use = c / NSLOT;
         tc_mbar_wait(&full_T[slot], use & 1);
@@ -224,21 +224,16 @@ hash_keys_tc2_kernel(const __grid_constant__ CUtensorMap tmK, const uint16_t* __
                 "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
               : "r"(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(slot * MMA_N + col)));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          const uint32_t pmask = (1u << P) - 1u;
           // 32 sign bits with one funnel shift per column (column c lands in bit
-          // 31 - c), inverted (bit = x >= 0) and bit-reversed: byte qq = table qq
+          // 31 - c), inverted (bit = x >= 0) and bit-reversed: byte qq = the code
+          // of table lb + qq (bit i = (x_i >= 0), i < P; padding tables >= L -> 0),
+          // staged as one word in TABLE order (the copy-out applies the slot rotation)
           uint32_t sg = 0;
 #pragma unroll
           for (int c = 0; c < 32; ++c) sg = __funnelshift_l(v[c], sg, 1);
-          const uint32_t bits = __brev(~sg);
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            const int l = (h * MMA_N + col) / 8 + qq;
-            uint32_t code = (bits >> (8 * qq)) & pmask;          // bit i = (x_i >= 0), i < P
-            if (l >= L) code = 0;
-            const int sl = (l & ~MM) | ((l - j) & MM);           // slot of table l for key j
-            stg[((r >> 5) * NCH + sl / CB) * (32 * CB) + (r & 31) * CB + (sl % CB)] = (uint8_t)code;
-          }
+          const int lb = (h * MMA_N + col) / 8;
+          const uint32_t lmask = lb + 4 <= L ? 0xFFFFFFFFu : (lb >= L ? 0u : (0xFFFFFFFFu >> (8 * (lb + 4 - L))));
+          stg[r * RS + (lb >> 2)] = __brev(~sg) & (((1u << P) - 1u) * 0x01010101u) & lmask;
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
@@ -251,8 +246,20 @@ hash_keys_tc2_kernel(const __grid_constant__ CUtensorMap tmK, const uint16_t* __
         const int jj = tile * kTcM + rr;
         if (jj < n_begin || jj >= n_end) continue;
         const int off = ((rr >> 5) * NCH + ch) * (32 * CB) + (rr & 31) * CB;
-        if constexpr (CB == 16) *reinterpret_cast<uint4*>(cbase + off) = *reinterpret_cast<const uint4*>(stg + off);
-        else *reinterpret_cast<uint2*>(cbase + off) = *reinterpret_cast<const uint2*>(stg + off);
+        // slot s of key jj holds table (s & ~MM) | ((s + jj) & MM): output word w =
+        // 4 consecutive tables of the row's group, a funnel shift of 2 staged words
+        const uint32_t* srow = stg + rr * RS;
+        uint32_t o[CB / 4];
+#pragma unroll
+        for (int w = 0; w < CB / 4; ++w) {
+          const int s0 = ch * CB + 4 * w;
+          const int gb = (s0 & ~MM) >> 2;                        // group base (words)
+          const int bq = (s0 + rr) & MM;                         // first table of the word (tile*128 = 0 mod 32)
+          const uint32_t lo = srow[gb + (bq >> 2)], hi = srow[gb + (((bq >> 2) + 1) & (MM >> 2))];
+          o[w] = __funnelshift_r(lo, hi, 8 * (bq & 3));
+        }
+        if constexpr (CB == 16) *reinterpret_cast<uint4*>(cbase + off) = make_uint4(o[0], o[1], o[2], o[3]);
+        else *reinterpret_cast<uint2*>(cbase + off) = make_uint2(o[0], o[1]);
       }
     }
   }
@@ -299,7 +306,7 @@ static socket_status launch_hash_keys_tc2(const socket_cfg& c, const void* K, co
   const int t_lo = n_begin / kTcM, t_hi = (n_begin + n_count - 1) / kTcM;
   const long long total = (long long)c.B * c.H_kv * (t_hi - t_lo + 1);
   const int grid = (int)(total < num_sms() ? total : num_sms());
-  const size_t smem = (size_t)NC * kTcK * 2 + 2 * (size_t)kTcM * kTcK * 2 + 2 * (size_t)kTcM * Lp;
+  const size_t smem = (size_t)NC * kTcK * 2 + 2 * (size_t)kTcM * kTcK * 2 + 2 * (size_t)kTcM * (Lp / 4 + 1) * 4;
 #define SK_TC2(NCV)                                                                                 \
   case NCV: {                                                                                       \
     cudaFuncSetAttribute(hash_keys_tc2_kernel<NCV>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
