@@ -248,7 +248,7 @@ def run_reference(a):
             "extrapolated": cb["extrapolated"], "units_timed_per_step": cb["units_timed_per_step"],
             "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit_line(line)
 
 
 # ---------------------------------------------------------------------------
@@ -363,7 +363,7 @@ def run_ours(a):
     try:
         line = run_seq(a, ctx) if a.layout == "seq" else run_heads(a, ctx)
         if ctx.rank == 0:
-            print(json.dumps(line), flush=True)
+            emit_line(line)
     finally:
         torch.cuda.synchronize()
         ctx.close()
@@ -814,7 +814,24 @@ def end_to_end(a, cfg, dec, q, K, V, lens, N, flush, stream, dev):
     return {"ms": ms, "h2d": h2d, "d2h": out_h.numel() * 2}
 
 
+_JSON_OUT = None
+
+
+def emit_line(line):
+    """The one JSON line on stdout (every other print, including the C
+    libraries' -- e.g. NCCL's version banner -- goes to stderr, see main)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # stdout carries exactly one JSON line: keep a private handle on it and send
+    # file descriptor 1 (Python prints and native libraries alike) to stderr
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     a = parse()
     if a.impl == "reference":
         run_reference(a)

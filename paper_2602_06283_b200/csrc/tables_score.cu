@@ -203,6 +203,7 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint32_t* __restrict__
   float* tab = w2;                          // [R][32]
   const char* tabc = reinterpret_cast<const char*>(w2);
   float* ast = tab + R * 32;                // [NH][RL][32] staged A half-tables of the group
+  float* bst = ast + NH * RL * 32;          // [NH][EH][32] staged B half-tables of the group
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lane4 = 4u * lane;
   const uint64_t pol_code = l2_policy_evict_first(), pol_score = l2_policy_evict_last();
@@ -228,22 +229,45 @@ score_wide2_kernel(const float* __restrict__ lut_g, const uint32_t* __restrict__
     const int vt1 = min(t1, (n + 31) >> 5);   // tiles with valid keys
     for (int gi = 0; gi < groups; ++gi) {
       if (t0 >= vt1) break;
-      __syncthreads();                        // previous sweep done with tab / ast
-      for (int e = tid; e < NH * RL * 32; e += kWideThreads) {
-        const int col = e & 31, lo = (e >> 5) % RL, h = e / (32 * RL);
-        ast[e] = img[((h * 2 + 0) * E + lo) * 64 + gi * 32 + col];
+      __syncthreads();                        // previous sweep done with tab / ast / bst
+      // stage the group's A and B half-tables (float4 loads, all in flight)
+      for (int e4 = tid; e4 < NH * (RL + EH) * 8; e4 += kWideThreads) {
+        const int c4 = e4 & 7, ent = (e4 >> 3) % (RL + EH), h = e4 / (8 * (RL + EH));
+        const bool hiv = ent >= RL;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(
+            img + ((h * 2 + (hiv ? 1 : 0)) * E + (hiv ? ent - RL : ent)) * 64 + gi * 32) + c4);
+        float* dst = hiv ? bst + (h * EH + ent - RL) * 32 : ast + (h * RL + ent) * 32;
+        reinterpret_cast<float4*>(dst)[c4] = v;
       }
       __syncthreads();
-      for (int task = tid; task < 32 * EH; task += kWideThreads) {
-        const int col = task & 31, hi = task >> 5;
-        float bh[NH];
+      // T_l(hi, lo) = sum_h A_h(lo) B_h(hi) (fp32 fma, h ascending): thread = (column,
+      // 8-row block of lo, block of hi), its A / B values in registers
+      {
+        constexpr int BL = RL >= 8 ? 8 : RL;              // lo rows per thread
+        constexpr int NBL = RL / BL;                      // lo blocks
+        constexpr int NBH = kWideThreads / 32 / NBL;      // hi blocks over the 16 warps
+        const int col = tid & 31, blo = (tid >> 5) % NBL, bhb = (tid >> 5) / NBL;
+        const int hb1 = min(EH, (bhb + 1) * ((EH + NBH - 1) / NBH));
+        for (int hb = bhb * ((EH + NBH - 1) / NBH); hb < hb1; hb += 8) {
+          const int nh8 = min(8, hb1 - hb);
+          float av[NH][BL];
 #pragma unroll
-        for (int h = 0; h < NH; ++h) bh[h] = img[((h * 2 + 1) * E + hi) * 64 + gi * 32 + col];
-        for (int lo = 0; lo < RL; ++lo) {
-          float T = 0.f;
+          for (int h = 0; h < NH; ++h)
 #pragma unroll
-          for (int h = 0; h < NH; ++h) T = fmaf(ast[(h * RL + lo) * 32 + col], bh[h], T);
-          tab[(hi * RL + lo) * 32 + col] = T;
+            for (int u = 0; u < BL; ++u) av[h][u] = ast[(h * RL + blo * BL + u) * 32 + col];
+          for (int v8 = 0; v8 < nh8; ++v8) {
+            const int hi = hb + v8;
+            float bv[NH];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) bv[h] = bst[(h * EH + hi) * 32 + col];
+#pragma unroll
+            for (int u = 0; u < BL; ++u) {
+              float T = 0.f;
+#pragma unroll
+              for (int h = 0; h < NH; ++h) T = fmaf(av[h][u], bv[h], T);
+              tab[(hi * RL + blo * BL + u) * 32 + col] = T;
+            }
+          }
         }
       }
       __syncthreads();
@@ -330,7 +354,7 @@ static socket_status launch_score_wide(const socket_cfg& c, const float* lut, co
   if (c.P <= 10) {
     // group-summed tables per 32-slot group (one LDS per lookup)
     const int R = 1 << c.P, RL = 1 << (c.P / 2);
-    const size_t sm2 = ((size_t)R * 32 + (size_t)NH * RL * 32) * sizeof(float);
+    const size_t sm2 = ((size_t)R * 32 + (size_t)NH * (RL + R / RL) * 32) * sizeof(float);   // tab + A + B
     const long long total_tiles = (long long)c.B * H_sel * (c.N_max / 32);
     const unsigned pgrid = (unsigned)(total_tiles < num_sms() ? total_tiles : num_sms());
 #define SK_WIDE2(N, PV)                                                                        \
