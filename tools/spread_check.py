@@ -21,7 +21,9 @@ from paper_2602_06283_b200 import Config, SocketDecoder, _lib  # noqa: E402
 MODES = {"spread": _lib.FLAG_ONE_LAUNCH, "chained": _lib.FLAG_CHAINED_STEP}
 
 
-def timed(fn, flush, reps=30):
+def timed(fn, flush, reps=60):
+    """Mean of reps CUDA-event timings (events tick in ~2 us quanta on this part:
+    the mean resolves below a quantum, the median does not)."""
     ts = []
     for i in range(reps + 3):
         flush.zero_()
@@ -32,8 +34,7 @@ def timed(fn, flush, reps=30):
         e1.synchronize()
         if i >= 3:
             ts.append(e0.elapsed_time(e1))
-    ts.sort()
-    return ts[len(ts) // 2] * 1e3
+    return sum(ts) / len(ts) * 1e3
 
 
 def run(B, N, sp, flush, modes, ragged=False, sink=0, window=0, hard=False, time_it=True):
