@@ -303,45 +303,54 @@ __device__ __forceinline__ void tables_tile(const ProArgs& a, int qt, int wt, ch
   // LUT row rr, 4-table group), one float4 store of 4 consecutive columns
   constexpr int kRows = kTQ / NH;
   const int panels = a.Lp <= 64 ? 1 : (a.Lp + 63) / 64;
-  for (int task = tid; task < kRows * 256 * 2; task += kPT) {
-    const int g4 = task & 1, rr = (task >> 1) & 255, srow = task >> 9;
+  // task = (selection row, 4-row quarter lq of the 16 low-half entries, high-half
+  // entry hi, table group g4): its 4 LUT rows rr = 16 hi + 4 lq + u share the hi
+  // factors (one 16-B load per head) and a warp's lo loads are broadcasts
+  for (int task = tid; task < kRows * 4 * 16 * 2; task += kPT) {
+    const int g4 = task & 1, hi = (task >> 1) & 15, lq = (task >> 5) & 3, srow = task >> 7;
     const int row = qv0 / NH + srow;
     const int lb = l0 + 4 * g4;
     if (qv0 + srow * NH >= nqv || lb >= a.Lp) continue;
-    float4 T = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (rr < R) {
+    float4 hv[NH];
 #pragma unroll
-      for (int h = 0; h < NH; ++h) {
-        const int m = srow * NH + h;
-        const float4 lo = *reinterpret_cast<const float4*>(half + ((m * 2 + 0) * 16 + (rr & 15)) * kTT + 4 * g4);
-        const float4 hv = *reinterpret_cast<const float4*>(half + ((m * 2 + 1) * 16 + (rr >> 4)) * kTT + 4 * g4);
-        T.x = fmaf(lo.x, hv.x, T.x);
-        T.y = fmaf(lo.y, hv.y, T.y);
-        T.z = fmaf(lo.z, hv.z, T.z);
-        T.w = fmaf(lo.w, hv.w, T.w);
+    for (int h = 0; h < NH; ++h)
+      hv[h] = *reinterpret_cast<const float4*>(half + (((srow * NH + h) * 2 + 1) * 16 + hi) * kTT + 4 * g4);
+    float* lrow = a.lut ? a.lut + (size_t)row * panels * (256 * 64) : nullptr;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int rr = hi * 16 + lq * 4 + u;
+      float4 T = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (rr < R) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const float4 lo = *reinterpret_cast<const float4*>(half + (((srow * NH + h) * 2 + 0) * 16 + (rr & 15)) * kTT + 4 * g4);
+          T.x = fmaf(lo.x, hv[h].x, T.x);
+          T.y = fmaf(lo.y, hv[h].y, T.y);
+          T.z = fmaf(lo.z, hv[h].z, T.z);
+          T.w = fmaf(lo.w, hv[h].w, T.w);
+        }
+        // tables >= L are padding: 0
+        if (lb + 0 >= L) T.x = 0.f;
+        if (lb + 1 >= L) T.y = 0.f;
+        if (lb + 2 >= L) T.z = 0.f;
+        if (lb + 3 >= L) T.w = 0.f;
+        if (a.plain) {
+          const float tv[4] = {T.x, T.y, T.z, T.w};
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            if (lb + v < L) a.plain[((size_t)row * L + lb + v) * R + rr] = tv[v];
+        }
       }
-      // tables >= L are padding: 0
-      if (lb + 0 >= L) T.x = 0.f;
-      if (lb + 1 >= L) T.y = 0.f;
-      if (lb + 2 >= L) T.z = 0.f;
-      if (lb + 3 >= L) T.w = 0.f;
-      if (a.plain) {
-        const float tv[4] = {T.x, T.y, T.z, T.w};
+      if (lrow) {
+        if (a.Lp >= 32) {
+          *reinterpret_cast<float4*>(lrow + (size_t)(lb >> 6) * (256 * 64) + rr * 64 + (lb & 63)) = T;
+        } else {
+          const float tv[4] = {T.x, T.y, T.z, T.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (lb + u < L) a.plain[((size_t)row * L + lb + u) * R + rr] = tv[u];
-      }
-    }
-    if (a.lut) {
-      float* lrow = a.lut + (size_t)row * panels * (256 * 64);
-      if (a.Lp >= 32) {
-        *reinterpret_cast<float4*>(lrow + (size_t)(lb >> 6) * (256 * 64) + rr * 64 + (lb & 63)) = T;
-      } else {
-        const float tv[4] = {T.x, T.y, T.z, T.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (lb + u < a.Lp)
-            for (int cc = lb + u; cc < 32; cc += a.Lp) lrow[rr * 64 + cc] = tv[u];
+          for (int v = 0; v < 4; ++v)
+            if (lb + v < a.Lp)
+              for (int cc = lb + v; cc < 32; cc += a.Lp) lrow[rr * 64 + cc] = tv[v];
+        }
       }
     }
   }
