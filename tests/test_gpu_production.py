@@ -3,9 +3,9 @@ times), sampled rows against the float64 oracle at the north-star tolerances
 (scores 1e-5 relative, selection identical except documented near-ties,
 outputs 2e-3 absolute, lse 1e-3):
 
-  * the decode step at B = 1 (32 q / 8 kv heads) for 32K, 64K and
-    128K context (4096 / 8192-key CTA slices of 8-CTA clusters) and the chained
-    kernels at 128K;
+  * the decode step at B = 1 (32 q / 8 kv heads) for 32K, 64K and 128K
+    context: the one-launch row-spread kernel (18 CTAs per row, 1824 / 3648 /
+    7296-key slices), and at B = 2 (9 CTAs per row, the default one-launch grid);
   * the chained 128K per-GPU step of configs[2] (B = 8, k = 13107 and 26214);
   * the wide-code (P = 10, 600 bits/token) step and score kernel at B = 16, 32K;
   * bind_host() leaves the cache untouched (its warm-up runs without append).
@@ -112,6 +112,15 @@ def test_one_launch_step_b1_production(N, sparsity):
     # one launch: the row-spread kernel (18 CTAs per row, 1824 .. 7296-key slices)
     assert ops.decode_step_launches(cfg) == 1
     check_rows(dec, cfg, q, K, V, Wb, N, k, [(0, 0), (0, 5), (0, 7)])
+
+
+@pytest.mark.parametrize("sparsity", [10, 5])
+def test_one_launch_step_b2_production(sparsity):
+    N = 32768
+    k = int(round(N / sparsity))
+    dec, cfg, q, K, V, Wb = run(2, N, k, seed=7 + sparsity, lens=[N - 3, N - 2000])
+    assert ops.decode_step_launches(cfg) == 1   # 16 selection rows: the row-spread kernel
+    check_rows(dec, cfg, q, K, V, Wb, N, k, [(0, 1), (1, 6)])
 
 
 @pytest.mark.parametrize("k", [13107, 26214])
