@@ -642,7 +642,11 @@ __device__ __forceinline__ void topk_emit(const TopkArgs& a, uint32_t* keys, Top
     if (tid == 0) a.cnt[row] = (int)k_out;
   }
   TK_TRACE(13);
-  cluster.sync();   // keep shared memory alive until every CTA finished remote reads
+  // keep shared memory alive until every CTA finished its remote reads (their
+  // values are consumed): a relaxed arrive -- the default release arrive would
+  // first drain this CTA's outstanding global idx stores (ncu: membar stalls)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 
 }  // namespace sk
