@@ -208,17 +208,34 @@ __device__ __forceinline__ int sp_select(const uint32_t* keys, int slen, uint32_
                                          int base, uint32_t* s_w, uint32_t* s_w2) {
   constexpr unsigned kFull = 0xffffffffu;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int per = ((slen + kSpWarps - 1) / kSpWarps + 31) & ~31;
+  // warp w owns a contiguous chunk of whole 128-key rows; lane l holds keys
+  // 4 l .. 4 l + 3 of a row (one 16-B load).  Counts are packed (gt | eq << 16;
+  // a chunk holds far fewer than 65536 keys).
+  const int per = ((slen + kSpWarps - 1) / kSpWarps + 127) & ~127;
   const int c0 = warp * per, c1 = min(slen, c0 + per);
-  uint32_t gcount = 0, ecount = 0;
-  for (int i0 = c0; i0 < c1; i0 += 32) {
-    const int li = i0 + lane;
-    const uint32_t key = li < c1 ? keys[li] : 0u;
-    gcount += __popc(__ballot_sync(kFull, key > T && key >= lo && key <= hi));
-    ecount += __popc(__ballot_sync(kFull, key != 0u && key == T));
+  auto load4 = [&](int li, uint32_t (&k)[4]) {
+    if (li + 3 < c1) {
+      const uint4 v = *reinterpret_cast<const uint4*>(keys + li);
+      k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) k[e] = li + e < c1 ? keys[li + e] : 0u;
+    }
+  };
+  auto flags = [&](uint32_t key) -> uint32_t {   // 1: > T inside [lo, hi]; 0x10000: == T
+    return (key > T && key >= lo && key <= hi) ? 1u : ((key != 0u && key == T) ? 0x10000u : 0u);
+  };
+  uint32_t cnt = 0;
+  for (int i0 = c0; i0 < c1; i0 += 128) {
+    uint32_t k[4];
+    load4(i0 + 4 * lane, k);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cnt += flags(k[e]);
   }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
   __syncthreads();   // previous readers of s_w / s_w2
-  if (lane == 0) { s_w[warp] = gcount; s_w2[warp] = ecount; }
+  if (lane == 0) { s_w[warp] = cnt & 0xFFFFu; s_w2[warp] = cnt >> 16; }
   __syncthreads();
   uint32_t gb = 0, eb = 0, gt = 0, et = 0;
 #pragma unroll
@@ -229,20 +246,34 @@ __device__ __forceinline__ int sp_select(const uint32_t* keys, int slen, uint32_
     gt += xg;
     et += xe;
   }
-  const unsigned ltm = (1u << lane) - 1u;
-  for (int i0 = c0; i0 < c1; i0 += 32) {
-    const int li = i0 + lane;
-    const uint32_t key = li < c1 ? keys[li] : 0u;
-    const bool isgt = key > T && key >= lo && key <= hi, iseq = key != 0u && key == T;
-    const unsigned gm = __ballot_sync(kFull, isgt), em = __ballot_sync(kFull, iseq);
-    const uint32_t er = eb + __popc(em & ltm);
-    if (isgt || (iseq && er < eqq)) {
-      const uint32_t p = gb + __popc(gm & ltm) + min(er, eqq);
-      if (list) list[list0 + p] = li;
-      if (orow) orow[pos0 + p] = base + li;
+  for (int i0 = c0; i0 < c1; i0 += 128) {
+    const int li = i0 + 4 * lane;
+    uint32_t k[4], f[4], mine = 0;
+    load4(li, k);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { f[e] = flags(k[e]); mine += f[e]; }
+    uint32_t inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
     }
-    gb += __popc(gm);
-    eb += __popc(em);
+    const uint32_t ex = inc - mine;
+    uint32_t g = gb + (ex & 0xFFFFu), ev = eb + (ex >> 16);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const bool isgt = f[e] == 1u, iseq = f[e] == 0x10000u;
+      if (isgt || (iseq && ev < eqq)) {
+        const uint32_t p = g + min(ev, eqq);
+        if (list) list[list0 + p] = li + e;
+        if (orow) orow[pos0 + p] = base + li + e;
+      }
+      g += isgt ? 1u : 0u;
+      ev += iseq ? 1u : 0u;
+    }
+    const uint32_t tot = __shfl_sync(kFull, inc, 31);
+    gb += tot & 0xFFFFu;
+    eb += tot >> 16;
   }
   __syncthreads();   // the list is read by other warps next
   return (int)(gt + min(et, eqq));
