@@ -103,9 +103,13 @@ def main():
         for s in ([5, 10, 20, 33, 50] if L == 60 and P == 8 else [10, 33]):
             pts.append(point(65536, 4, L, P, s, flush, cache))
             print(json.dumps(pts[-1]), flush=True)
-    for s in (10, 33):   # 1024 bits/token: P = 16 half-tables fit only per query head (R-25)
-        pts.append(point(65536, 4, 64, 16, s, flush, cache, mode=PER_QHEAD))
-        print(json.dumps(pts[-1]), flush=True)
+    # 768 and 1024 bits/token (P = 12, 16): factored half-table lookups (DESIGN 4.6),
+    # both selection modes (KV_SHARED sums G = 4 heads per lookup; PER_QHEAD reads
+    # each code once per query head)
+    for (P, mode) in [(12, KV_SHARED), (16, KV_SHARED), (16, PER_QHEAD)]:
+        for s in (10, 33):
+            pts.append(point(65536, 4, 64, P, s, flush, cache, mode=mode))
+            print(json.dumps(pts[-1]), flush=True)
     # configs[2] per-GPU shard on one GPU: 128K context, B = 8, all 8 KV heads (G = 1)
     for s in (5, 10, 33):
         pts.append(point(131072, 8, 60, 8, s, flush, cache))
