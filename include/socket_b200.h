@@ -237,7 +237,7 @@ socket_status socket_score_lut(const socket_cfg* cfg, const void* lut, const uin
  *     otherwise the caller has written row j already;
  *   then scores (Eq. 4 / Alg. 4, written to `scores`), TopK with sink/window
  *   (idx, cnt as socket_topk) and sparse attention (out, lse as
- *   socket_sparse_decode).  Up to 16 selection rows (KV_SHARED, P <= 8, and
+ *   socket_sparse_decode).  Up to 32 selection rows (KV_SHARED, P <= 8, and
  *   every selection row spread over >= 2 SMs) run as ONE cooperative launch
  *   over all SMs (the row-spread kernel; SOCKET_FLAG_ONE_LAUNCH: whenever the
  *   shape allows); otherwise 4 launches chained with programmatic dependent

@@ -1377,7 +1377,9 @@ socket_status launch_spread_step(const socket_cfg& c, const void* q, void* K, vo
   a.tau = c.tau;
   a.scale_log2 = c.sm_scale * kLog2eM;
   a.S = S;
-  a.tpc = (Lp + C - 1) / C;
+  // tables per CTA, a multiple of 4: the LUT columns are written as float4 groups
+  // starting at table c * tpc (C = 6 once gave 11 -> misaligned 16-B stores)
+  a.tpc = ((Lp + C - 1) / C + 3) & ~3;
   a.nst = spread_stages(Lp, S);
   a.zone = sp_zone(Lp, S, a.nst);
   const size_t sm = spread_smem_bytes(Lp, S, a.nst);

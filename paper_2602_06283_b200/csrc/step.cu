@@ -47,10 +47,11 @@ socket_status launch_spread_step(const socket_cfg& c, const void* q, void* K, vo
                                  float* scores, int32_t* idx, int32_t* cnt, void* out, float* lse,
                                  void* ws, cudaStream_t st);
 
-// one-launch row-spread step (spread.cu): by default up to 16 selection rows
-// (measured crossover with the chained kernels, DESIGN 4.5b: -21..24% at B = 2,
-// equal at B = 4); SOCKET_FLAG_ONE_LAUNCH whenever the shape allows
-constexpr int kSpreadMaxRows = 16;
+// one-launch row-spread step (spread.cu): by default up to 32 selection rows
+// (measured against the chained kernels, DESIGN 4.5b: -21..24% at B = 2, -10% at
+// B = 3 and -5% at B = 4 (32K); larger shapes fall back to the chained kernels by
+// geometry); SOCKET_FLAG_ONE_LAUNCH whenever the shape allows
+constexpr int kSpreadMaxRows = 32;
 bool one_launch_step(const socket_cfg& c) {
   if (c.flags & SOCKET_FLAG_CHAINED_STEP) return false;
   int C, S;

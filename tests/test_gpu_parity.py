@@ -561,6 +561,9 @@ def one_vs_chained(cfg, d, k, sink=0, window=0):
     (2, 32, 8, 4096, 60, [4096, 3001], 0, 0, 0),   # 16 rows (the default one-launch grid), 9 CTAs per row
     (4, 32, 8, 2048, 60, [2048, 77, 2000, 1500], 0, 64, 128),   # 32 rows, 4 CTAs per row
     (1, 32, 8, 16384, 60, [16384], 0, 0, 0),       # 18 CTAs per row (B = 1 production geometry)
+    (3, 32, 8, 4096, 60, [4096, 4000, 3333], 0, 0, 0),   # 24 rows, 6 CTAs per row: ceil(64 / 6) = 11
+    # tables per CTA, rounded to 12 so that the float4 LUT-column stores stay 16-B aligned
+    (5, 32, 8, 2048, 60, [2048, 2048, 1500, 999, 2047], 0, 0, 0),   # 40 rows, 3 CTAs per row
 ])
 def test_one_launch_step_matches_chained(B, H_q, H_kv, N, L, lens, scoring, sink, window):
     """The one-launch row-spread step and the PDL-chained kernels agree on every

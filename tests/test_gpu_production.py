@@ -119,7 +119,7 @@ def test_one_launch_step_b2_production(sparsity):
     N = 32768
     k = int(round(N / sparsity))
     dec, cfg, q, K, V, Wb = run(2, N, k, seed=7 + sparsity, lens=[N - 3, N - 2000])
-    assert ops.decode_step_launches(cfg) == 1   # 16 selection rows: the row-spread kernel
+    assert ops.decode_step_launches(cfg) == 1   # 16 selection rows (<= 32): the row-spread kernel
     check_rows(dec, cfg, q, K, V, Wb, N, k, [(0, 1), (1, 6)])
 
 
