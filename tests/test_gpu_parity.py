@@ -616,7 +616,7 @@ def test_one_launch_selection_modes(case):
         assert a[3][0, 0, :k].cpu().numpy().tolist() == list(range(k))
 
 
-def _random_one_launch_shapes(n_shapes=28, seed=2026):
+def _random_one_launch_shapes(n_shapes=40, seed=2026):
     """Seeded shapes the one-launch kernel accepts, spread over its geometry:
     1..74 selection rows (2..74 CTAs per row), 1/2/4/8 heads per row, L with and
     without 4-table alignment, ragged and empty rows, sink / window."""
@@ -680,3 +680,80 @@ def test_one_launch_random_shapes(B, H_q, H_kv, N, L, lens, sink, window, k):
                         assert abs(float(ls[bb, h]) - lse) <= 1e-3 + 2.0 ** -8
                     else:
                         assert not torch.isfinite(ls[bb, h])
+
+
+def _random_step_cases(n_cases=40, seed=2027):
+    """Seeded decode-step cases over the chained path's geometry: batch 1..16,
+    1..8 KV heads, 1..8 heads per row, both selection modes, N 64..8288, L 1..64,
+    P 1..12 (P > 8: packed wide codes), tau, ragged / empty rows, sink / window,
+    a key mask, any k <= N."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n_cases:
+        NH, H_kv = int(rng.choice([1, 2, 4, 8])), int(rng.choice([1, 2, 4, 8]))
+        B = int(rng.integers(1, 17))
+        N = int(rng.choice([64, 128, 256, 512, 1024, 2048, 4096, 8192])) + 32 * int(rng.integers(0, 4))
+        if B * NH * H_kv * N > 1_500_000:
+            continue
+        mode = PER_QHEAD if rng.random() < 0.25 else KV_SHARED
+        L = int(rng.integers(1, 65))
+        P = int(rng.integers(1, 9)) if rng.random() < 0.8 else int(rng.integers(9, 13))
+        tau = float(rng.choice([0.25, 0.5, 1.0]))
+        lens = [int(rng.integers(0, N + 1)) if rng.random() < 0.4 else N for _ in range(B)]
+        sink, window = (int(rng.integers(0, 8)), int(rng.integers(0, 64))) if rng.random() < 0.3 else (0, 0)
+        k = int(rng.integers(max(1, sink + window), N + 1))
+        masked = bool(rng.random() < 0.3)
+        out.append((B, NH * H_kv, H_kv, N, L, P, mode, tau, lens, sink, window, k, masked))
+    return out
+
+
+@pytest.mark.parametrize("B,H_q,H_kv,N,L,P,mode,tau,lens,sink,window,k,masked", _random_step_cases())
+def test_chained_step_random_cases_vs_oracle(B, H_q, H_kv, N, L, P, mode, tau, lens, sink, window, k, masked):
+    """socket_decode_step through the PDL-chained kernels on seeded random shapes,
+    against the oracle: codes bit-exact up to near-zero projection margins, scores
+    within 1e-5 relative, the selection identical to the oracle's TopK of the
+    GPU's own fp32 scores, attention within the R-28 bound on that selection."""
+    cfg, c, W, d = make(B, H_q, H_kv, N, L, P, seed=1000 + 13 * B + L + P, seq_lens=lens, tau=tau, mode=mode)
+    cfg = chained(cfg)
+    dec = SocketDecoder(cfg, d["W"], d["K"], d["V"], k=k, sink=sink, window=window)
+    dec.prefill()
+    mask = None
+    if masked:
+        g = torch.Generator().manual_seed(B * 7919 + N)
+        mask = (torch.rand((B, N), generator=g) > 0.2).to(torch.uint8).to(DEV)
+    out, lse = dec.step(d["q"], d["seq_lens"], append=True, mask=mask)
+    codes = ops.unpack_codes(cfg, dec.codes).cpu().numpy().astype(np.int64)
+    ref_codes, margin = O.hash_keys(O.widen(c["K"]), O.widen(W))
+    for b, h, l, j in zip(*np.nonzero(codes != ref_codes)):
+        flipped = codes[b, h, l, j] ^ ref_codes[b, h, l, j]
+        assert all(margin[b, h, l, i, j] < 1e-5 for i in range(P) if flipped >> i & 1)
+    ref = O.decode_step(c["q"], c["K"], c["V"], W, c["seq_lens"], tau=tau, k=k, sm_scale=cfg.scale,
+                        group_mode=mode, sink=sink, window=window, codes=codes,
+                        mask=None if mask is None else mask.cpu().numpy())
+    q, K, V = O.widen(c["q"]), O.widen(c["K"]), O.widen(c["V"])
+    sc, idx, cnt = dec.scores.cpu().numpy(), dec.idx.cpu().numpy(), dec.cnt.cpu().numpy()
+    G = H_q // H_kv
+    for b in range(B):
+        n = lens[b]
+        for r in range(cfg.H_sel):
+            s_ref = ref["scores"][(b, r)]
+            fin = np.isfinite(s_ref)
+            assert np.array_equal(np.isfinite(sc[b, r]), fin)
+            if fin.any():
+                assert np.max(rel_err(sc[b, r][fin], s_ref[fin])) <= 1e-5
+            S = idx[b, r, :cnt[b, r]]
+            assert S.tolist() == list(O.topk_select(sc[b, r].astype(np.float64), k, n, sink, window))
+            g = r if mode == KV_SHARED else r // G
+            for h in (range(g * G, (g + 1) * G) if mode == KV_SHARED else [r]):
+                y, l_ref = O.sparse_attention(q[b, h], K[b, g], V[b, g], S, cfg.scale)
+                tol = 2e-3 + 2.0 ** (np.floor(np.log2(np.maximum(np.abs(y), 2.0 ** -126))) - 7)
+                if len(S):
+                    z = cfg.scale * (K[b, g][S] @ q[b, h])
+                    al = np.exp(z - z.max())
+                    al /= al.sum()
+                    tol = tol + 2.0 ** -8 * (al[:, None] * np.abs(V[b, g][S] - y)).sum(axis=0)
+                assert (np.abs(out[b, h].float().cpu().numpy() - y) <= tol).all()
+                if np.isfinite(l_ref):
+                    assert abs(float(lse[b, h]) - l_ref) <= 1e-3 + 2.0 ** -8
+                else:
+                    assert not math.isfinite(float(lse[b, h]))
