@@ -217,3 +217,64 @@ def test_virtual_shards_full_size_heavy_ties():
         assert got[h] == idx_f[0, h, :int(cnt_f[0, h])].tolist()
     ref = O.topk_select(full[0, 2].double().cpu().numpy(), k, N)
     assert got[2] == ref.tolist()
+
+
+def _random_protocol_cases(n_cases=40, seed=4242):
+    """Seeded cases of the exact sequence-shard top-k: 2..8 shards, 32..20000
+    keys per shard, any k (also k > keys per shard), ragged rows that end inside
+    any shard (or are empty), sink / window, four score distributions."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n_cases):
+        G = int(rng.integers(2, 9))
+        Ns = 32 * int(rng.integers(1, 626))
+        N = G * Ns
+        B, H = int(rng.integers(1, 4)), int(rng.choice([1, 2, 4]))
+        lens = [int(rng.integers(0, N + 1)) if rng.random() < 0.5 else N for _ in range(B)]
+        sink, window = (int(rng.integers(0, 16)), int(rng.integers(0, 200))) if rng.random() < 0.4 else (0, 0)
+        k = int(rng.integers(max(1, sink + window), N + 1))
+        kind = str(rng.choice(["gauss", "ties", "outliers", "levels3"]))
+        out.append((G, Ns, B, H, lens, sink, window, k, kind, int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("G,Ns,B,H,lens,sink,window,k,kind,seed", _random_protocol_cases())
+def test_shard_protocol_random_cases(G, Ns, B, H, lens, sink, window, k, kind, seed):
+    """The digest / bracket / window / resolve / emit exchange on seeded random
+    shapes: every shard's share unions to the oracle's Alg. 3 TopK of the whole
+    row (same fp32 scores) and to the single-device socket_topk, in at most 3
+    window rounds."""
+    N = G * Ns
+    cfg = Config(B=B, H_q=H, H_kv=H, N_max=N, L=16, P=8)
+    if kind == "levels3":   # three exact values: massive ties at the threshold
+        g = torch.Generator(device=DEV).manual_seed(seed)
+        full = torch.randint(0, 3, (B * H, N), generator=g, device=DEV).float()
+    else:
+        full = _synthetic(kind, B * H, N, seed)
+    full = full.view(B, H, N).contiguous()
+    lt = torch.tensor(lens, dtype=torch.int32, device=DEV)
+    sc = [seq_shard_config(cfg, G, r) for r in range(G)]
+    parts = [full[:, :, r * Ns:(r + 1) * Ns].contiguous() for r in range(G)]
+    all_d = torch.stack([ops.topk_digest(sc[r], parts[r], lt, k, G, sink=sink, window=window)
+                         for r in range(G)])
+    st = [ops.topk_bracket(sc[r], all_d, k) for r in range(G)]
+    rounds = 0
+    while not all(bool((x[..., 3] != 0).all()) for x in st):
+        all_m = torch.stack([ops.topk_window(sc[r], parts[r], lt, st[r], sink=sink, window=window)
+                             for r in range(G)])
+        for r in range(G):
+            ops.topk_resolve(sc[r], all_m, r, st[r])
+        rounds += 1
+        assert rounds <= 3
+    got = [[[] for _ in range(H)] for _ in range(B)]
+    for r in range(G):
+        idx, cnt = ops.topk_emit(sc[r], parts[r], lt, k, st[r], sink=sink, window=window)
+        for b in range(B):
+            for h in range(H):
+                got[b][h] += (idx[b, h, :int(cnt[b, h])].long() + r * Ns).tolist()
+    idx_f, cnt_f = ops.topk(cfg, full, lt, k, sink, window)
+    for b in range(B):
+        for h in range(H):
+            ref = O.topk_select(full[b, h].double().cpu().numpy(), k, lens[b], sink, window).tolist()
+            assert got[b][h] == ref
+            assert idx_f[b, h, :int(cnt_f[b, h])].tolist() == ref
