@@ -757,3 +757,51 @@ def test_chained_step_random_cases_vs_oracle(B, H_q, H_kv, N, L, P, mode, tau, l
                     assert abs(float(lse[b, h]) - l_ref) <= 1e-3 + 2.0 ** -8
                 else:
                     assert not math.isfinite(float(lse[b, h]))
+
+
+def _random_hash_cases(n_cases=30, seed=31337):
+    """Seeded prefill / append hashing cases: L 1..128, P 1..16, B x H up to 8
+    rows, N up to 3000, 1-3 key ranges each (short ranges take the CUDA-core
+    kernel, >= 128 keys the tcgen05 GEMM; L > 64 the CUDA-core fallback)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n_cases):
+        B, H = int(rng.integers(1, 3)), int(rng.choice([1, 2, 4]))
+        N = 32 * int(rng.integers(1, 94))
+        L = int(rng.choice([1, 3, 8, 16, 31, 33, 60, 64, 100, 128]))
+        P = int(rng.integers(1, 17)) if L <= 64 else int(rng.integers(1, 9))
+        ranges, start = [], 0
+        for _ in range(int(rng.integers(1, 4))):
+            if start >= N:
+                break
+            b0 = int(rng.integers(start, N))
+            cnt = int(rng.integers(1, N - b0 + 1))
+            ranges.append((b0, cnt))
+            start = b0 + cnt
+        out.append((B, H, N, L, P, ranges, int(rng.integers(0, 1 << 20))))
+    return out
+
+
+@pytest.mark.parametrize("B,H,N,L,P,ranges,seed", _random_hash_cases())
+def test_hash_random_ranges_vs_oracle(B, H, N, L, P, ranges, seed):
+    """Alg. 1 codes (and value norms) of seeded random key ranges, bit-exact
+    against the oracle up to near-zero projection margins; keys outside the
+    ranges stay untouched."""
+    cfg, c, W, d = make(B, H, H, N, L, P, seed=seed)
+    codes = ops.alloc_codes(cfg, DEV)
+    vnorm = torch.full((B, H, N), -1.0, dtype=torch.float32, device=DEV)
+    for b0, cnt in ranges:
+        ops.hash_keys(cfg, d["K"], d["W"], codes, V=d["V"], vnorm=vnorm, n_begin=b0, n_count=cnt)
+    got = ops.unpack_codes(cfg, codes).cpu().numpy().astype(np.int64)
+    ref, margin = O.hash_keys(O.widen(c["K"]), O.widen(W))
+    inside = np.zeros(N, bool)
+    for b0, cnt in ranges:
+        inside[b0:b0 + cnt] = True
+    assert np.all(got[..., ~inside] == 0)
+    vn = vnorm.cpu().numpy()
+    assert np.all(vn[..., ~inside] == -1.0)
+    vn_ref = O.value_norms(O.widen(c["V"]))
+    assert np.max(rel_err(vn[..., inside], vn_ref[..., inside])) < 1e-6
+    for b, h, l, j in zip(*np.nonzero((got != ref) & inside)):
+        flipped = got[b, h, l, j] ^ ref[b, h, l, j]
+        assert all(margin[b, h, l, i, j] < 1e-5 for i in range(P) if flipped >> i & 1)
