@@ -805,3 +805,99 @@ def test_hash_random_ranges_vs_oracle(B, H, N, L, P, ranges, seed):
     for b, h, l, j in zip(*np.nonzero((got != ref) & inside)):
         flipped = got[b, h, l, j] ^ ref[b, h, l, j]
         assert all(margin[b, h, l, i, j] < 1e-5 for i in range(P) if flipped >> i & 1)
+
+
+def _random_topk_cases(n_cases=30, seed=777):
+    """Seeded socket_topk cases over its cluster geometries: 1..130 rows, rows of
+    32..700000 keys (slices in shared memory up to 16 x 40960 keys, beyond in the
+    workspace), any k, ragged / empty rows, sink / window, ties."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n_cases:
+        big = rng.random() < 0.15
+        N = 32 * int(rng.integers(20480, 21900)) if big else 32 * int(rng.integers(1, 2049))
+        B = 1 if big else int(rng.integers(1, 17))
+        H = 1 if big else int(rng.choice([1, 2, 4, 8]))
+        if B * H * N > 3_000_000:
+            continue
+        lens = [int(rng.integers(0, N + 1)) if rng.random() < 0.4 else N for _ in range(B)]
+        sink, window = (int(rng.integers(0, 16)), int(rng.integers(0, 300))) if rng.random() < 0.3 else (0, 0)
+        k = int(rng.integers(max(1, sink + window), N + 1))
+        kind = str(rng.choice(["gauss", "ties", "levels2"]))
+        out.append((B, H, N, lens, sink, window, k, kind, int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("B,H,N,lens,sink,window,k,kind,seed", _random_topk_cases())
+def test_topk_random_cases(B, H, N, lens, sink, window, k, kind, seed):
+    """socket_topk on seeded random shapes equals the oracle's Alg. 3 TopK of the
+    same fp32 scores (ties to the smaller index, forced sink / window first),
+    and the -1 padding past cnt."""
+    cfg = Config(B=B, H_q=H, H_kv=H, N_max=N, L=16, P=8)
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    if kind == "gauss":
+        s = torch.randn((B, H, N), generator=g, device=DEV)
+    elif kind == "ties":
+        s = torch.randint(0, 50, (B, H, N), generator=g, device=DEV).float() * 0.25
+    else:
+        s = torch.randint(0, 2, (B, H, N), generator=g, device=DEV).float()
+    lt = torch.tensor(lens, dtype=torch.int32, device=DEV)
+    idx, cnt = ops.topk(cfg, s, lt, k, sink, window)
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            ref = O.topk_select(s[b, h].double().cpu().numpy(), k, lens[b], sink, window)
+            assert idx[b, h, :cnt[b, h]].tolist() == ref.tolist()
+            assert np.all(idx[b, h, cnt[b, h]:] == -1)
+
+
+def _random_sparse_cases(n_cases=24, seed=99):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n_cases:
+        NH, H_kv = int(rng.choice([1, 2, 4, 8])), int(rng.choice([1, 2, 4, 8]))
+        B = int(rng.integers(1, 9))
+        N = 32 * int(rng.integers(1, 257))
+        if B * NH * H_kv * N > 2_000_000:
+            continue
+        mode = PER_QHEAD if rng.random() < 0.3 else KV_SHARED
+        k = int(rng.integers(1, N + 1))
+        out.append((B, NH * H_kv, H_kv, N, mode, k, int(rng.integers(0, 1 << 20))))
+    return out
+
+
+@pytest.mark.parametrize("B,H_q,H_kv,N,mode,k,seed", _random_sparse_cases())
+def test_sparse_decode_random_selections(B, H_q, H_kv, N, mode, k, seed):
+    """socket_sparse_decode (and its fused split merge) on seeded random
+    selections -- random subsets of any size up to k per row, empty rows, -1
+    padding -- against the oracle's Eq. 2 (R-28 bound)."""
+    cfg, c, W, d = make(B, H_q, H_kv, N, 16, 8, seed=seed, mode=mode)
+    rng = np.random.default_rng(seed)
+    H_sel = cfg.H_sel
+    idx = np.full((B, H_sel, k), -1, np.int32)
+    cnt = np.zeros((B, H_sel), np.int32)
+    for b in range(B):
+        for r in range(H_sel):
+            m = 0 if rng.random() < 0.1 else int(rng.integers(1, k + 1))
+            idx[b, r, :m] = np.sort(rng.choice(N, m, replace=False))
+            cnt[b, r] = m
+    out, lse = ops.sparse_decode(cfg, d["q"], d["K"], d["V"], torch.from_numpy(idx).to(DEV),
+                                 torch.from_numpy(cnt).to(DEV), k)
+    q, K, V = O.widen(c["q"]), O.widen(c["K"]), O.widen(c["V"])
+    G = H_q // H_kv
+    for b in range(B):
+        for h in range(H_q):
+            g, r = h // G, (h // G if mode == KV_SHARED else h)
+            S = idx[b, r, :cnt[b, r]]
+            y, l_ref = O.sparse_attention(q[b, h], K[b, g], V[b, g], S, cfg.scale)
+            tol = 2e-3 + 2.0 ** (np.floor(np.log2(np.maximum(np.abs(y), 2.0 ** -126))) - 7)
+            if len(S):
+                z = cfg.scale * (K[b, g][S] @ q[b, h])
+                al = np.exp(z - z.max())
+                al /= al.sum()
+                tol = tol + 2.0 ** -8 * (al[:, None] * np.abs(V[b, g][S] - y)).sum(axis=0)
+            assert (np.abs(out[b, h].float().cpu().numpy() - y) <= tol).all()
+            if np.isfinite(l_ref):
+                assert abs(float(lse[b, h]) - l_ref) <= 1e-3 + 2.0 ** -8
+            else:
+                assert not math.isfinite(float(lse[b, h]))
