@@ -145,3 +145,52 @@ def test_wide_decode_step_end_to_end(mode, L, P):
         S = idx[0, r, :cnt[0, r]]
         y, _ = O.sparse_attention(q[0, h], K[0, h // G], V[0, h // G], S, cfg.scale)
         assert np.max(np.abs(out[0, h].float().cpu().numpy() - y)) <= 2e-3
+
+
+def _random_score_cases(n_cases=30, seed=5150):
+    """Seeded socket_score cases: P 1..16 (byte and packed codes), L 1..64, both
+    selection modes, 1..8 heads per row, tau, ragged / empty rows, a key mask."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n_cases:
+        NH, H_kv = int(rng.choice([1, 2, 4, 8])), int(rng.choice([1, 2, 4]))
+        B = int(rng.integers(1, 4))
+        N = 32 * int(rng.integers(1, 97))
+        L, P = int(rng.integers(1, 65)), int(rng.integers(1, 17))
+        mode = PER_QHEAD if rng.random() < 0.3 else KV_SHARED
+        if B * NH * H_kv * N * (1 << max(0, P - 8)) > 4_000_000:
+            continue
+        lens = [int(rng.integers(0, N + 1)) if rng.random() < 0.4 else N for _ in range(B)]
+        out.append((B, NH * H_kv, H_kv, N, L, P, mode, float(rng.choice([0.25, 0.5, 1.0])), lens,
+                    bool(rng.random() < 0.3), int(rng.integers(0, 1 << 20))))
+    return out
+
+
+@pytest.mark.parametrize("B,H_q,H_kv,N,L,P,mode,tau,lens,masked,seed", _random_score_cases())
+def test_score_random_cases(B, H_q, H_kv, N, L, P, mode, tau, lens, masked, seed):
+    """Eq. 4 scores of seeded random configurations (every score kernel: byte
+    codes, group-summed P <= 10, factored P >= 11, tiled KV_SHARED images) within
+    1e-5 relative of the oracle's, -inf exactly where the oracle has it."""
+    cfg, c, W, d = make(B, H_q, H_kv, N, L, P, seed, mode=mode, lens=lens, tau=tau)
+    codes_ref, _ = O.hash_keys(O.widen(c["K"]), O.widen(W))
+    plain_codes = codes_ref.astype(np.uint8) if P <= 8 else codes_ref.astype(np.uint16).view(np.int16)
+    codes = ops.pack_codes(cfg, torch.from_numpy(plain_codes).to(DEV))
+    vn_ref = O.value_norms(O.widen(c["V"]))
+    vnorm = torch.from_numpy(vn_ref.astype(np.float32)).to(DEV)
+    mask = None
+    if masked:
+        mask = (torch.rand((B, N), generator=torch.Generator().manual_seed(seed)) > 0.25).to(torch.uint8)
+    got = ops.score(cfg, d["q"], d["W"], codes, vnorm, d["seq_lens"],
+                    mask=None if mask is None else mask.to(DEV)).cpu().numpy()
+    T = O.selection_tables(O.widen(c["q"]), O.widen(W), tau, H_kv, mode)
+    G = H_q // H_kv
+    for b in range(B):
+        for r in range(cfg.H_sel):
+            g = r if mode == KV_SHARED else r // G
+            w = O.soft_scores(T[b, r], codes_ref[b, g])
+            s = O.masked_value_scores(w, vn_ref[b, g].astype(np.float32).astype(np.float64), lens[b],
+                                      None if mask is None else mask[b].numpy())
+            fin = np.isfinite(s)
+            assert np.array_equal(np.isfinite(got[b, r]), fin)
+            if fin.any():
+                assert np.max(rel_err(got[b, r][fin], s[fin])) <= 1e-5
