@@ -901,3 +901,37 @@ def test_sparse_decode_random_selections(B, H_q, H_kv, N, mode, k, seed):
                 assert abs(float(lse[b, h]) - l_ref) <= 1e-3 + 2.0 ** -8
             else:
                 assert not math.isfinite(float(lse[b, h]))
+
+
+@pytest.mark.parametrize("B,H_q,H_kv,N,L,lens,sink,window,k", _random_one_launch_shapes(16, seed=9091))
+def test_one_launch_random_shapes_new_rows(B, H_q, H_kv, N, L, lens, sink, window, k):
+    """The same geometries with the new token's K/V rows passed to the step
+    (k_new / v_new): the one-launch kernel stores them into the cache at
+    seq_lens[b] - 1 exactly as the chained kernels do, and every output agrees."""
+    import dataclasses
+    cfg, c, W, d = make(B, H_q, H_kv, N, L, 8, seed=11 * B + L, seq_lens=lens)
+    g = torch.Generator(device=DEV).manual_seed(B * 31 + L)
+    k_new = torch.randn((B, H_kv, 128), generator=g, device=DEV).to(torch.bfloat16)
+    v_new = torch.randn((B, H_kv, 128), generator=g, device=DEV).to(torch.bfloat16)
+    res = []
+    for flags in (_lib.FLAG_ONE_LAUNCH, _lib.FLAG_CHAINED_STEP):
+        cf = dataclasses.replace(cfg, flags=flags)
+        dec = SocketDecoder(cf, d["W"], d["K"].clone(), d["V"].clone(), k=k, sink=sink, window=window)
+        dec.prefill()
+        out, lse = dec.step(d["q"], d["seq_lens"], append=True, k_new=k_new, v_new=v_new)
+        res.append([t.clone() for t in (dec.K, dec.V, dec.codes, dec.vnorm, dec.scores, dec.idx, dec.cnt,
+                                         out, lse)])
+    a, b = res
+    for x, y in zip(a[:7], b[:7]):
+        assert torch.equal(x, y)
+    for bb in range(B):
+        if 0 < lens[bb] <= N:
+            assert torch.equal(a[0][bb, :, lens[bb] - 1], k_new[bb])
+            assert torch.equal(a[1][bb, :, lens[bb] - 1], v_new[bb])
+    ya, yb = a[7].float(), b[7].float()
+    mag = torch.maximum(ya.abs(), yb.abs()).clamp_min(2.0 ** -126)
+    # two correct paths: each within the R-28 bound of Eq. 2, so at most twice apart
+    assert ((ya - yb).abs() <= 4e-3 + 2 * torch.exp2(torch.floor(torch.log2(mag)) - 7) + 2.0 ** -7 * mag).all()
+    fin = torch.isfinite(b[8])
+    assert torch.equal(torch.isfinite(a[8]), fin)
+    assert ((a[8][fin] - b[8][fin]).abs() <= 2e-3 + 2.0 ** -7).all()
