@@ -935,3 +935,54 @@ def test_one_launch_random_shapes_new_rows(B, H_q, H_kv, N, L, lens, sink, windo
     fin = torch.isfinite(b[8])
     assert torch.equal(torch.isfinite(a[8]), fin)
     assert ((a[8][fin] - b[8][fin]).abs() <= 2e-3 + 2.0 ** -7).all()
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_partials_and_lse_combine_random_splits(case):
+    """A row's selection split at random over G = 2..8 disjoint parts (as the
+    sequence shards split it): socket_sparse_decode's partial states of each
+    part, merged by socket_lse_combine, equal the oracle's Eq. 2 over the union
+    (R-28 bound); empty parts and empty rows included."""
+    rng = np.random.default_rng(600 + case)
+    G = int(rng.integers(2, 9))
+    B, H_kv, NH = int(rng.integers(1, 4)), int(rng.choice([1, 2, 4])), int(rng.choice([1, 2, 4, 8]))
+    N = 32 * int(rng.integers(2, 200))
+    mode = PER_QHEAD if rng.random() < 0.3 else KV_SHARED
+    cfg, c, W, d = make(B, NH * H_kv, H_kv, N, 16, 8, seed=700 + case, mode=mode)
+    k = int(rng.integers(1, N + 1))
+    H_sel = cfg.H_sel
+    owner = rng.integers(0, G, size=(B, H_sel, N))
+    sel = [[np.sort(rng.choice(N, 0 if rng.random() < 0.1 else int(rng.integers(1, k + 1)), replace=False))
+            for _ in range(H_sel)] for _ in range(B)]
+    parts = []
+    for s in range(G):
+        idx = np.full((B, H_sel, k), -1, np.int32)
+        cnt = np.zeros((B, H_sel), np.int32)
+        for b in range(B):
+            for r in range(H_sel):
+                mine = [j for j in sel[b][r] if owner[b, r, j] == s]
+                idx[b, r, :len(mine)] = mine
+                cnt[b, r] = len(mine)
+        part = torch.empty((B, cfg.H_q, 130), dtype=torch.float32, device=DEV)
+        ops.sparse_decode(cfg, d["q"], d["K"], d["V"], torch.from_numpy(idx).to(DEV), torch.from_numpy(cnt).to(DEV),
+                          k, partial=part, want_out=False)
+        parts.append(part)
+    out, lse = ops.lse_combine(cfg, torch.stack(parts))
+    q, K, V = O.widen(c["q"]), O.widen(c["K"]), O.widen(c["V"])
+    G_h = cfg.H_q // H_kv
+    for b in range(B):
+        for h in range(cfg.H_q):
+            g = h // G_h
+            S = sel[b][g if mode == KV_SHARED else h]
+            y, l_ref = O.sparse_attention(q[b, h], K[b, g], V[b, g], S, cfg.scale)
+            tol = 2e-3 + 2.0 ** (np.floor(np.log2(np.maximum(np.abs(y), 2.0 ** -126))) - 7)
+            if len(S):
+                z = cfg.scale * (K[b, g][S] @ q[b, h])
+                al = np.exp(z - z.max())
+                al /= al.sum()
+                tol = tol + 2.0 ** -8 * (al[:, None] * np.abs(V[b, g][S] - y)).sum(axis=0)
+            assert (np.abs(out[b, h].float().cpu().numpy() - y) <= tol).all()
+            if np.isfinite(l_ref):
+                assert abs(float(lse[b, h]) - l_ref) <= 1e-3 + 2.0 ** -8
+            else:
+                assert not math.isfinite(float(lse[b, h]))
