@@ -64,7 +64,10 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 //                    (double-buffered by tile), releases the slot; after a tile the
 //                    16 warps copy the staging tile out with 16-byte stores.
 // ----------------------------------------------------------------------------
-constexpr int kEpiWarps = 16;
+#ifndef SK_EPI_WARPS
+#define SK_EPI_WARPS 20
+#endif
+constexpr int kEpiWarps = SK_EPI_WARPS;   // a multiple of 4 (one group per TMEM lane quadrant)
 constexpr int kTc2Threads = 64 + kEpiWarps * 32;   // producer warp, MMA warp, epilogue warps
 constexpr int kColSplit = kEpiWarps / 4;            // epilogue warps per TMEM lane quadrant
 
@@ -199,7 +202,11 @@ hash_keys_tc2_kernel(const __grid_constant__ CUtensorMap tmK, const uint16_t* __
     const int r = qd * 32 + lane;                                // key row of this thread
     constexpr int MM = (LP < 32 ? LP : 32) - 1;
     constexpr int PART = MMA_N / kColSplit;                      // columns per warp and chunk
+#if SK_EPI_WARPS == 16
     constexpr int GROUPS = PART >= 32 ? PART / 32 : 1;           // x32 loads per warp and chunk
+#else
+    constexpr int GROUPS = ((MMA_N >= 32 ? MMA_N / 32 : 1) + kColSplit - 1) / kColSplit;
+#endif
     int it = 0, c = 0;
     for (long long t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       const int bh = (int)(t / tiles_in_range), tile = t_lo + (int)(t % tiles_in_range);
@@ -210,8 +217,20 @@ hash_keys_tc2_kernel(const __grid_constant__ CUtensorMap tmK, const uint16_t* __
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
         for (int g = 0; g < GROUPS; ++g) {
+#if SK_EPI_WARPS == 16
           const int col = PART >= 32 ? cpart * PART + g * 32 : cpart * 32;   // within the chunk
           if (col >= MMA_N) break;                               // narrow chunks: fewer busy warps
+#else
+          // 32-column groups of the whole tile dealt round-robin to the quadrant's
+          // kColSplit warps: tile group gg = h * (MMA_N / 32) + col / 32
+          constexpr int GPC = MMA_N >= 32 ? MMA_N / 32 : 1;     // groups per chunk
+          int gg0 = h * GPC;
+          gg0 += ((cpart - gg0) % kColSplit + kColSplit) % kColSplit;   // first tile group of mine in chunk h
+          const int gg = gg0 + g * kColSplit;
+          if (gg >= (h + 1) * GPC) break;
+          const int col = (gg - h * GPC) * 32;
+          if (col >= MMA_N) break;
+#endif
           uint32_t v[32];
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -228,9 +247,17 @@ hash_keys_tc2_kernel(const __grid_constant__ CUtensorMap tmK, const uint16_t* __
           // 31 - c), inverted (bit = x >= 0) and bit-reversed: byte qq = the code
           // of table lb + qq (bit i = (x_i >= 0), i < P; padding tables >= L -> 0),
           // staged as one word in TABLE order (the copy-out applies the slot rotation)
-          uint32_t sg = 0;
+          // four independent 8-column funnel-shift chains (dependency depth 8 + 2;
+          // one 32-deep chain measured 0.452 vs 0.448 ms at the bench cache)
+          uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
 #pragma unroll
-          for (int c = 0; c < 32; ++c) sg = __funnelshift_l(v[c], sg, 1);
+          for (int c = 0; c < 8; ++c) {
+            q0 = __funnelshift_l(v[c], q0, 1);
+            q1 = __funnelshift_l(v[8 + c], q1, 1);
+            q2 = __funnelshift_l(v[16 + c], q2, 1);
+            q3 = __funnelshift_l(v[24 + c], q3, 1);
+          }
+          const uint32_t sg = __byte_perm(__byte_perm(q3, q2, 0x0040), __byte_perm(q1, q0, 0x0040), 0x5410);
           const int lb = (h * MMA_N + col) / 8;
           const uint32_t lmask = lb + 4 <= L ? 0xFFFFFFFFu : (lb >= L ? 0u : (0xFFFFFFFFu >> (8 * (lb + 4 - L))));
           stg[r * RS + (lb >> 2)] = __brev(~sg) & (((1u << P) - 1u) * 0x01010101u) & lmask;
