@@ -119,3 +119,42 @@ def test_ranking_harness_soft_beats_hard():
     for k in ks:
         for key in ("precision", "jaccard", "ndcg"):
             assert res["soft"][k][key] > res["hard"][k][key], (k, key, res["soft"][k], res["hard"][k])
+
+
+def _random_hard_cases(n_cases=20, seed=1234):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n_cases):
+        NH, H_kv = int(rng.choice([1, 2, 4, 8])), int(rng.choice([1, 2, 4]))
+        B = int(rng.integers(1, 4))
+        N = 32 * int(rng.integers(1, 129))
+        mode = PER_QHEAD if rng.random() < 0.3 else KV_SHARED
+        lens = [int(rng.integers(0, N + 1)) if rng.random() < 0.4 else N for _ in range(B)]
+        k = int(rng.integers(1, N + 1))
+        out.append((B, NH * H_kv, H_kv, N, int(rng.integers(1, 65)), int(rng.integers(1, 9)), mode, lens, k,
+                    int(rng.integers(0, 1 << 20))))
+    return out
+
+
+@pytest.mark.parametrize("B,H_q,H_kv,N,L,P,mode,lens,k,seed", _random_hard_cases())
+def test_hard_scores_random_cases(B, H_q, H_kv, N, L, P, mode, lens, k, seed):
+    """Eq. 3 collision counts x ||v|| on seeded random shapes: bit-exact against
+    the oracle after its one fp32 rounding, and the top-k over these massively
+    tied scores identical to the oracle's TopK (ties to the smaller index)."""
+    cfg, c, W, d = make(B, H_q, H_kv, N, L, P, seed, mode, lens=lens)
+    codes_ref, _ = O.hash_keys(O.widen(c["K"]), O.widen(W))
+    codes = ops.pack_codes(cfg, torch.from_numpy(codes_ref.astype(np.uint8)).to(DEV))
+    vn = O.value_norms(O.widen(c["V"])).astype(np.float32)
+    got = ops.score(cfg, d["q"], d["W"], codes, torch.from_numpy(vn).to(DEV), d["seq_lens"]).cpu().numpy()
+    T = O.selection_tables_hard(O.widen(c["q"]), O.widen(W), H_kv, mode)
+    idx, cnt = ops.topk(cfg, torch.from_numpy(got).to(DEV), d["seq_lens"], k)
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    G = H_q // H_kv
+    for b in range(B):
+        for r in range(cfg.H_sel):
+            g = r if mode == KV_SHARED else r // G
+            w = O.soft_scores(T[b, r], codes_ref[b, g])
+            s32 = O.masked_value_scores(w, vn[b, g].astype(np.float64), lens[b]).astype(np.float32)
+            assert np.array_equal(got[b, r], s32)
+            S = O.topk_select(s32.astype(np.float64), k, lens[b])
+            assert cnt[b, r] == len(S) and np.array_equal(idx[b, r, :cnt[b, r]], S)
